@@ -1,0 +1,148 @@
+/*
+ * pa.h -- C ABI of libpa: bit-exact Toeplitz-hash privacy amplification on
+ * NVIDIA B200 (sm_100a).
+ *
+ * The operation (PAPER.md = arXiv 1805.02372, lines cited as P:L):
+ *   Alice draws a uniform seed of n+l-1 bits, builds the Toeplitz matrix T
+ *   from it and computes r = u T; Bob computes the same with his copy of the
+ *   corrected key (Sec. 2.3 Steps 1-2).  T is diagonal-constant
+ *   (Sec. 2.1, Eq. (1)) and need not be square.  Written as a
+ *   matrix-vector product over GF(2) with m = l output bits:
+ *
+ *       y[i] = XOR_{j=0}^{n-1} s[i - j + n - 1] AND x[j],   0 <= i < m,
+ *
+ *   i.e. T[i][j] = s[i-j+n-1] (readings R1, R2).  Equivalently y
+ *   is the window [n-1, n+m-1) of the integer convolution x * s reduced
+ *   mod 2 -- the paper's Sec. 3 Step 3 "results of IFFT from the nth to
+ *   (n+k-1)th".
+ *
+ * Bit strings: LSB-first.  Bit b of a string lives in uint32 word b/32 at
+ * bit position b%32 (identical bits to uint64 word b/64, bit b%64, and to
+ * bytes, on little-endian).  Lengths are always in bits.
+ *
+ * Memory: every key/seed/out pointer of pa_create... and pa_hash... is a DEVICE
+ * pointer on the handle's device (e.g. a torch CUDA tensor's data_ptr()),
+ * 16-byte aligned.  Host pointers are rejected with PA_ERR_INVALID_ARG.
+ * pa_hash_host is the one entry point that takes HOST buffers.
+ *
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  pa_create... and pa_hash... only enqueue work; results are ready
+ * when the stream reaches them.  One hash in flight per handle (the handle
+ * owns scratch); use one handle per stream for concurrency.
+ *
+ * Errors: every call returns a pa_status; no C++ exception crosses the ABI.
+ * pa_last_error() returns a thread-local message naming the offending field
+ * and values of the most recent failing call on this thread.
+ */
+#ifndef PA_H
+#define PA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PA_VERSION 100u /* 1.0.0 */
+
+typedef struct pa_ctx *pa_handle;
+
+typedef enum pa_status {
+    PA_OK = 0,
+    PA_ERR_INVALID_ARG = 1, /* n == 0, m == 0, m > n, NULL/unaligned/host pointer, bad option */
+    PA_ERR_UNSUPPORTED = 2, /* lengths beyond what the chosen route can plan */
+    PA_ERR_NOMEM = 3,       /* device allocation failed */
+    PA_ERR_CUDA = 4,        /* a CUDA runtime call or launch failed (message has the CUDA error) */
+    PA_ERR_PRECISION = 5    /* FP64 route: max |v - rint(v)| over the output window exceeded
+                               PA_RESIDUAL_LIMIT (never expected; see DESIGN.md error bound) */
+} pa_status;
+
+/* Route (a): exact convolution by an FP64 transform of length N >= n+m-1
+ * with a proven < 0.5 rounding bound.
+ * Route (b): bit-packed direct GF(2) product (AND/XOR/popcount), O(n m).
+ * AUTO picks (b) for small n*m and (a) otherwise. */
+typedef enum pa_route {
+    PA_ROUTE_AUTO = 0,
+    PA_ROUTE_TRANSFORM = 1,
+    PA_ROUTE_BITPACKED = 2
+} pa_route;
+
+#define PA_RESIDUAL_LIMIT 0.25
+
+typedef struct pa_options {
+    uint32_t struct_size;     /* sizeof(pa_options); set by pa_options_init */
+    int32_t route;            /* pa_route */
+    uint64_t seed_bit_offset; /* the handle uses seed bits [off, off+n+m-1) of the
+                                 caller's seed buffer (row/column shards) */
+    uint32_t reserved[8];     /* must be zero */
+} pa_options;
+
+/* Runtime facts about a handle (all lengths in bits or elements). */
+typedef struct pa_info {
+    uint64_t n, m;            /* key bits, output bits */
+    int32_t route;            /* PA_ROUTE_TRANSFORM or PA_ROUTE_BITPACKED */
+    int32_t device;
+    uint64_t transform_len;   /* route (a): real transform length N = 2*M (0 for route b) */
+    uint64_t n1, n2;          /* route (a): complex length M = n1 * n2 (row x column split) */
+    uint64_t cols_per_cta;    /* route (a): columns per CTA in the strided passes */
+    uint64_t workspace_bytes; /* device bytes owned by the handle */
+    uint64_t kernels_per_hash;/* kernel launches enqueued by one pa_hash */
+} pa_info;
+
+/* Fill *opt with defaults (route AUTO, offset 0, residual recorded). */
+pa_status pa_options_init(pa_options *opt);
+
+/* Create a hashing context for n-bit keys and m-bit outputs with the
+ * (n+m-1)-bit seed at `seed_bits` (device, ceil((off+n+m-1)/32) uint32 words
+ * readable).  Requires 1 <= m <= n (SPEC reading R7).  The seed is consumed
+ * on `stream` during create (route (a) transforms it once into a cached
+ * spectrum; route (b) stores it bit-reversed); the caller may free it after
+ * the stream passes this call.  On success *h owns all device memory it
+ * needs; on failure *h is NULL. */
+pa_status pa_create(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits,
+                    void *stream);
+pa_status pa_create_ex(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits,
+                       const pa_options *opt, void *stream);
+
+/* y = T x.  key_bits: device, ceil(n/32) uint32 words; bits >= n are ignored.
+ * out_bits: device, ceil(m/32) uint32 words; every bit >= m is written 0.
+ * Deterministic, bit-exact, stream-ordered, asynchronous. */
+pa_status pa_hash(pa_handle h, const uint32_t *key_bits, uint32_t *out_bits, void *stream);
+
+/* count keys against the same seed.  Key k at keys + k*key_stride_words,
+ * output k at outs + k*out_stride_words (strides in uint32 words, at least
+ * ceil(n/32) and ceil(m/32)).  Output order = input order. */
+pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_words,
+                        uint32_t *outs, uint64_t out_stride_words, uint32_t count,
+                        void *stream);
+
+/* End-to-end variant with HOST buffers (pinned memory recommended): copies the
+ * key host->device, hashes, copies the output device->host, and synchronises
+ * the stream before returning. key_host: ceil(n/32) words; out_host: ceil(m/32). */
+pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream);
+
+/* uint64-packed aliases (same bits on little-endian).  pa_hash_u64 writes all
+ * ceil(m/64) output words, zero-filling the half-word past ceil(m/32). */
+pa_status pa_create_u64(pa_handle *h, uint64_t n, uint64_t m, const uint64_t *seed_bits,
+                        void *stream);
+pa_status pa_hash_u64(pa_handle h, const uint64_t *key_bits, uint64_t *out_bits, void *stream);
+
+/* Route (a): synchronises `stream`, returns the largest |v - rint(v)| seen over
+ * output-window values since the previous call (0 for route b), and resets it.
+ * Returns PA_ERR_PRECISION if it exceeded PA_RESIDUAL_LIMIT. */
+pa_status pa_residual(pa_handle h, double *max_residual, void *stream);
+
+pa_status pa_get_info(pa_handle h, pa_info *info);
+
+/* Stream-ordered release of everything the handle owns.  Safe on NULL. */
+void pa_destroy(pa_handle h);
+
+const char *pa_last_error(void);
+const char *pa_status_string(pa_status s);
+uint32_t pa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PA_H */

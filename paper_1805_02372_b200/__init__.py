@@ -1,0 +1,137 @@
+"""paper_1805_02372_b200 -- bit-exact Toeplitz-hash privacy amplification on B200.
+
+The hot path of arXiv 1805.02372 (length-compatible privacy amplification for
+CV-QKD): y = T x over GF(2), T the m x n Toeplitz matrix of an (n+m-1)-bit
+seed, x the n-bit corrected key (Sec. 2.1 Eq. (1), Sec. 2.3, Sec. 3).
+All arithmetic runs in the sm_100a kernels of ``libpa.so`` (C ABI in
+``include/pa.h``); this package only marshals torch CUDA tensors into it.
+
+    import torch, paper_1805_02372_b200 as pa
+    h = pa.Hasher(n, m, seed_words_cuda)     # pa_create
+    y = h.hash(key_words_cuda)               # pa_hash -> int32 words, LSB-first
+    h.close()                                # pa_destroy
+
+Bit strings are LSB-first in 32-bit words (any integer dtype is accepted; its
+bytes are reinterpreted).  torch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import torch  # loads the CUDA runtime that libpa.so binds to
+
+from . import _lib
+from ._lib import (PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISION,  # noqa: F401
+                   PA_ERR_UNSUPPORTED, PA_OK, PA_RESIDUAL_LIMIT, PA_ROUTE_AUTO, PA_ROUTE_BITPACKED,
+                   PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
+                   pa_get_info, pa_hash, pa_hash_batch, pa_hash_host, pa_hash_u64, pa_last_error,
+                   pa_options_init, pa_residual, pa_status_string, pa_version)
+
+ROUTES = {"auto": PA_ROUTE_AUTO, "transform": PA_ROUTE_TRANSFORM, "bitpacked": PA_ROUTE_BITPACKED}
+
+
+def words32(nbits: int) -> int:
+    return (nbits + 31) // 32
+
+
+def _nbits(t: torch.Tensor) -> int:
+    return t.numel() * t.element_size() * 8
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _need_cuda(t: torch.Tensor, name: str, nbits: int) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (use Hasher.hash_host for host buffers)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if _nbits(t) < nbits:
+        raise ValueError(f"{name} holds {_nbits(t)} bits, {nbits} required")
+
+
+class Hasher:
+    """One pa_handle: fixed (n, m, seed); hash any number of n-bit keys."""
+
+    def __init__(self, n: int, m: int, seed: torch.Tensor, route: str = "auto",
+                 seed_bit_offset: int = 0, stream=None):
+        _need_cuda(seed, "seed", seed_bit_offset + n + m - 1)
+        self.n, self.m = int(n), int(m)
+        self.device = seed.device
+        opt = pa_options_init()
+        opt.route = ROUTES[route]
+        opt.seed_bit_offset = int(seed_bit_offset)
+        with torch.cuda.device(self.device):
+            self._h = pa_create_ex(self.n, self.m, seed.data_ptr(), opt, _stream_ptr(stream))
+        self.info = pa_get_info(self._h)
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    @property
+    def route(self) -> str:
+        return {PA_ROUTE_TRANSFORM: "transform", PA_ROUTE_BITPACKED: "bitpacked"}[self.info["route"]]
+
+    def new_out(self, count: int | None = None) -> torch.Tensor:
+        w = words32(self.m)
+        w4 = (w + 3) // 4 * 4
+        shape = (w4,) if count is None else (count, w4)
+        return torch.empty(shape, dtype=torch.int32, device=self.device)
+
+    def hash(self, key: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        _need_cuda(key, "key", self.n)
+        if out is None:
+            out = self.new_out()
+        _need_cuda(out, "out", self.m)
+        with torch.cuda.device(self.device):
+            pa_hash(self._h, key.data_ptr(), out.data_ptr(), _stream_ptr(stream))
+        return out
+
+    def hash_batch(self, keys: torch.Tensor, outs: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """keys: (count, words) CUDA tensor, one key per row."""
+        if keys.dim() != 2:
+            raise ValueError("keys must be 2-D (count, words)")
+        count = keys.shape[0]
+        if outs is None:
+            outs = self.new_out(count)
+        _need_cuda(keys, "keys", self.n * count)
+        _need_cuda(outs, "outs", self.m * count)
+        kstride = keys.stride(0) * keys.element_size() // 4
+        ostride = outs.stride(0) * outs.element_size() // 4
+        with torch.cuda.device(self.device):
+            pa_hash_batch(self._h, keys.data_ptr(), kstride, outs.data_ptr(), ostride, count,
+                          _stream_ptr(stream))
+        return outs
+
+    def hash_host(self, key_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> torch.Tensor:
+        """End-to-end: host (preferably pinned) key in, host output words out."""
+        if key_host.is_cuda or out_host.is_cuda:
+            raise ValueError("hash_host takes CPU tensors")
+        if _nbits(key_host) < self.n or _nbits(out_host) < 32 * words32(self.m):
+            raise ValueError("host buffers too small")
+        with torch.cuda.device(self.device):
+            pa_hash_host(self._h, key_host.data_ptr(), out_host.data_ptr(), _stream_ptr(stream))
+        return out_host
+
+    def residual(self, stream=None) -> float:
+        with torch.cuda.device(self.device):
+            return pa_residual(self._h, _stream_ptr(stream))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            pa_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

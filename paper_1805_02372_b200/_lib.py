@@ -1,0 +1,159 @@
+"""ctypes binding of libpa.so (include/pa.h).  Argument marshalling only.
+
+Every function below has the name and argument order of its C counterpart;
+pointers are passed as Python ints (e.g. ``tensor.data_ptr()``) and streams as
+``torch.cuda.Stream.cuda_stream`` ints (0 = legacy default stream).  Non-OK
+statuses raise :class:`PaError` carrying the library's ``pa_last_error()``.
+There is no fallback: if the shared library is missing this module raises at
+import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpa.so")
+
+PA_OK = 0
+PA_ERR_INVALID_ARG = 1
+PA_ERR_UNSUPPORTED = 2
+PA_ERR_NOMEM = 3
+PA_ERR_CUDA = 4
+PA_ERR_PRECISION = 5
+STATUS_NAMES = {0: "PA_OK", 1: "PA_ERR_INVALID_ARG", 2: "PA_ERR_UNSUPPORTED", 3: "PA_ERR_NOMEM",
+                4: "PA_ERR_CUDA", 5: "PA_ERR_PRECISION"}
+
+PA_ROUTE_AUTO = 0
+PA_ROUTE_TRANSFORM = 1
+PA_ROUTE_BITPACKED = 2
+PA_RESIDUAL_LIMIT = 0.25
+
+EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
+            "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
+            "pa_destroy", "pa_last_error", "pa_status_string", "pa_version"]
+
+
+class PaError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+
+
+class pa_options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("route", ctypes.c_int32),
+                ("seed_bit_offset", ctypes.c_uint64), ("reserved", ctypes.c_uint32 * 8)]
+
+
+class pa_info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("m", ctypes.c_uint64), ("route", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("transform_len", ctypes.c_uint64),
+                ("n1", ctypes.c_uint64), ("n2", ctypes.c_uint64), ("cols_per_cta", ctypes.c_uint64),
+                ("workspace_bytes", ctypes.c_uint64), ("kernels_per_hash", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1805_02372_b200.build` "
+                      "(nvcc, sm_100a).  There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_u64, _p, _st = ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int
+_H = ctypes.c_void_p
+_sig = {
+    "pa_options_init": (_st, [ctypes.POINTER(pa_options)]),
+    "pa_create": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, _p]),
+    "pa_create_ex": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, ctypes.POINTER(pa_options), _p]),
+    "pa_hash": (_st, [_H, _p, _p, _p]),
+    "pa_hash_batch": (_st, [_H, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
+    "pa_hash_host": (_st, [_H, _p, _p, _p]),
+    "pa_create_u64": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, _p]),
+    "pa_hash_u64": (_st, [_H, _p, _p, _p]),
+    "pa_residual": (_st, [_H, ctypes.POINTER(ctypes.c_double), _p]),
+    "pa_get_info": (_st, [_H, ctypes.POINTER(pa_info)]),
+    "pa_destroy": (None, [_H]),
+    "pa_last_error": (ctypes.c_char_p, []),
+    "pa_status_string": (ctypes.c_char_p, [_st]),
+    "pa_version": (ctypes.c_uint32, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def _check(status: int) -> None:
+    if status != PA_OK:
+        raise PaError(status, _lib.pa_last_error().decode(errors="replace"))
+
+
+def pa_version() -> int:
+    return int(_lib.pa_version())
+
+
+def pa_last_error() -> str:
+    return _lib.pa_last_error().decode(errors="replace")
+
+
+def pa_status_string(status: int) -> str:
+    return _lib.pa_status_string(status).decode()
+
+
+def pa_options_init() -> pa_options:
+    o = pa_options()
+    _check(_lib.pa_options_init(ctypes.byref(o)))
+    return o
+
+
+def pa_create(n: int, m: int, seed_ptr: int, stream: int = 0) -> int:
+    h = _H()
+    _check(_lib.pa_create(ctypes.byref(h), n, m, seed_ptr, stream))
+    return h.value
+
+
+def pa_create_ex(n: int, m: int, seed_ptr: int, opt: pa_options | None, stream: int = 0) -> int:
+    h = _H()
+    _check(_lib.pa_create_ex(ctypes.byref(h), n, m, seed_ptr,
+                             ctypes.byref(opt) if opt is not None else None, stream))
+    return h.value
+
+
+def pa_create_u64(n: int, m: int, seed_ptr: int, stream: int = 0) -> int:
+    h = _H()
+    _check(_lib.pa_create_u64(ctypes.byref(h), n, m, seed_ptr, stream))
+    return h.value
+
+
+def pa_hash(h: int, key_ptr: int, out_ptr: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash(h, key_ptr, out_ptr, stream))
+
+
+def pa_hash_u64(h: int, key_ptr: int, out_ptr: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash_u64(h, key_ptr, out_ptr, stream))
+
+
+def pa_hash_batch(h: int, keys_ptr: int, key_stride_words: int, outs_ptr: int,
+                  out_stride_words: int, count: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash_batch(h, keys_ptr, key_stride_words, outs_ptr, out_stride_words, count, stream))
+
+
+def pa_hash_host(h: int, key_host_ptr: int, out_host_ptr: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash_host(h, key_host_ptr, out_host_ptr, stream))
+
+
+def pa_residual(h: int, stream: int = 0) -> float:
+    r = ctypes.c_double()
+    _check(_lib.pa_residual(h, ctypes.byref(r), stream))
+    return r.value
+
+
+def pa_get_info(h: int) -> dict:
+    info = pa_info()
+    _check(_lib.pa_get_info(h, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def pa_destroy(h: int) -> None:
+    _lib.pa_destroy(h)

@@ -1,0 +1,344 @@
+// pa_api.cu -- the C ABI declared in include/pa.h: argument validation, route
+// selection and dispatch.  No exceptions cross this boundary.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "pa_internal.h"
+
+namespace pa {
+
+static thread_local std::string g_err;
+
+void set_error(const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+pa_status cuda_fail(cudaError_t e, const char *what)
+{
+    set_error("%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+    return PA_ERR_CUDA;
+}
+
+// Route (b) costs ~n*m/1024 SHF+LOP3 pairs per SM-cycle; route (a) a few
+// microseconds of fixed latency plus ~40 bytes of HBM traffic per output
+// point.  Below ~2^26 bit-products (e.g. n = 4096, m = 1024: 2^22) the direct
+// product wins (SURVEY.md Sec. 8(d) crossover).
+static int choose_route(uint64_t n, uint64_t m)
+{
+    double prod = (double)n * (double)m;
+    return prod <= 67108864.0 ? PA_ROUTE_BITPACKED : PA_ROUTE_TRANSFORM;
+}
+
+static pa_status check_dev_ptr(const void *p, const char *name, int device)
+{
+    if (!p) {
+        set_error("%s is NULL", name);
+        return PA_ERR_INVALID_ARG;
+    }
+    if ((uintptr_t)p & 15) {
+        set_error("%s = %p is not 16-byte aligned", name, p);
+        return PA_ERR_INVALID_ARG;
+    }
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("%s = %p: cudaPointerGetAttributes failed (%s)", name, p, cudaGetErrorString(e));
+        return PA_ERR_INVALID_ARG;
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) {
+        set_error("%s = %p is not device memory (cudaMemoryType %d); use pa_hash_host for host "
+                  "buffers", name, p, (int)at.type);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (at.type == cudaMemoryTypeDevice && at.device != device) {
+        set_error("%s = %p lives on device %d, the handle on device %d", name, p, at.device, device);
+        return PA_ERR_INVALID_ARG;
+    }
+    return PA_OK;
+}
+
+}  // namespace pa
+
+using namespace pa;
+
+extern "C" {
+
+uint32_t pa_version(void) { return PA_VERSION; }
+
+const char *pa_last_error(void) { return g_err.c_str(); }
+
+const char *pa_status_string(pa_status s)
+{
+    switch (s) {
+    case PA_OK: return "PA_OK";
+    case PA_ERR_INVALID_ARG: return "PA_ERR_INVALID_ARG";
+    case PA_ERR_UNSUPPORTED: return "PA_ERR_UNSUPPORTED";
+    case PA_ERR_NOMEM: return "PA_ERR_NOMEM";
+    case PA_ERR_CUDA: return "PA_ERR_CUDA";
+    case PA_ERR_PRECISION: return "PA_ERR_PRECISION";
+    }
+    return "PA_ERR_UNKNOWN";
+}
+
+pa_status pa_options_init(pa_options *opt)
+{
+    if (!opt) {
+        set_error("opt is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    memset(opt, 0, sizeof *opt);
+    opt->struct_size = sizeof *opt;
+    opt->route = PA_ROUTE_AUTO;
+    return PA_OK;
+}
+
+void pa_destroy(pa_handle h)
+{
+    if (!h) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(h->device);
+    ra_destroy(h);
+    rb_destroy(h);
+    if (h->stage_key) cudaFree(h->stage_key);
+    if (h->stage_out) cudaFree(h->stage_out);
+    cudaSetDevice(prev);
+    delete h;
+}
+
+pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *seed_bits,
+                       const pa_options *opt, void *stream)
+{
+    if (!out) {
+        set_error("h (output handle pointer) is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    if (n == 0 || m == 0 || m > n) {
+        set_error("need 1 <= m <= n, got n = %llu, m = %llu", (unsigned long long)n,
+                  (unsigned long long)m);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (n > (1ull << 40)) {
+        set_error("n = %llu bits exceeds the supported 2^40", (unsigned long long)n);
+        return PA_ERR_UNSUPPORTED;
+    }
+    pa_options o;
+    pa_options_init(&o);
+    if (opt) {
+        if (opt->struct_size != sizeof(pa_options)) {
+            set_error("opt->struct_size = %u, expected %u (call pa_options_init)",
+                      opt->struct_size, (unsigned)sizeof(pa_options));
+            return PA_ERR_INVALID_ARG;
+        }
+        o = *opt;
+    }
+    if (o.route < PA_ROUTE_AUTO || o.route > PA_ROUTE_BITPACKED) {
+        set_error("opt->route = %d is not a pa_route", o.route);
+        return PA_ERR_INVALID_ARG;
+    }
+    for (int i = 0; i < 8; ++i)
+        if (o.reserved[i]) {
+            set_error("opt->reserved[%d] = %u must be 0", i, o.reserved[i]);
+            return PA_ERR_INVALID_ARG;
+        }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    pa_status st = check_dev_ptr(seed_bits, "seed_bits", dev);
+    if (st != PA_OK) return st;
+
+    pa_ctx *h = new (std::nothrow) pa_ctx();
+    if (!h) {
+        set_error("host allocation of the handle failed");
+        return PA_ERR_NOMEM;
+    }
+    h->device = dev;
+    h->n = n;
+    h->m = m;
+    h->L = n + m - 1;
+    h->off = o.seed_bit_offset;
+    h->route = o.route == PA_ROUTE_AUTO ? choose_route(n, m) : o.route;
+    cudaStream_t s = (cudaStream_t)stream;
+    st = h->route == PA_ROUTE_TRANSFORM ? ra_create(h, seed_bits, s) : rb_create(h, seed_bits, s);
+    if (st != PA_OK) {
+        std::string keep = g_err;
+        pa_destroy(h);
+        g_err = keep;
+        return st;
+    }
+    *out = h;
+    return PA_OK;
+}
+
+pa_status pa_create(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits, void *stream)
+{
+    return pa_create_ex(h, n, m, seed_bits, nullptr, stream);
+}
+
+pa_status pa_create_u64(pa_handle *h, uint64_t n, uint64_t m, const uint64_t *seed_bits,
+                        void *stream)
+{
+    return pa_create_ex(h, n, m, (const uint32_t *)seed_bits, nullptr, stream);
+}
+
+static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
+                           cudaStream_t s, bool validate)
+{
+    if (!h) {
+        set_error("handle is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    if (validate) {
+        pa_status st;
+        if (key != h->ok_key) {
+            if ((st = check_dev_ptr(key, "key_bits", h->device)) != PA_OK) return st;
+            h->ok_key = key;
+        }
+        if (out != h->ok_out) {
+            if ((st = check_dev_ptr(out, "out_bits", h->device)) != PA_OK) return st;
+            h->ok_out = out;
+        }
+    }
+    return h->route == PA_ROUTE_TRANSFORM ? ra_hash(h, key, out, zero_words, s)
+                                          : rb_hash(h, key, out, zero_words, s);
+}
+
+pa_status pa_hash(pa_handle h, const uint32_t *key_bits, uint32_t *out_bits, void *stream)
+{
+    if (!h) {
+        set_error("handle is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    return hash_impl(h, key_bits, out_bits, (h->m + 31) / 32, (cudaStream_t)stream, true);
+}
+
+pa_status pa_hash_u64(pa_handle h, const uint64_t *key_bits, uint64_t *out_bits, void *stream)
+{
+    if (!h) {
+        set_error("handle is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    return hash_impl(h, (const uint32_t *)key_bits, (uint32_t *)out_bits, 2 * ((h->m + 63) / 64),
+                     (cudaStream_t)stream, true);
+}
+
+pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_words,
+                        uint32_t *outs, uint64_t out_stride_words, uint32_t count, void *stream)
+{
+    if (!h) {
+        set_error("handle is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    if (key_stride_words < (h->n + 31) / 32 || out_stride_words < (h->m + 31) / 32) {
+        set_error("key_stride_words = %llu (need >= %llu), out_stride_words = %llu (need >= %llu)",
+                  (unsigned long long)key_stride_words, (unsigned long long)((h->n + 31) / 32),
+                  (unsigned long long)out_stride_words, (unsigned long long)((h->m + 31) / 32));
+        return PA_ERR_INVALID_ARG;
+    }
+    if (count == 0) return PA_OK;
+    if ((key_stride_words & 3) || (out_stride_words & 3)) {
+        set_error("strides must keep every key/output 16-byte aligned (multiples of 4 words)");
+        return PA_ERR_INVALID_ARG;
+    }
+    pa_status st;
+    if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
+    if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
+    for (uint32_t k = 0; k < count; ++k) {
+        st = hash_impl(h, keys + k * key_stride_words, outs + k * out_stride_words,
+                       (h->m + 31) / 32, (cudaStream_t)stream, false);
+        if (st != PA_OK) return st;
+    }
+    return PA_OK;
+}
+
+pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream)
+{
+    if (!h || !key_host || !out_host) {
+        set_error("pa_hash_host: NULL argument (h=%p key_host=%p out_host=%p)", (void *)h,
+                  (const void *)key_host, (void *)out_host);
+        return PA_ERR_INVALID_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t kb = ((h->n + 31) / 32) * 4, ob = ((h->m + 31) / 32) * 4;
+    cudaError_t e;
+    if (!h->stage_key) {
+        if ((e = cudaMalloc(&h->stage_key, kb)) != cudaSuccess) {
+            h->stage_key = nullptr;
+            return cuda_fail(e, "pa_hash_host staging alloc");
+        }
+        if ((e = cudaMalloc(&h->stage_out, ob)) != cudaSuccess) {
+            h->stage_out = nullptr;
+            return cuda_fail(e, "pa_hash_host staging alloc");
+        }
+        h->ws_bytes += kb + ob;
+    }
+    if ((e = cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "pa_hash_host H2D");
+    pa_status st = hash_impl(h, h->stage_key, h->stage_out, (h->m + 31) / 32, s, false);
+    if (st != PA_OK) return st;
+    if ((e = cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "pa_hash_host D2H");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host sync");
+    return PA_OK;
+}
+
+pa_status pa_residual(pa_handle h, double *max_residual, void *stream)
+{
+    if (!h || !max_residual) {
+        set_error("pa_residual: NULL argument");
+        return PA_ERR_INVALID_ARG;
+    }
+    *max_residual = 0.0;
+    if (h->route != PA_ROUTE_TRANSFORM) return PA_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long bits = 0;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(&bits, h->a.resid, sizeof bits, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->a.resid, 0, sizeof bits, s)) != cudaSuccess)
+        return cuda_fail(e, "pa_residual");
+    double r;
+    memcpy(&r, &bits, sizeof r);
+    *max_residual = r;
+    if (r > PA_RESIDUAL_LIMIT) {
+        set_error("FP64 residual %.3e exceeds PA_RESIDUAL_LIMIT %.2f", r, PA_RESIDUAL_LIMIT);
+        return PA_ERR_PRECISION;
+    }
+    return PA_OK;
+}
+
+pa_status pa_get_info(pa_handle h, pa_info *info)
+{
+    if (!h || !info) {
+        set_error("pa_get_info: NULL argument");
+        return PA_ERR_INVALID_ARG;
+    }
+    memset(info, 0, sizeof *info);
+    info->n = h->n;
+    info->m = h->m;
+    info->route = h->route;
+    info->device = h->device;
+    if (h->route == PA_ROUTE_TRANSFORM) {
+        info->transform_len = 2 * h->a.g.M;
+        info->n1 = h->a.g.N1;
+        info->n2 = h->a.g.N2;
+        info->cols_per_cta = h->a.g.C;
+    }
+    info->workspace_bytes = h->ws_bytes;
+    info->kernels_per_hash = h->kernels_per_hash;
+    return PA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// route_b.cu -- route (b): bit-packed direct GF(2) Toeplitz product.
+//
+// y[i] = XOR_j s[i-j+n-1] AND x[j]   (Eq. (1), r = uT P:88-92)
+//
+// With the reversed seed sr[u] = s[L-1-u] (L = n+m-1) the row i reads a forward
+// window:  s[i+n-1-j] = sr[(m-1-i) + j], so
+//     y[i] = parity( OR-free XOR_k  X_k AND window32(sr, o_i + 32k) ),  o_i = m-1-i,
+// where X_k is key word k.  A thread owns a group of 32 consecutive offsets
+// o = 32q + b (b = 0..31): for key word k every one of its 32 windows lies in
+// the word pair (sr[q+k], sr[q+k+1]) and is one funnel shift (SHF) away, so the
+// inner loop is SHF + LOP3 per 32 bit-products, register resident.  Threads of a
+// CTA take consecutive q (coalesced seed loads), the key word is a warp-uniform
+// broadcast load, and CTAs along y take disjoint key-word chunks whose partial
+// parities are merged with atomicXor (order-independent, hence deterministic).
+#include "bits.cuh"
+#include "pa_internal.h"
+
+namespace pa {
+namespace {
+
+// sr word w = bits [32w, 32w+32) of reverse(s), zero past L.
+__global__ void k_reverse_seed(const uint32_t *__restrict__ seed, uint64_t off, uint64_t L,
+                               uint32_t *__restrict__ sr, uint64_t srw)
+{
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < srw;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        if (32 * w < L) {
+            // source positions off+L-1-32w-b, b = 0..31: a window starting at P0
+            int64_t P0 = (int64_t)(off + L) - 32 - 32 * (int64_t)w;
+            v = __brev(bits32(seed, P0, (int64_t)off, (int64_t)(off + L)));
+            uint64_t valid = L - 32 * w;            // bits b < valid are real
+            if (valid < 32) v &= (1u << valid) - 1u;
+        }
+        sr[w] = v;
+    }
+}
+
+constexpr int kThreadsB = 128;
+
+__global__ void __launch_bounds__(kThreadsB)
+k_toeplitz_bitpacked(const uint32_t *__restrict__ key, uint64_t n, uint64_t m,
+                     const uint32_t *__restrict__ sr, uint32_t *__restrict__ out,
+                     uint64_t Q, uint64_t KW, uint64_t KC)
+{
+    uint64_t q = blockIdx.x * (uint64_t)kThreadsB + threadIdx.x;
+    uint64_t k0 = blockIdx.y * KC;
+    uint64_t k1 = min(KW, k0 + KC);
+    if (q >= Q || k0 >= k1) return;
+    uint32_t acc[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) acc[b] = 0u;
+    const uint32_t lastmask = (n & 31) ? ((1u << (n & 31)) - 1u) : 0xFFFFFFFFu;
+    uint32_t A = __ldg(sr + q + k0);
+    for (uint64_t k = k0; k < k1; ++k) {
+        uint32_t X = __ldg(key + k);
+        if (k == KW - 1) X &= lastmask;
+        uint32_t B = __ldg(sr + q + k + 1);
+#pragma unroll
+        for (int b = 0; b < 32; ++b) acc[b] ^= X & __funnelshift_r(A, B, b);
+        A = B;
+    }
+    uint32_t P = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) P |= (uint32_t)(__popc(acc[b]) & 1) << b;
+    // offset o = 32q + b is row i = m-1-o; valid only for o <= m-1
+    uint64_t o0 = 32 * q;
+    uint64_t nvalid = m - o0;                // >= 1 since q < Q = ceil(m/32)
+    if (nvalid < 32) P &= (1u << nvalid) - 1u;
+    // rows m-32-32q .. m-1-32q in increasing order <-> b = 31 .. 0
+    uint32_t R = __brev(P);
+    int64_t base = (int64_t)m - 32 - (int64_t)o0;
+    if (base < 0) {
+        R >>= (int)(-base);                  // dropped bits were masked rows
+        if (R) atomicXor(out, R);
+        return;
+    }
+    uint64_t wd = (uint64_t)base >> 5;
+    int sh = (int)(base & 31);
+    if (R << sh) atomicXor(out + wd, R << sh);
+    if (sh && (R >> (32 - sh))) atomicXor(out + wd + 1, R >> (32 - sh));
+}
+
+}  // namespace
+
+pa_status rb_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
+{
+    uint64_t Q = (h->m + 31) / 32, KW = (h->n + 31) / 32;
+    h->b.srw = Q + KW + 4;
+    cudaError_t e = cudaMalloc(&h->b.sr, h->b.srw * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        h->b.sr = nullptr;
+        set_error("route (b): cudaMalloc of %llu bytes failed: %s",
+                  (unsigned long long)(h->b.srw * 4), cudaGetErrorString(e));
+        return PA_ERR_NOMEM;
+    }
+    h->ws_bytes += h->b.srw * sizeof(uint32_t);
+    uint64_t gw = (h->b.srw + 255) / 256;
+    int grid = (int)(gw < 4096 ? gw : 4096);
+    k_reverse_seed<<<grid, 256, 0, s>>>(seed, h->off, h->L, h->b.sr, h->b.srw);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "route (b) seed reversal launch");
+    h->kernels_per_hash = 1;
+    return PA_OK;
+}
+
+pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
+                  cudaStream_t s)
+{
+    uint64_t Q = (h->m + 31) / 32, KW = (h->n + 31) / 32;
+    cudaError_t e = cudaMemsetAsync(out, 0, zero_words * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return cuda_fail(e, "route (b) output memset");
+    // key-word chunk so that ~8 CTAs per SM worth of (q, chunk) items exist
+    uint64_t gx = (Q + kThreadsB - 1) / kThreadsB;
+    uint64_t want_y = (148ull * 8 + gx - 1) / gx;
+    uint64_t KC = (KW + want_y - 1) / want_y;
+    if (KC < 16) KC = 16;
+    uint64_t gy = (KW + KC - 1) / KC;
+    if (gy > 65535) {
+        gy = 65535;
+        KC = (KW + gy - 1) / gy;
+        gy = (KW + KC - 1) / KC;
+    }
+    dim3 grid((unsigned)gx, (unsigned)gy);
+    k_toeplitz_bitpacked<<<grid, kThreadsB, 0, s>>>(key, h->n, h->m, h->b.sr, out, Q, KW, KC);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "route (b) kernel launch");
+    return PA_OK;
+}
+
+void rb_destroy(pa_ctx *h)
+{
+    if (h->b.sr) cudaFree(h->b.sr);
+    h->b.sr = nullptr;
+}
+
+}  // namespace pa

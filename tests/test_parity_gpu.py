@@ -1,0 +1,239 @@
+"""GPU parity: libpa (through the C ABI) vs the CPU oracle, bit-exact.
+
+Inputs are seeded SplitMix64 bit strings (pa_synth).  Sizes span several
+tiles and ragged tails; full outputs are compared where the oracle finishes in
+seconds, sampled rows (each an independent O(n) oracle evaluation) plus
+closed forms at the BASELINE.json sizes.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import pa_synth as syn
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU hosts
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1805_02372_b200 as pa  # noqa: E402
+
+DEV = torch.device("cuda:0")
+FULL_LIMIT = 3e10   # n*m bit-products the oracle runs in full (OpenMP, seconds)
+
+
+def to_dev(words64: np.ndarray) -> torch.Tensor:
+    w = np.ascontiguousarray(words64).view(np.int32)
+    pad = (-w.size) % 4
+    if pad:
+        w = np.concatenate([w, np.zeros(pad, np.int32)])
+    return torch.from_numpy(w.copy()).to(DEV)
+
+
+def from_dev(t: torch.Tensor, m: int) -> np.ndarray:
+    return oracle.unpack(t.cpu().numpy().view(np.uint32), m)
+
+
+def sample_rows(m: int, seed: int = 0, k: int = 4096) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    r = np.concatenate([np.arange(min(m, 256)), np.arange(max(0, m - 256), m), rng.integers(0, m, k)])
+    return np.unique(r)
+
+
+def check(n, m, sw, kw, route, full=None):
+    seed_t, key_t = to_dev(sw), to_dev(kw)
+    with pa.Hasher(n, m, seed_t, route=route) as h:
+        out = h.hash(key_t)
+        torch.cuda.synchronize()
+        got = from_dev(out, m)
+        # tail bits beyond m are zero
+        allbits = oracle.unpack(out.cpu().numpy().view(np.uint32), 32 * ((m + 31) // 32))
+        assert not allbits[m:].any()
+        res = h.residual()
+        info = h.info
+    if full is None:
+        full = n * m <= FULL_LIMIT
+    if full:
+        want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+        bad = np.flatnonzero(got != want)
+        assert bad.size == 0, f"n={n} m={m} route={route} {bad.size} wrong bits, first {bad[:8]} info={info}"
+    else:
+        rows = sample_rows(m, n)
+        want = oracle.toeplitz_rows(n, m, sw, kw, rows)
+        bad = np.flatnonzero(got[rows] != want)
+        assert bad.size == 0, f"n={n} m={m} route={route} sampled rows wrong: {rows[bad[:8]]}"
+    if info["route"] == pa.PA_ROUTE_TRANSFORM:
+        assert res < 1e-3, res
+    return got, info
+
+
+SWEEP_N = [1, 2, 31, 32, 33, 63, 64, 65, 127, 1000, 4095, 4096, 4097, 65537, 1_000_003]
+
+
+def _ms(n):
+    return sorted({m for m in (1, 32, 33, n // 10, n // 4, n) if 1 <= m <= n})
+
+
+@pytest.mark.parametrize("route", ["bitpacked", "transform"])
+@pytest.mark.parametrize("n", SWEEP_N)
+def test_length_sweep(route, n):
+    for m in _ms(n):
+        if route == "bitpacked" and n * m > 2e11:
+            continue
+        sw = syn.random_bits(syn.seed_stream(100 + n % 97), n + m - 1)
+        kw = syn.random_bits(syn.key_stream(100, n + m), n)
+        check(n, m, sw, kw, route)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_configs_full(name):
+    n, m, sw, kw = syn.config_inputs(name)
+    for route in ("transform", "bitpacked") if name == "C1" else ("transform",):
+        check(n, m, sw, kw, route, full=True)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5a", "C5c"])
+def test_configs_sampled_and_closed_forms(name):
+    """BASELINE.json sizes, same launch configuration as bench.py: sampled rows
+    vs the oracle, plus full-output closed forms (all-ones key, unit keys)."""
+    n, m, sw, kw = syn.config_inputs(name)
+    check(n, m, sw, kw, "auto", full=False)
+    L = n + m - 1
+    s = oracle.unpack(sw, L)
+    P = np.zeros(L + 1, np.uint8)
+    P[1:] = np.bitwise_xor.accumulate(s)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        got = from_dev(h.hash(to_dev(syn.ones_bits(n))), m)
+        i = np.arange(m)
+        assert np.array_equal(got, P[i + n] ^ P[i])
+        for j in (0, n // 3, n - 1):
+            got = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
+            assert np.array_equal(got, s[n - 1 - j: n - 1 - j + m]), j
+        assert h.residual() < 1e-3
+
+
+def test_routes_agree():
+    """P8: the two exact GPU algorithms agree bit for bit."""
+    for n, m in ((20_011, 2_001), (100_000, 25_000), (333_333, 3_333)):
+        sw = syn.random_bits(syn.seed_stream(7 + n), n + m - 1)
+        kw = syn.random_bits(syn.key_stream(7, n), n)
+        a, _ = check(n, m, sw, kw, "transform", full=False)
+        b, _ = check(n, m, sw, kw, "bitpacked", full=False)
+        assert np.array_equal(a, b)
+
+
+def test_structured_inputs():
+    n, m = 50_000, 12_345
+    L = n + m - 1
+    sw = syn.random_bits(syn.seed_stream(9), L)
+    s = oracle.unpack(sw, L)
+    for route in ("transform", "bitpacked"):
+        with pa.Hasher(n, m, to_dev(sw), route=route) as h:
+            assert not from_dev(h.hash(to_dev(syn.zero_bits(n))), m).any()
+            kw, pos = syn.sparse_bits(11, n, 25)
+            want = np.zeros(m, np.uint8)
+            for j in pos:
+                want ^= s[n - 1 - j: n - 1 - j + m]
+            assert np.array_equal(from_dev(h.hash(to_dev(kw)), m), want)
+        with pa.Hasher(n, m, to_dev(syn.ones_bits(L)), route=route) as h:
+            kw = syn.random_bits(5, n)
+            par = int(oracle.unpack(kw, n).sum() & 1)
+            assert np.all(from_dev(h.hash(to_dev(kw)), m) == par)
+
+
+def test_linearity_and_garbage_tail_bits():
+    n, m = 77_777, 7_777
+    sw = syn.random_bits(syn.seed_stream(21), n + m - 1)
+    a = syn.random_bits(31, n)
+    b = syn.random_bits(32, n)
+    for route in ("transform", "bitpacked"):
+        with pa.Hasher(n, m, to_dev(sw), route=route) as h:
+            ya = from_dev(h.hash(to_dev(a)), m)
+            yb = from_dev(h.hash(to_dev(b)), m)
+            assert np.array_equal(from_dev(h.hash(to_dev(a ^ b)), m), ya ^ yb)
+            a2 = a.copy()
+            a2[-1] |= np.uint64(0xFFFF_FFFF_FFFF_FFFF) << np.uint64(n % 64)
+            assert np.array_equal(from_dev(h.hash(to_dev(a2)), m), ya)
+
+
+@pytest.mark.parametrize("route", ["transform", "bitpacked"])
+def test_seed_offset_row_and_column_shards(route):
+    """Row and column shards via pa_options.seed_bit_offset reassemble y (P7,
+    the paper's Eq. (4) split and Eq. (7) merge)."""
+    n, m = 40_000, 9_000
+    L = n + m - 1
+    sw = syn.random_bits(syn.seed_stream(33), L)
+    kw = syn.random_bits(syn.key_stream(33, 0), n)
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    seed_t = to_dev(sw)
+    key_bits = oracle.unpack(kw, n)
+    parts = []
+    for r0, r1 in ((0, 3000), (3000, 3001), (3001, m)):
+        with pa.Hasher(n, r1 - r0, seed_t, route=route, seed_bit_offset=r0) as h:
+            parts.append(from_dev(h.hash(to_dev(kw)), r1 - r0))
+    assert np.array_equal(np.concatenate(parts), want)
+    acc = np.zeros(m, np.uint8)
+    for c0, c1 in ((0, 12_345), (12_345, 21_346), (21_346, n)):  # each >= m bits (m <= n_g)
+        ng = c1 - c0
+        with pa.Hasher(ng, m, seed_t, route=route, seed_bit_offset=n - ng - c0) as h:
+            acc ^= from_dev(h.hash(to_dev(oracle.pack(key_bits[c0:c1]))), m)
+    assert np.array_equal(acc, want)
+
+
+def test_batch_and_u64_and_host_paths():
+    n, m = 123_457, 30_000
+    sw = syn.random_bits(syn.seed_stream(44), n + m - 1)
+    keys = [syn.random_bits(syn.key_stream(44, k), n) for k in range(5)]
+    kw32 = (n + 31) // 32
+    stride = (kw32 + 3) // 4 * 4
+    mat = np.zeros((5, stride), np.int32)
+    for k, w in enumerate(keys):
+        mat[k, :kw32] = w.view(np.int32)[:kw32]
+    for route in ("transform", "bitpacked"):
+        with pa.Hasher(n, m, to_dev(sw), route=route) as h:
+            outs = h.hash_batch(torch.from_numpy(mat).to(DEV))
+            torch.cuda.synchronize()
+            for k, w in enumerate(keys):
+                want = oracle.unpack(oracle.toeplitz_words(n, m, sw, w), m)
+                assert np.array_equal(oracle.unpack(outs[k].cpu().numpy().view(np.uint32), m), want)
+                # host end-to-end path
+                kh = torch.from_numpy(w.view(np.int32).copy()).pin_memory()
+                oh = torch.zeros((m + 31) // 32, dtype=torch.int32).pin_memory()
+                h.hash_host(kh, oh)
+                assert np.array_equal(oracle.unpack(oh.numpy().view(np.uint32), m), want)
+        # uint64 aliases: output tail half-word zero-filled
+        seed_t = to_dev(sw)
+        hh = pa.pa_create_u64(n, m, seed_t.data_ptr(), 0)
+        try:
+            out = torch.full(((m + 63) // 64 * 2,), -1, dtype=torch.int32, device=DEV)
+            pa.pa_hash_u64(hh, to_dev(keys[0]).data_ptr(), out.data_ptr(), 0)
+            torch.cuda.synchronize()
+            allb = oracle.unpack(out.cpu().numpy().view(np.uint32), 64 * ((m + 63) // 64))
+            want = oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[0]), m)
+            assert np.array_equal(allb[:m], want) and not allb[m:].any()
+        finally:
+            pa.pa_destroy(hh)
+
+
+def test_rejects_host_pointer_and_misalignment():
+    n, m = 1000, 100
+    seed_t = to_dev(syn.random_bits(1, n + m - 1))
+    host = torch.zeros(64, dtype=torch.int32)
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_create(n, m, host.data_ptr(), 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG
+    with pytest.raises(pa.PaError):
+        pa.pa_create(n, m, seed_t.data_ptr() + 4, 0)
+    with pa.Hasher(n, m, seed_t) as h:
+        with pytest.raises(pa.PaError):
+            pa.pa_hash(h.handle, host.data_ptr(), h.new_out().data_ptr(), 0)
+
+
+def test_tiny_transform_edge_cases():
+    """Degenerate lengths on the transform route: n = m = 1, m = n, m = 1."""
+    for n, m in ((1, 1), (2, 1), (2, 2), (3, 3), (7, 1), (8, 8), (100, 1), (100, 100)):
+        for sv in range(3):
+            sw = syn.random_bits(1000 + sv, n + m - 1)
+            kw = syn.random_bits(2000 + sv, n)
+            check(n, m, sw, kw, "transform", full=True)
