@@ -1,0 +1,257 @@
+// fft_core.cuh -- FP64 complex mixed-radix (2,3,4,5,7,8) FFT building blocks for
+// libpa route (a).  In-place stages on a batch of C interleaved sequences held in
+// padded shared memory; the first and last stage of a pass may load from / store
+// to anything (bits, global memory, the parity epilogue) through functors.
+#pragma once
+#include <stdint.h>
+
+namespace pa {
+
+constexpr int kMaxStages = 24;
+
+// One radix-R stage of a length-Lt transform: span L = R * Ls, twiddle stride
+// G = Lt / L (omega_L^{jk} = omega_Lt^{jkG}), nb = Lt / R butterflies per sequence.
+struct StageDesc {
+    uint32_t R, L, Ls, G, nb;
+    uint64_t magic;  // ceil(2^40 / Ls): t / Ls == (t * magic) >> 40 for t < 2^24
+};
+
+struct FftPlan {
+    int S;              // number of stages (0 when Lt == 1)
+    uint32_t Lt;        // transform length
+    uint32_t nhi;       // two-level twiddle table: omega_Lt^e = hi[e >> 6] * lo[e & 63]
+    StageDesc st[kMaxStages];
+};
+
+__device__ __forceinline__ uint32_t pidx(uint32_t e) { return e + (e >> 4); }
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b)
+{
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b)  // a * conj(b)
+{
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }
+__device__ __forceinline__ double2 mul_pi(double2 a) { return make_double2(-a.y, a.x); }
+
+// ---- small DFTs: X_k = sum_r v_r w^{rk}, w = exp(-2 pi i / R) (forward) or conj (INV)
+template <int R, bool INV> struct Dft;
+
+template <bool INV> struct Dft<2, INV> {
+    __device__ __forceinline__ static void run(double2 *v)
+    {
+        double2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    }
+};
+
+template <bool INV> struct Dft<4, INV> {
+    __device__ __forceinline__ static void run(double2 *v)
+    {
+        double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+        double2 t2 = cadd(v[1], v[3]), d = csub(v[1], v[3]);
+        double2 t3 = INV ? mul_pi(d) : mul_mi(d);
+        v[0] = cadd(t0, t2);
+        v[2] = csub(t0, t2);
+        v[1] = cadd(t1, t3);
+        v[3] = csub(t1, t3);
+    }
+};
+
+template <bool INV> struct Dft<8, INV> {
+    __device__ __forceinline__ static void run(double2 *v)
+    {
+        const double h = 0.70710678118654752440;  // sqrt(1/2)
+        double2 e[4] = {v[0], v[2], v[4], v[6]};
+        double2 o[4] = {v[1], v[3], v[5], v[7]};
+        Dft<4, INV>::run(e);
+        Dft<4, INV>::run(o);
+        double2 o1 = INV ? make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
+                         : make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+        double2 o2 = INV ? mul_pi(o[2]) : mul_mi(o[2]);
+        double2 o3 = INV ? make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
+                         : make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+        v[0] = cadd(e[0], o[0]);
+        v[4] = csub(e[0], o[0]);
+        v[1] = cadd(e[1], o1);
+        v[5] = csub(e[1], o1);
+        v[2] = cadd(e[2], o2);
+        v[6] = csub(e[2], o2);
+        v[3] = cadd(e[3], o3);
+        v[7] = csub(e[3], o3);
+    }
+};
+
+// cos/sin(2 pi t / R), t = 1..R-1, odd R (20 significant digits)
+template <int R> struct Trig;
+template <> struct Trig<3> {
+    __device__ static constexpr double c(int) { return -0.5; }
+    __device__ static constexpr double s(int t) { return t == 1 ? 0.86602540378443864676 : -0.86602540378443864676; }
+};
+template <> struct Trig<5> {
+    __device__ static constexpr double c(int t) { return (t == 1 || t == 4) ? 0.30901699437494742410 : -0.80901699437494742410; }
+    __device__ static constexpr double s(int t)
+    {
+        return t == 1 ? 0.95105651629515357212 : t == 2 ? 0.58778525229247312917
+               : t == 3 ? -0.58778525229247312917 : -0.95105651629515357212;
+    }
+};
+template <> struct Trig<7> {
+    __device__ static constexpr double c(int t)
+    {
+        return (t == 1 || t == 6) ? 0.62348980185873353053
+               : (t == 2 || t == 5) ? -0.22252093395631440429 : -0.90096886790241912624;
+    }
+    __device__ static constexpr double s(int t)
+    {
+        return t == 1 ? 0.78183148246802980871 : t == 2 ? 0.97492791218182360702
+               : t == 3 ? 0.43388373911755812048 : t == 4 ? -0.43388373911755812048
+               : t == 5 ? -0.97492791218182360702 : -0.78183148246802980871;
+    }
+};
+
+// odd R: X_k = v0 + sum_r (v_r + v_{R-r}) cos(2 pi rk/R) -+ i sum_r (v_r - v_{R-r}) sin(2 pi rk/R)
+template <int R, bool INV> struct DftOdd {
+    __device__ __forceinline__ static void run(double2 *v)
+    {
+        constexpr int H = (R - 1) / 2;
+        double2 sum[H + 1], dif[H + 1];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+            sum[r] = cadd(v[r], v[R - r]);
+            dif[r] = csub(v[r], v[R - r]);
+        }
+        double2 out[R];
+        out[0] = v[0];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) out[0] = cadd(out[0], sum[r]);
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+            double2 re = v[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 1; r <= H; ++r) {
+                const int t = (r * k) % R;
+                re.x = fma(sum[r].x, Trig<R>::c(t), re.x);
+                re.y = fma(sum[r].y, Trig<R>::c(t), re.y);
+                im.x = fma(dif[r].x, Trig<R>::s(t), im.x);
+                im.y = fma(dif[r].y, Trig<R>::s(t), im.y);
+            }
+            double2 minus = make_double2(re.x + im.y, re.y - im.x);  // re - i*im
+            double2 plus = make_double2(re.x - im.y, re.y + im.x);   // re + i*im
+            out[k] = INV ? plus : minus;
+            out[R - k] = INV ? minus : plus;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = out[r];
+    }
+};
+template <bool INV> struct Dft<3, INV> : DftOdd<3, INV> {};
+template <bool INV> struct Dft<5, INV> : DftOdd<5, INV> {};
+template <bool INV> struct Dft<7, INV> : DftOdd<7, INV> {};
+
+// omega_Lt^e from the two-level table (shared memory)
+__device__ __forceinline__ double2 twiddle(const double2 *lo, const double2 *hi, uint32_t e)
+{
+    return cmul(hi[e >> 6], lo[e & 63]);
+}
+
+// One in-place stage over all butterflies of a batch of 2^logC sequences.
+//   DIF (forward): v = DFT_R(v); v_k *= omega_L^{jk}
+//   DIT (inverse): v_k *= conj omega_L^{jk}; v = IDFT_R(v)
+// ld(idx, c) returns element idx of sequence c; st(idx, c, v) stores it.
+template <int R, bool INV, class LD, class ST>
+__device__ __forceinline__ void stage_run(const StageDesc &sd, uint32_t logC, const double2 *wlo,
+                                          const double2 *whi, LD &ld, ST &st)
+{
+    const uint32_t nb = sd.nb << logC;
+    const uint32_t cm = (1u << logC) - 1;
+    for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
+        const uint32_t c = q & cm, t = q >> logC;
+        const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
+        const uint32_t j = t - g * sd.Ls;
+        const uint32_t base = g * sd.L + j;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = ld(base + r * sd.Ls, c);
+        if (!INV) {
+            Dft<R, false>::run(v);
+            if (j) {
+#pragma unroll
+                for (int k = 1; k < R; ++k) v[k] = cmul(v[k], twiddle(wlo, whi, j * k * sd.G));
+            }
+        } else {
+            if (j) {
+#pragma unroll
+                for (int k = 1; k < R; ++k) v[k] = cmulc(v[k], twiddle(wlo, whi, j * k * sd.G));
+            }
+            Dft<R, true>::run(v);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) st(base + r * sd.Ls, c, v[r]);
+    }
+}
+
+template <bool INV, class LD, class ST>
+__device__ __forceinline__ void stage_any(const StageDesc &sd, uint32_t logC, const double2 *wlo,
+                                          const double2 *whi, LD &ld, ST &st)
+{
+    switch (sd.R) {
+    case 2: stage_run<2, INV>(sd, logC, wlo, whi, ld, st); break;
+    case 3: stage_run<3, INV>(sd, logC, wlo, whi, ld, st); break;
+    case 4: stage_run<4, INV>(sd, logC, wlo, whi, ld, st); break;
+    case 5: stage_run<5, INV>(sd, logC, wlo, whi, ld, st); break;
+    case 7: stage_run<7, INV>(sd, logC, wlo, whi, ld, st); break;
+    default: stage_run<8, INV>(sd, logC, wlo, whi, ld, st); break;
+    }
+}
+
+// A whole forward DIF over stages [0, S): stage 0 loads with ld0, the last stores
+// with stN, the rest go through shared memory `sm` (batch layout).  Ends without
+// a barrier after the last stage (its stores may go anywhere).
+template <class LD0, class STN>
+__device__ __forceinline__ void dif_pass(const FftPlan &P, uint32_t logC, double2 *sm, const double2 *wlo,
+                                         const double2 *whi, LD0 &ld0, STN &stN)
+{
+    auto lds = [&](uint32_t idx, uint32_t c) { return sm[pidx((idx << logC) + c)]; };
+    auto sts = [&](uint32_t idx, uint32_t c, double2 v) { sm[pidx((idx << logC) + c)] = v; };
+    if (P.S == 1) {
+        stage_any<false>(P.st[0], logC, wlo, whi, ld0, stN);
+        return;
+    }
+    stage_any<false>(P.st[0], logC, wlo, whi, ld0, sts);
+    __syncthreads();
+    for (int i = 1; i < P.S - 1; ++i) {
+        stage_any<false>(P.st[i], logC, wlo, whi, lds, sts);
+        __syncthreads();
+    }
+    stage_any<false>(P.st[P.S - 1], logC, wlo, whi, lds, stN);
+}
+
+// A whole inverse DIT (stages S-1 .. 0): the first (stage S-1) loads with ld0,
+// stage 0 stores with stN.
+template <class LD0, class STN>
+__device__ __forceinline__ void dit_pass(const FftPlan &P, uint32_t logC, double2 *sm, const double2 *wlo,
+                                         const double2 *whi, LD0 &ld0, STN &stN)
+{
+    auto lds = [&](uint32_t idx, uint32_t c) { return sm[pidx((idx << logC) + c)]; };
+    auto sts = [&](uint32_t idx, uint32_t c, double2 v) { sm[pidx((idx << logC) + c)] = v; };
+    if (P.S == 1) {
+        stage_any<true>(P.st[0], logC, wlo, whi, ld0, stN);
+        return;
+    }
+    stage_any<true>(P.st[P.S - 1], logC, wlo, whi, ld0, sts);
+    __syncthreads();
+    for (int i = P.S - 2; i >= 1; --i) {
+        stage_any<true>(P.st[i], logC, wlo, whi, lds, sts);
+        __syncthreads();
+    }
+    stage_any<true>(P.st[0], logC, wlo, whi, lds, stN);
+}
+
+}  // namespace pa

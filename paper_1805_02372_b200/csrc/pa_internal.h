@@ -6,39 +6,38 @@
 #include <stdint.h>
 
 #include "../../include/pa.h"
+#include "fft_core.cuh"
 
 namespace pa {
 
 // ---------------------------------------------------------------- route (a)
 // FP64 negacyclic ("right-angle") convolution of length N = 2M real points
 // via a complex DFT of length M = N1 * N2 (four-step split), DESIGN.md Sec. 4.
-constexpr int kMaxStages = 24;
-
-struct RadixPlan {
-    int S;                  // number of stages
-    int R[kMaxStages];      // radix of stage i (DIF order; DIT runs them reversed)
-};
-
 struct Geometry {
     uint64_t M;             // complex transform length
-    uint64_t M4;            // 4*M (exponent modulus of the twist/twiddle table)
-    uint32_t N1, N2, C;     // rows are N1 long (contiguous), N2 rows, C columns per CTA
-    uint32_t taus;          // tau_lo table size B; tau(e) = tau_hi[e / B] * tau_lo[e % B]
-    RadixPlan p1, p2;       // radix plans of N1 and N2
+    uint32_t N1, N2;        // rows are N1 long (contiguous), N2 rows
+    uint32_t C, logC;       // columns per CTA in the strided passes (power of two <= 16)
+    FftPlan f1, f2;         // stage plans of N1 (row pass) and N2 (strided passes)
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)
+    uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)
     uint32_t smem1, smem2;  // dynamic shared bytes: K1/K3, K2
+};
+
+struct RouteTables {
+    double2 *W1lo, *W1hi;   // omega_N1^e = W1hi[e >> 6] * W1lo[e & 63]
+    double2 *W2lo, *W2hi;   // omega_N2^e
+    double2 *zeta;          // exp(i pi a / N), a < N1  (twist, N = 2M)
+    double2 *theta;         // exp(i pi b / (2 N2)), b < N2 (= zeta^{N1 b})
+    double2 *Mlo, *Mhi;     // omega_M^e = Mhi[e >> 12] * Mlo[e & 4095]
+    uint32_t *rev2;         // K1 DIF output position p -> frequency index k_b
 };
 
 struct RouteA {
     Geometry g;
     double2 *buf = nullptr;    // [N2][N1] working array (also the seed's scratch)
     double2 *spec = nullptr;   // [N2][N1] seed spectrum / M, in K2's position order
-    double2 *W1 = nullptr;     // omega_N1^e, e < N1
-    double2 *W2 = nullptr;     // omega_N2^e, e < N2
-    double2 *theta = nullptr;  // exp(i pi b / (2 N2)), b < N2
-    double2 *tau_lo = nullptr; // exp(2 pi i e / 4M), e < B
-    double2 *tau_hi = nullptr; // exp(2 pi i h B / 4M), h < ceil(4M/B)
-    int *rev2 = nullptr;       // DIF output position -> frequency index, N2 entries
+    double2 *tables = nullptr; // backing store of T's double2 tables
+    RouteTables T{};
     unsigned long long *resid = nullptr; // max |v - rint v| (as double bits)
 };
 

@@ -4,31 +4,32 @@
 // P:128-136): zero-pad, FFT both, multiply, IFFT, take the window
 // [n-1, n+m-1) (one-based "nth to (n+k-1)th") and reduce mod 2.  Here:
 //
-//  * Length (reading R4): a wrap-free window needs only N >= n+m-1 real points
-//    (not the paper's 2n+l-2), and the NEGACYCLIC product mod X^N + 1 is as good
-//    as the cyclic one (wrapped terms land below n-1).  A real negacyclic
-//    product of length N = 2M is a complex cyclic product of length M of the
-//    "right-angle" packed, twisted sequence
+//  * Length (reading R4): a wrap-free window needs only N >= n+m-1
+//    real points (not the paper's 2n+l-2), and the NEGACYCLIC product mod
+//    X^N + 1 serves as well as the cyclic one (wrapped terms land below n-1).
+//    A real negacyclic product of length N = 2M is a complex cyclic product of
+//    length M of the "right-angle" packed, twisted sequence
 //        z[u] = (x[u] + i x[u+M]) * zeta^u,   zeta = exp(i pi / N),  u < M,
 //    so every transform is a plain complex DFT of length M (no real-to-complex
 //    post-pass), 16 bytes per 2 real points.
 //  * Four-step split M = N1 * N2, u = a + N1 b (a < N1 contiguous), frequency
 //    k = N2 k_a + k_b:
-//        K1  strided pass: per column a, DIF over b (N2 points) of the twisted
-//            bits, then twiddle tau(a, k_b) = zeta^a * omega_M^{a k_b}; writes the
-//            [N2][N1] work array (row = DIF output position p, k_b = rev2[p]).
-//        K2  row pass: per row, DIF over a (N1 points, natural -> digit-reversed
-//            order), pointwise * seed spectrum (stored in the same order, scaled
-//            by 1/M), DIT inverse (digit-reversed -> natural).  In place.
-//        K3  strided pass: * conj tau, DIT inverse over k_b -> natural b, untwist
-//            by conj(theta_b) = zeta^{-N1 b}, keep t in [n-1, n+m-1): Re part is
-//            c[u], Im part is c[u+M]; rint, &1, set the output bit.  Records
-//            max |v - rint(v)| (the FP64 error tripwire, PA_ERR_PRECISION).
-//  * The seed goes through K1 and K2's forward half once at create (spectrum
-//    cached: the seed is bound at pa_create, BASELINE.json north_star (1)).
-//  * Shared memory holds C columns x N2 (K1/K3) or one N1 row (K2) of complex
-//    doubles, in-place mixed-radix (2,3,4,5,7,8) butterflies, padded index
-//    e + e/16 so strided butterfly accesses stay bank-conflict free.
+//      K1  strided pass, C columns per CTA: DIF over b (N2 points) of the
+//          twisted key bits (stage 0 reads the bits directly), the last stage
+//          multiplies by tau(a, k_b) = zeta^a omega_M^{a k_b} and writes the
+//          [N2][N1] work array (row = DIF output position p, k_b = rev2[p]).
+//      K2  row pass, one row per CTA: cp.async row -> smem, DIF over a
+//          (natural -> digit-reversed), [last DIF stage * spectrum * first DIT
+//          stage] fused in registers (the spectrum is stored in the same
+//          digit-reversed order, scaled by 1/M), DIT back to natural order, the
+//          last stage storing straight to global memory (in place).
+//      K3  strided pass: cp.async the C-column tile, first DIT stage multiplies
+//          by conj tau, DIT over k_b -> natural b, the last stage feeds the
+//          epilogue: untwist by conj theta_b = zeta^{-N1 b}, keep t in
+//          [n-1, n+m-1) (Re part = c[u], Im part = c[u+M]), rint, &1,
+//          ballot-pack runs of C bits, atomicOr into the output words; records
+//          max |v - rint(v)| (the PA_ERR_PRECISION tripwire).
+//  * The seed goes through K1 and K2's forward half once at create.
 #include <math.h>
 #include <stdio.h>
 
@@ -36,409 +37,284 @@
 #include <vector>
 
 #include "bits.cuh"
+#include "fft_core.cuh"
 #include "pa_internal.h"
 
 namespace pa {
 namespace {
 
 constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic shared memory per CTA
+constexpr uint32_t kMlo = 4096;          // omega_M^e = Mhi[e >> 12] * Mlo[e & 4095]
 
-__device__ __forceinline__ uint32_t pidx(uint32_t e) { return e + (e >> 4); }
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-// a * b
-__device__ __forceinline__ double2 cmul(double2 a, double2 b)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
-// a * conj(b)
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b)
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// tau(a, kb) = zeta^a * omega_M^{a kb};  a*kb < M < 2^32
+__device__ __forceinline__ double2 tau(const RouteTables &T, uint32_t a, uint32_t kb)
 {
-    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
-}
-// a * (-i) and a * (+i)
-__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }
-__device__ __forceinline__ double2 mul_pi(double2 a) { return make_double2(-a.y, a.x); }
-
-// ---- small DFTs in registers: X_k = sum_r v_r w^{rk}, w = exp(-+2 pi i / R)
-template <int R, bool INV> struct Dft;
-
-template <bool INV> struct Dft<2, INV> {
-    __device__ __forceinline__ static void run(double2 *v)
-    {
-        double2 a = v[0], b = v[1];
-        v[0] = cadd(a, b);
-        v[1] = csub(a, b);
-    }
-};
-
-template <bool INV> struct Dft<4, INV> {
-    __device__ __forceinline__ static void run(double2 *v)
-    {
-        double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-        double2 t2 = cadd(v[1], v[3]), d = csub(v[1], v[3]);
-        double2 t3 = INV ? mul_pi(d) : mul_mi(d);
-        v[0] = cadd(t0, t2);
-        v[2] = csub(t0, t2);
-        v[1] = cadd(t1, t3);
-        v[3] = csub(t1, t3);
-    }
-};
-
-template <bool INV> struct Dft<8, INV> {
-    __device__ __forceinline__ static void run(double2 *v)
-    {
-        const double h = 0.70710678118654752440;  // sqrt(1/2)
-        double2 e[4] = {v[0], v[2], v[4], v[6]};
-        double2 o[4] = {v[1], v[3], v[5], v[7]};
-        Dft<4, INV>::run(e);
-        Dft<4, INV>::run(o);
-        // o_k *= w8^k  (w8 = exp(-+ i pi / 4))
-        double2 o1 = INV ? make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
-                         : make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-        double2 o2 = INV ? mul_pi(o[2]) : mul_mi(o[2]);
-        double2 o3 = INV ? make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
-                         : make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-        v[0] = cadd(e[0], o[0]);
-        v[4] = csub(e[0], o[0]);
-        v[1] = cadd(e[1], o1);
-        v[5] = csub(e[1], o1);
-        v[2] = cadd(e[2], o2);
-        v[6] = csub(e[2], o2);
-        v[3] = cadd(e[3], o3);
-        v[7] = csub(e[3], o3);
-    }
-};
-
-// cos/sin(2 pi t / R), t = 1..R-1, for odd R (values to 20 significant digits)
-template <int R> struct Trig;
-template <> struct Trig<3> {
-    __device__ static constexpr double c(int t) { return -0.5; }
-    __device__ static constexpr double s(int t) { return t == 1 ? 0.86602540378443864676 : -0.86602540378443864676; }
-};
-template <> struct Trig<5> {
-    __device__ static constexpr double c(int t)
-    {
-        return (t == 1 || t == 4) ? 0.30901699437494742410 : -0.80901699437494742410;
-    }
-    __device__ static constexpr double s(int t)
-    {
-        return t == 1 ? 0.95105651629515357212
-               : t == 2 ? 0.58778525229247312917
-               : t == 3 ? -0.58778525229247312917
-                        : -0.95105651629515357212;
-    }
-};
-template <> struct Trig<7> {
-    __device__ static constexpr double c(int t)
-    {
-        return (t == 1 || t == 6) ? 0.62348980185873353053
-               : (t == 2 || t == 5) ? -0.22252093395631440429
-                                    : -0.90096886790241912624;
-    }
-    __device__ static constexpr double s(int t)
-    {
-        return t == 1 ? 0.78183148246802980871
-               : t == 2 ? 0.97492791218182360702
-               : t == 3 ? 0.43388373911755812048
-               : t == 4 ? -0.43388373911755812048
-               : t == 5 ? -0.97492791218182360702
-                        : -0.78183148246802980871;
-    }
-};
-
-// odd R: pair r with R-r.  X_k = v0 + sum_r (v_r + v_{R-r}) cos(2 pi rk/R)
-//                                   -+ i sum_r (v_r - v_{R-r}) sin(2 pi rk/R)
-template <int R, bool INV> struct DftOdd {
-    __device__ __forceinline__ static void run(double2 *v)
-    {
-        constexpr int H = (R - 1) / 2;
-        double2 sum[H + 1], dif[H + 1];
-#pragma unroll
-        for (int r = 1; r <= H; ++r) {
-            sum[r] = cadd(v[r], v[R - r]);
-            dif[r] = csub(v[r], v[R - r]);
-        }
-        double2 out[R];
-        out[0] = v[0];
-#pragma unroll
-        for (int r = 1; r <= H; ++r) out[0] = cadd(out[0], sum[r]);
-#pragma unroll
-        for (int k = 1; k <= H; ++k) {
-            double2 re = v[0], im = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int r = 1; r <= H; ++r) {
-                const int t = (r * k) % R;
-                re.x = fma(sum[r].x, Trig<R>::c(t), re.x);
-                re.y = fma(sum[r].y, Trig<R>::c(t), re.y);
-                im.x = fma(dif[r].x, Trig<R>::s(t), im.x);
-                im.y = fma(dif[r].y, Trig<R>::s(t), im.y);
-            }
-            // forward: X_k = re - i*im, X_{R-k} = re + i*im
-            double2 minus = make_double2(re.x + im.y, re.y - im.x);
-            double2 plus = make_double2(re.x - im.y, re.y + im.x);
-            out[k] = INV ? plus : minus;
-            out[R - k] = INV ? minus : plus;
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = out[r];
-    }
-};
-template <bool INV> struct Dft<3, INV> : DftOdd<3, INV> {};
-template <bool INV> struct Dft<5, INV> : DftOdd<5, INV> {};
-template <bool INV> struct Dft<7, INV> : DftOdd<7, INV> {};
-
-// One in-place stage on a batch of C (power of two) interleaved sequences of
-// length Lt in padded shared memory (element t of sequence c at t*C + c).
-// Span L = R * Ls.  DIF (forward): DFT_R then twiddle omega_L^{jk};
-// DIT (inverse): conj twiddle then inverse DFT_R.  W[e] = omega_Lt^e.
-template <int R, bool INV>
-__device__ __forceinline__ void stage(double2 *__restrict__ sm, uint32_t Lt, uint32_t logC,
-                                      uint32_t L, const double2 *__restrict__ W)
-{
-    const uint32_t Ls = L / R;
-    const uint32_t G = Lt / L;
-    const uint32_t C = 1u << logC;
-    const uint32_t nb = (Lt / R) << logC;
-    for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
-        const uint32_t c = q & (C - 1);
-        const uint32_t t = q >> logC;
-        const uint32_t j = t % Ls, g = t / Ls;
-        const uint32_t base = g * L + j;
-        double2 v[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = sm[pidx(((base + r * Ls) << logC) + c)];
-        if (!INV) {
-            Dft<R, false>::run(v);
-            if (j) {
-#pragma unroll
-                for (int k = 1; k < R; ++k) v[k] = cmul(v[k], __ldg(W + j * k * G));
-            }
-        } else {
-            if (j) {
-#pragma unroll
-                for (int k = 1; k < R; ++k) v[k] = cmulc(v[k], __ldg(W + j * k * G));
-            }
-            Dft<R, true>::run(v);
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) sm[pidx(((base + r * Ls) << logC) + c)] = v[r];
-    }
+    uint32_t e = a * kb;
+    double2 w = cmul(__ldg(T.Mhi + (e >> 12)), __ldg(T.Mlo + (e & (kMlo - 1))));
+    return cmul(w, __ldg(T.zeta + a));
 }
 
-template <bool INV>
-__device__ __forceinline__ void stage_dispatch(int R, double2 *sm, uint32_t Lt, uint32_t logC,
-                                               uint32_t L, const double2 *W)
+__device__ __forceinline__ void load_tables(double2 *wlo, double2 *whi, const double2 *glo,
+                                            const double2 *ghi, uint32_t nhi)
 {
-    switch (R) {
-    case 2: stage<2, INV>(sm, Lt, logC, L, W); break;
-    case 3: stage<3, INV>(sm, Lt, logC, L, W); break;
-    case 4: stage<4, INV>(sm, Lt, logC, L, W); break;
-    case 5: stage<5, INV>(sm, Lt, logC, L, W); break;
-    case 7: stage<7, INV>(sm, Lt, logC, L, W); break;
-    default: stage<8, INV>(sm, Lt, logC, L, W); break;
+    for (uint32_t i = threadIdx.x; i < 64 + nhi; i += blockDim.x) {
+        if (i < 64) wlo[i] = glo[i];
+        else whi[i - 64] = ghi[i - 64];
     }
-}
-
-// Forward DIF: natural order in, digit-reversed out.
-__device__ void fft_dif(double2 *sm, uint32_t Lt, uint32_t logC, const RadixPlan &P,
-                        const double2 *W)
-{
-    uint32_t L = Lt;
-    for (int i = 0; i < P.S; ++i) {
-        stage_dispatch<false>(P.R[i], sm, Lt, logC, L, W);
-        L /= (uint32_t)P.R[i];
-        __syncthreads();
-    }
-}
-
-// Inverse DIT (unscaled): digit-reversed in, natural order out.
-__device__ void ifft_dit(double2 *sm, uint32_t Lt, uint32_t logC, const RadixPlan &P,
-                         const double2 *W)
-{
-    uint32_t L = 1;
-    for (int i = P.S - 1; i >= 0; --i) {
-        L *= (uint32_t)P.R[i];
-        stage_dispatch<true>(P.R[i], sm, Lt, logC, L, W);
-        __syncthreads();
-    }
-}
-
-__device__ __forceinline__ double2 tau(const Geometry &g, const double2 *__restrict__ lo,
-                                       const double2 *__restrict__ hi, uint64_t a, uint64_t kb)
-{
-    // E = a * (1 - 4 kb) mod 4M
-    int64_t e = (int64_t)a * (1 - 4 * (int64_t)kb);
-    int64_t M4 = (int64_t)g.M4;
-    e %= M4;
-    if (e < 0) e += M4;
-    return cmul(__ldg(hi + e / g.taus), __ldg(lo + e % g.taus));
 }
 
 // ------------------------------------------------------------------ tables
-__global__ void k_tables(Geometry g, double2 *W1, double2 *W2, double2 *theta, double2 *tlo,
-                         double2 *thi, int *rev2, uint64_t nhi)
+__global__ void k_tables(Geometry g, RouteTables T)
 {
-    uint64_t tot = max(max((uint64_t)g.N1, (uint64_t)g.N2), max((uint64_t)g.taus, nhi));
+    const uint64_t nMhi = (g.M + kMlo - 1) / kMlo;
+    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), std::max<uint64_t>(kMlo, nMhi));
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < tot;
          e += (uint64_t)gridDim.x * blockDim.x) {
         double s, c;
-        if (e < g.N1) {
-            sincospi((double)(2 * e) / (double)g.N1, &s, &c);
-            W1[e] = make_double2(c, -s);
+        if (e < 64) {
+            sincospi(2.0 * (double)e / (double)g.N1, &s, &c);
+            T.W1lo[e] = make_double2(c, -s);
+            sincospi(2.0 * (double)e / (double)g.N2, &s, &c);
+            T.W2lo[e] = make_double2(c, -s);
+        }
+        if (e < g.f1.nhi) {
+            sincospi(2.0 * (double)(e * 64) / (double)g.N1, &s, &c);
+            T.W1hi[e] = make_double2(c, -s);
+        }
+        if (e < g.f2.nhi) {
+            sincospi(2.0 * (double)(e * 64) / (double)g.N2, &s, &c);
+            T.W2hi[e] = make_double2(c, -s);
+        }
+        if (e < g.N1) {  // zeta^a = exp(i pi a / N), N = 2M
+            sincospi((double)e / (double)(2 * g.M), &s, &c);
+            T.zeta[e] = make_double2(c, s);
         }
         if (e < g.N2) {
-            sincospi((double)(2 * e) / (double)g.N2, &s, &c);
-            W2[e] = make_double2(c, -s);
             sincospi((double)e / (double)(2 * (uint64_t)g.N2), &s, &c);
-            theta[e] = make_double2(c, s);
+            T.theta[e] = make_double2(c, s);
             // DIF output position e -> frequency index
             uint32_t rem = (uint32_t)e, L = g.N2, mult = 1, k = 0;
-            for (int i = 0; i < g.p2.S; ++i) {
-                uint32_t Ls = L / (uint32_t)g.p2.R[i];
+            for (int i = 0; i < g.f2.S; ++i) {
+                uint32_t R = g.f2.st[i].R, Ls = L / R;
                 k += (rem / Ls) * mult;
                 rem %= Ls;
-                mult *= (uint32_t)g.p2.R[i];
+                mult *= R;
                 L = Ls;
             }
-            rev2[e] = (int)k;
+            T.rev2[e] = k;
         }
-        if (e < g.taus) {
-            sincospi((double)e / (double)(2 * g.M), &s, &c);
-            tlo[e] = make_double2(c, s);
+        if (e < kMlo) {
+            sincospi(2.0 * (double)e / (double)g.M, &s, &c);
+            T.Mlo[e] = make_double2(c, -s);
         }
-        if (e < nhi) {
-            sincospi((double)(e * g.taus) / (double)(2 * g.M), &s, &c);
-            thi[e] = make_double2(c, s);
+        if (e < nMhi) {
+            sincospi(2.0 * (double)(e * kMlo) / (double)g.M, &s, &c);
+            T.Mhi[e] = make_double2(c, -s);
         }
     }
 }
 
 // ------------------------------------------------------------------ K1
-// bits: the real sequence (key or seed) = bits [off, off+nbits) of `w`,
-// zero padded to N = 2M.  Writes buf[p][a] for a in this CTA's C columns.
-__global__ void k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits,
-                               double2 *__restrict__ buf, Geometry g,
-                               const double2 *__restrict__ W2, const double2 *__restrict__ theta,
-                               const double2 *__restrict__ tlo, const double2 *__restrict__ thi,
-                               const int *__restrict__ rev2, uint32_t *__restrict__ zero_out,
-                               uint64_t zero_words)
+// The real sequence = bits [off, off+nbits) of w, zero padded to N = 2M.
+__global__ void __launch_bounds__(512)
+k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, double2 *__restrict__ buf,
+               Geometry g, RouteTables T, uint32_t *__restrict__ zero_out, uint64_t zero_words)
 {
     extern __shared__ double2 sm[];
-    const uint32_t C = g.C, logC = __ffs(C) - 1;
-    const uint64_t a0 = (uint64_t)blockIdx.x * C;
+    const uint32_t logC = g.logC, C = 1u << logC;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64;
+    uint32_t *rowbits = reinterpret_cast<uint32_t *>(whi + g.f2.nhi);
+    const uint32_t a0 = blockIdx.x * C;
     const int64_t lo = (int64_t)off, hi = (int64_t)(off + nbits);
 
-    if (zero_out) {  // the output bits of this hash are OR-ed in by K3
+    if (zero_out) {  // K3 ORs this hash's output bits in
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
              i += (uint64_t)gridDim.x * blockDim.x)
             zero_out[i] = 0u;
     }
-    // load: z(b, c) = (x[a + N1 b] + i x[a + N1 b + M]) * theta_b
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    // per row b: C real-part bits (low half) and C imaginary-part bits (high half)
+    const uint32_t cmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
     for (uint32_t b = threadIdx.x; b < g.N2; b += blockDim.x) {
-        int64_t P = (int64_t)(a0 + (uint64_t)g.N1 * b) + lo;
-        uint32_t re = bits32(w, P, lo, hi);
-        uint32_t im = bits32(w, P + (int64_t)g.M, lo, hi);
-        double2 th = __ldg(theta + b);
-        for (uint32_t c = 0; c < C; ++c) {
-            double xr = (double)((re >> c) & 1u), xi = (double)((im >> c) & 1u);
-            // (xr + i xi)(th.x + i th.y)
-            sm[pidx((b << logC) + c)] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
-        }
+        int64_t P = (int64_t)a0 + (int64_t)g.N1 * b + lo;
+        uint32_t re = bits32(w, P, lo, hi) & cmask;
+        uint32_t im = bits32(w, P + (int64_t)g.M, lo, hi) & cmask;
+        rowbits[b] = re | (im << 16);
     }
     __syncthreads();
-    fft_dif(sm, g.N2, logC, g.p2, W2);
-    // twiddle and store rows p (k_b = rev2[p])
-    const uint32_t tot = g.N2 << logC;
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        uint32_t p = e >> logC, c = e & (C - 1);
-        uint64_t a = a0 + c;
-        double2 v = cmul(sm[pidx(e)], tau(g, tlo, thi, a, (uint64_t)__ldg(rev2 + p)));
-        buf[(uint64_t)p * g.N1 + a] = v;
+    auto ld_bits = [&](uint32_t b, uint32_t c) {
+        uint32_t rb = rowbits[b];
+        double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (16 + c)) & 1u);
+        double2 th = __ldg(T.theta + b);
+        return make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
+    };
+    auto st_out = [&](uint32_t p, uint32_t c, double2 v) {
+        uint32_t a = a0 + c;
+        buf[(uint64_t)p * g.N1 + a] = cmul(v, tau(T, a, __ldg(T.rev2 + p)));
+    };
+    if (g.f2.S == 0) {
+        for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) st_out(0, c, ld_bits(0, c));
+        return;
     }
+    dif_pass(g.f2, logC, sm, wlo, whi, ld_bits, st_out);
 }
 
 // ------------------------------------------------------------------ K2
-// mode 0 (hash): DIF, * spec, DIT, store back in place.
-// mode 1 (create): DIF, * scale, store to spec.
-__global__ void k2_rows(double2 *__restrict__ buf, const double2 *__restrict__ spec_in,
-                        double2 *__restrict__ spec_out, Geometry g,
-                        const double2 *__restrict__ W1, int mode, double scale)
+// Fused last DIF stage (Ls = 1, no twiddles) * spectrum * first DIT stage.
+template <int R>
+__device__ __forceinline__ void fused_mid(const StageDesc &sd, double2 *sm, const double2 *__restrict__ sp)
+{
+    for (uint32_t gq = threadIdx.x; gq < sd.nb; gq += blockDim.x) {
+        const uint32_t base = gq * R;
+        double2 s[R], v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[r] = __ldg(sp + base + r);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = sm[pidx(base + r)];
+        Dft<R, false>::run(v);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = cmul(v[r], s[r]);
+        Dft<R, true>::run(v);
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[pidx(base + r)] = v[r];
+    }
+}
+
+__device__ __forceinline__ void fused_mid_any(const StageDesc &sd, double2 *sm, const double2 *sp)
+{
+    switch (sd.R) {
+    case 2: fused_mid<2>(sd, sm, sp); break;
+    case 3: fused_mid<3>(sd, sm, sp); break;
+    case 4: fused_mid<4>(sd, sm, sp); break;
+    case 5: fused_mid<5>(sd, sm, sp); break;
+    case 7: fused_mid<7>(sd, sm, sp); break;
+    default: fused_mid<8>(sd, sm, sp); break;
+    }
+}
+
+// mode 0 (hash): in place, buf row -> DIF, * spec, DIT -> buf row.
+// mode 1 (create): buf row -> DIF -> * scale -> spec row.
+__global__ void __launch_bounds__(512)
+k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, RouteTables T, int mode,
+        double scale)
 {
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
-    for (uint32_t row = blockIdx.x; row < g.N2; row += gridDim.x) {
-        double2 *rp = buf + (uint64_t)row * N1;
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = rp[e];
-        __syncthreads();
-        fft_dif(sm, N1, 0, g.p1, W1);
-        if (mode == 1) {
-            double2 *sp = spec_out + (uint64_t)row * N1;
-            for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) {
-                double2 v = sm[pidx(e)];
-                sp[e] = make_double2(v.x * scale, v.y * scale);
-            }
-            __syncthreads();
-            continue;
+    double2 *wlo = sm + g.tile2, *whi = wlo + 64;
+    const uint32_t row = blockIdx.x;
+    double2 *rp = buf + (uint64_t)row * N1;
+    double2 *sp = spec + (uint64_t)row * N1;
+    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
+    load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi);
+    cp_async_wait_all();
+    __syncthreads();
+    auto lds = [&](uint32_t idx, uint32_t) { return sm[pidx(idx)]; };
+    auto sts = [&](uint32_t idx, uint32_t, double2 v) { sm[pidx(idx)] = v; };
+    const FftPlan &P = g.f1;
+    if (mode == 1) {
+        auto st_spec = [&](uint32_t idx, uint32_t, double2 v) { sp[idx] = cscale(v, scale); };
+        if (P.S == 0) {
+            if (threadIdx.x == 0) st_spec(0, 0, sm[0]);
+            return;
         }
-        const double2 *sp = spec_in + (uint64_t)row * N1;
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x)
-            sm[pidx(e)] = cmul(sm[pidx(e)], __ldg(sp + e));
+        dif_pass(P, 0, sm, wlo, whi, lds, st_spec);
+        return;
+    }
+    if (P.S == 0) {
+        if (threadIdx.x == 0) rp[0] = cmul(sm[0], sp[0]);
+        return;
+    }
+    for (int i = 0; i < P.S - 1; ++i) {
+        stage_any<false>(P.st[i], 0, wlo, whi, lds, sts);
         __syncthreads();
-        ifft_dit(sm, N1, 0, g.p1, W1);
+    }
+    fused_mid_any(P.st[P.S - 1], sm, sp);
+    __syncthreads();
+    auto st_row = [&](uint32_t idx, uint32_t, double2 v) { rp[idx] = v; };
+    for (int i = P.S - 2; i >= 1; --i) {
+        stage_any<true>(P.st[i], 0, wlo, whi, lds, sts);
+        __syncthreads();
+    }
+    if (P.S >= 2) {
+        stage_any<true>(P.st[0], 0, wlo, whi, lds, st_row);
+    } else {
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) rp[e] = sm[pidx(e)];
-        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------ K3
-__global__ void k3_inv_columns(const double2 *__restrict__ buf, Geometry g,
-                               const double2 *__restrict__ W2, const double2 *__restrict__ theta,
-                               const double2 *__restrict__ tlo, const double2 *__restrict__ thi,
-                               const int *__restrict__ rev2, uint64_t n, uint64_t m,
-                               uint32_t *__restrict__ out, unsigned long long *__restrict__ resid)
+__global__ void __launch_bounds__(512)
+k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
+               uint32_t *__restrict__ out, unsigned long long *__restrict__ resid)
 {
     extern __shared__ double2 sm[];
-    const uint32_t C = g.C, logC = __ffs(C) - 1;
-    const uint64_t a0 = (uint64_t)blockIdx.x * C;
+    const uint32_t logC = g.logC, C = 1u << logC;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64;
+    const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        uint32_t p = e >> logC, c = e & (C - 1);
-        uint64_t a = a0 + c;
-        double2 v = buf[(uint64_t)p * g.N1 + a];
-        sm[pidx(e)] = cmulc(v, tau(g, tlo, thi, a, (uint64_t)__ldg(rev2 + p)));
-    }
+    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
+        cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    cp_async_wait_all();
     __syncthreads();
-    ifft_dit(sm, g.N2, logC, g.p2, W2);
-    const uint64_t t0 = n - 1, t1 = n + m - 1;  // output window [t0, t1)
+
+    auto ld_tau = [&](uint32_t p, uint32_t c) {
+        return cmulc(sm[pidx((p << logC) + c)], tau(T, a0 + c, __ldg(T.rev2 + p)));
+    };
+    const int64_t t0 = (int64_t)n - 1;  // output window [t0, t0 + m)
     double rmax = 0.0;
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        uint32_t b = e >> logC, c = e & (C - 1);
-        uint64_t u = a0 + c + (uint64_t)g.N1 * b;
-        double2 wv = cmulc(sm[pidx(e)], __ldg(theta + b));
-        uint64_t tr = u, ti = u + g.M;
-        if (tr >= t0 && tr < t1) {
-            double r = rint(wv.x);
-            rmax = fmax(rmax, fabs(wv.x - r));
-            if (((long long)r) & 1) {
-                uint64_t i = tr - t0;
-                atomicOr(out + (i >> 5), 1u << (i & 31));
+    const uint32_t lane = threadIdx.x & 31;
+    auto emit = [&](int64_t i0, bool odd, uint32_t c) {
+        // i0 = output bit index of this element; runs of C lanes hold C consecutive bits
+        bool valid = odd && i0 >= 0 && i0 < (int64_t)m;
+        uint32_t bal = __ballot_sync(__activemask(), valid);
+        if (c == 0) {
+            uint32_t run = (bal >> lane) & ((C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u));
+            if (run) {
+                if (i0 < 0) {
+                    run >>= (int)(-i0);
+                    i0 = 0;
+                }
+                uint64_t wd = (uint64_t)i0 >> 5;
+                int sh = (int)(i0 & 31);
+                atomicOr(out + wd, run << sh);
+                if (sh && (run >> (32 - sh))) atomicOr(out + wd + 1, run >> (32 - sh));
             }
         }
-        if (ti >= t0 && ti < t1) {
-            double r = rint(wv.y);
-            rmax = fmax(rmax, fabs(wv.y - r));
-            if (((long long)r) & 1) {
-                uint64_t i = ti - t0;
-                atomicOr(out + (i >> 5), 1u << (i & 31));
-            }
+    };
+    auto st_epi = [&](uint32_t b, uint32_t c, double2 v) {
+        double2 wv = cmulc(v, __ldg(T.theta + b));
+        int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
+        // real part -> t = u, imaginary part -> t = u + M
+        bool inr = u >= t0 && u < t0 + (int64_t)m;
+        double rr = rint(wv.x);
+        if (inr) rmax = fmax(rmax, fabs(wv.x - rr));
+        emit(u - t0, inr && (((long long)rr) & 1), c);
+        int64_t ui = u + (int64_t)g.M;
+        bool ini = ui >= t0 && ui < t0 + (int64_t)m;
+        double ri = rint(wv.y);
+        if (ini) rmax = fmax(rmax, fabs(wv.y - ri));
+        emit(ui - t0, ini && (((long long)ri) & 1), c);
+    };
+    if (g.f2.S == 0) {
+        if (threadIdx.x < 32) {
+            bool act = threadIdx.x < C;
+            double2 v = act ? ld_tau(0, threadIdx.x) : make_double2(0, 0);
+            if (act) st_epi(0, threadIdx.x, v);
         }
+    } else {
+        dit_pass(g.f2, logC, sm, wlo, whi, ld_tau, st_epi);
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, d));
-    if ((threadIdx.x & 31) == 0 && rmax > 0.0)
-        atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
+    if (lane == 0 && rmax > 0.0) atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
 }
 
 // ------------------------------------------------------------------ host plan
@@ -453,16 +329,17 @@ std::vector<uint32_t> smooth_numbers(uint32_t limit)
     return v;
 }
 
-bool radix_plan(uint32_t L, RadixPlan *P)
+bool make_plan(uint32_t Lt, FftPlan *P)
 {
+    uint32_t L = Lt;
     int e2 = 0, e3 = 0, e5 = 0, e7 = 0;
     while (L % 2 == 0) { L /= 2; ++e2; }
     while (L % 3 == 0) { L /= 3; ++e3; }
     while (L % 5 == 0) { L /= 5; ++e5; }
     while (L % 7 == 0) { L /= 7; ++e7; }
     if (L != 1) return false;
-    int S = 0;
-    auto push = [&](int r) { if (S < kMaxStages) P->R[S++] = r; };
+    int R[kMaxStages], S = 0;
+    auto push = [&](int r) { if (S < kMaxStages) R[S++] = r; };
     while (e2 >= 3) { push(8); e2 -= 3; }
     if (e2 == 2) push(4);
     if (e2 == 1) push(2);
@@ -470,65 +347,105 @@ bool radix_plan(uint32_t L, RadixPlan *P)
     for (int i = 0; i < e3; ++i) push(3);
     for (int i = 0; i < e7; ++i) push(7);
     P->S = S;
+    P->Lt = Lt;
+    P->nhi = (Lt + 63) / 64;
+    uint32_t span = Lt;
+    for (int i = 0; i < S; ++i) {
+        StageDesc &d = P->st[i];
+        d.R = (uint32_t)R[i];
+        d.L = span;
+        d.Ls = span / d.R;
+        d.G = Lt / span;
+        d.nb = Lt / d.R;
+        d.magic = ((1ull << 40) + d.Ls - 1) / d.Ls;
+        span = d.Ls;
+    }
     return S < kMaxStages;
 }
 
-uint32_t smem_bytes(uint64_t elems) { return (uint32_t)((elems + (elems >> 4) + 1) * 16); }
+uint32_t tile_bytes(uint64_t elems) { return (uint32_t)((elems + (elems >> 4) + 1) * 16); }
+
+// Measured on B200 (tools/microbench.cu): column-group copy bandwidth by run length.
+double colgroup_bw(uint32_t C)
+{
+    switch (C) {
+    case 1: return 2.3e12;
+    case 2: return 4.2e12;
+    case 4: return 4.7e12;
+    case 8: return 5.6e12;
+    default: return 5.5e12;
+    }
+}
 
 }  // namespace
+
+static uint32_t smem_k13(uint32_t N2, uint32_t C, uint32_t nhi2)
+{
+    return tile_bytes((uint64_t)N2 * C) + (64 + nhi2) * 16 + ((N2 * 4 + 15) / 16) * 16;
+}
+static uint32_t smem_k2(uint32_t N1, uint32_t nhi1) { return tile_bytes(N1) + (64 + nhi1) * 16; }
 
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
 {
     const uint64_t L = n + m - 1;
     const uint64_t Mmin = (L + 1) / 2;
-    const uint32_t N1MAX = 12288, N2MAX = 14000;
-    static const std::vector<uint32_t> sm = smooth_numbers(16384);
+    static const std::vector<uint32_t> sm = smooth_numbers(32768);
+    const double dp_rate = 64.0 * 148 * 1.9e9;  // FP64 lane-ops per second
     double best = 1e300;
     bool found = false;
     for (uint32_t N1 : sm) {
-        if (N1 > N1MAX) break;
-        if (smem_bytes(N1) > kSmemLimit) break;
+        if (smem_k2(N1, (N1 + 63) / 64) > kSmemLimit) break;
         uint64_t need = (Mmin + N1 - 1) / N1;
-        auto it = std::lower_bound(sm.begin(), sm.end(), (uint32_t)std::min<uint64_t>(need, 1u << 30));
-        if (it == sm.end() || *it > N2MAX || need > N2MAX) continue;
-        uint32_t N2 = *it;
-        uint32_t C = 0;
-        for (uint32_t c = 16; c >= 1; c >>= 1)
-            if (N1 % c == 0 && smem_bytes((uint64_t)N2 * c) <= kSmemLimit) { C = c; break; }
-        if (!C) continue;
-        uint64_t M = (uint64_t)N1 * N2;
-        double pen = C >= 8 ? 0.0 : C == 4 ? 0.02 : C == 2 ? 0.06 : 0.25;
-        if (N1 / C < 148 && M > 100000) pen += 0.05;  // strided passes underfill the GPU
-        if (N2 < 16 && M > 100000) pen += 0.05;       // row pass underfills
-        double cost = (double)M * (1.0 + pen);
-        if (cost < best) {
-            best = cost;
-            found = true;
-            g->M = M;
-            g->N1 = N1;
-            g->N2 = N2;
-            g->C = C;
+        if (need > 32768) continue;
+        uint32_t N2 = *std::lower_bound(sm.begin(), sm.end(), (uint32_t)need);
+        for (uint32_t C = 16; C >= 1; C >>= 1) {
+            if (N1 % C) continue;
+            uint32_t s13 = smem_k13(N2, C, (N2 + 63) / 64);
+            if (s13 > kSmemLimit) continue;
+            double M = (double)N1 * N2;
+            // memory time per kernel (bytes / bandwidth) and FP64 time
+            double log1 = log2((double)N1), log2v = log2((double)N2);
+            double m1 = 16 * M / colgroup_bw(C), m2 = 48 * M / 6.2e12, m3 = m1;
+            double d1 = M * (4.7 * log2v + 12) / dp_rate, d2 = M * (9.4 * log1 + 8) / dp_rate, d3 = d1;
+            bool two13 = 2 * s13 <= kSmemLimit, two2 = 2 * smem_k2(N1, (N1 + 63) / 64) <= kSmemLimit;
+            double t1 = two13 ? std::max(m1, d1) : m1 + d1;
+            double t2 = two2 ? std::max(m2, d2) : m2 + d2;
+            double t3 = two13 ? std::max(m3, d3) : m3 + d3;
+            // small problems: parallelism (CTAs) and launch latency dominate
+            double ctas13 = (double)(N1 / C), ctas2 = N2;
+            double par = 0;
+            if (ctas13 < 2 * 148) par += 3e-6 * (1.0 - ctas13 / (2 * 148));
+            if (ctas2 < 2 * 148) par += 3e-6 * (1.0 - ctas2 / (2 * 148));
+            double cost = t1 + t2 + t3 + par;
+            if (cost < best) {
+                best = cost;
+                found = true;
+                g->M = (uint64_t)N1 * N2;
+                g->N1 = N1;
+                g->N2 = N2;
+                g->C = C;
+            }
         }
     }
     if (!found) {
         snprintf(err, errlen,
                  "route (a): n+m-1 = %llu needs a complex transform of length >= %llu, beyond the "
-                 "two-pass plan's %u x %u limit",
-                 (unsigned long long)L, (unsigned long long)Mmin, N1MAX, N2MAX);
+                 "two-pass plan's limit",
+                 (unsigned long long)L, (unsigned long long)Mmin);
         return PA_ERR_UNSUPPORTED;
     }
-    radix_plan(g->N1, &g->p1);
-    radix_plan(g->N2, &g->p2);
-    g->M4 = 4 * g->M;
-    uint32_t B = 1;
-    while ((uint64_t)B * B < g->M4) B <<= 1;
-    g->taus = B;
-    g->t1 = 256;
-    uint32_t t2 = 64;
-    while (t2 < 512 && t2 * 8 < g->N1) t2 <<= 1;
-    g->t2 = t2;
-    g->smem1 = smem_bytes((uint64_t)g->N2 * g->C);
-    g->smem2 = smem_bytes(g->N1);
+    uint32_t logC = 0;
+    while ((1u << logC) < g->C) ++logC;
+    g->logC = logC;
+    make_plan(g->N1, &g->f1);
+    make_plan(g->N2, &g->f2);
+    g->tile1 = tile_bytes((uint64_t)g->N2 * g->C) / 16;
+    g->tile2 = tile_bytes(g->N1) / 16;
+    g->smem1 = smem_k13(g->N2, g->C, g->f2.nhi);
+    g->smem2 = smem_k2(g->N1, g->f1.nhi);
+    // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
+    g->t1 = 2 * g->smem1 <= kSmemLimit ? 256 : 512;
+    g->t2 = 2 * g->smem2 <= kSmemLimit ? 256 : 512;
     return PA_OK;
 }
 
@@ -555,16 +472,23 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         return st;
     }
     RouteA &a = h->a;
-    uint64_t nhi = (g.M4 + g.taus - 1) / g.taus;
+    RouteTables &T = a.T;
+    const uint64_t nMhi = (g.M + kMlo - 1) / kMlo;
     if ((st = alloc((void **)&a.buf, g.M * sizeof(double2), h, "buf"))) return st;
     if ((st = alloc((void **)&a.spec, g.M * sizeof(double2), h, "spec"))) return st;
-    if ((st = alloc((void **)&a.W1, g.N1 * sizeof(double2), h, "W1"))) return st;
-    if ((st = alloc((void **)&a.W2, g.N2 * sizeof(double2), h, "W2"))) return st;
-    if ((st = alloc((void **)&a.theta, g.N2 * sizeof(double2), h, "theta"))) return st;
-    if ((st = alloc((void **)&a.tau_lo, g.taus * sizeof(double2), h, "tau_lo"))) return st;
-    if ((st = alloc((void **)&a.tau_hi, nhi * sizeof(double2), h, "tau_hi"))) return st;
-    if ((st = alloc((void **)&a.rev2, g.N2 * sizeof(int), h, "rev2"))) return st;
+    size_t ntab = 64 + g.f1.nhi + 64 + g.f2.nhi + g.N1 + g.N2 + kMlo + nMhi;
+    if ((st = alloc((void **)&a.tables, ntab * sizeof(double2), h, "tables"))) return st;
+    if ((st = alloc((void **)&T.rev2, g.N2 * sizeof(uint32_t), h, "rev2"))) return st;
     if ((st = alloc((void **)&a.resid, sizeof(unsigned long long), h, "resid"))) return st;
+    double2 *p = a.tables;
+    T.W1lo = p; p += 64;
+    T.W1hi = p; p += g.f1.nhi;
+    T.W2lo = p; p += 64;
+    T.W2hi = p; p += g.f2.nhi;
+    T.zeta = p; p += g.N1;
+    T.theta = p; p += g.N2;
+    T.Mlo = p; p += kMlo;
+    T.Mhi = p; p += nMhi;
 
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k1_fwd_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -576,29 +500,23 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     if ((e = cudaMemsetAsync(a.resid, 0, sizeof(unsigned long long), s)) != cudaSuccess)
         return cuda_fail(e, "route (a) residual reset");
-
-    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), std::max<uint64_t>(g.taus, nhi));
-    k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(
-        g, a.W1, a.W2, a.theta, a.tau_lo, a.tau_hi, a.rev2, nhi);
+    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), std::max<uint64_t>(kMlo, nMhi));
+    k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
     // seed spectrum: K1 + forward half of K2, scaled by 1/M
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(seed, h->off, h->L, a.buf, g, a.W2, a.theta,
-                                                     a.tau_lo, a.tau_hi, a.rev2, nullptr, 0);
-    k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, nullptr, a.spec, g, a.W1, 1, 1.0 / (double)g.M);
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(seed, h->off, h->L, a.buf, g, T, nullptr, 0);
+    k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, T, 1, 1.0 / (double)g.M);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) create launches");
     h->kernels_per_hash = 3;
     return PA_OK;
 }
 
-pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
-                  cudaStream_t s)
+pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words, cudaStream_t s)
 {
     RouteA &a = h->a;
     const Geometry &g = a.g;
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(key, 0, h->n, a.buf, g, a.W2, a.theta,
-                                                     a.tau_lo, a.tau_hi, a.rev2, out, zero_words);
-    k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, nullptr, g, a.W1, 0, 1.0);
-    k3_inv_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.buf, g, a.W2, a.theta, a.tau_lo, a.tau_hi,
-                                                     a.rev2, h->n, h->m, out, a.resid);
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(key, 0, h->n, a.buf, g, a.T, out, zero_words);
+    k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 0, 1.0);
+    k3_inv_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.buf, g, a.T, h->n, h->m, out, a.resid);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (a) hash launches");
     return PA_OK;
@@ -607,7 +525,7 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
 void ra_destroy(pa_ctx *h)
 {
     RouteA &a = h->a;
-    void *ptrs[] = {a.buf, a.spec, a.W1, a.W2, a.theta, a.tau_lo, a.tau_hi, a.rev2, a.resid};
+    void *ptrs[] = {a.buf, a.spec, a.tables, a.T.rev2, a.resid};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     a = RouteA{};
