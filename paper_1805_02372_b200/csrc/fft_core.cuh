@@ -161,6 +161,16 @@ __device__ __forceinline__ double2 twiddle(const double2 *lo, const double2 *hi,
     return cmul(hi[e >> 6], lo[e & 63]);
 }
 
+// w[k] = w1^k, k = 1..R-1, by squaring (even k) or one more factor (odd k):
+// at most ~log2(R)+2 roundings deep (DESIGN.md error bound, twiddle term).
+template <int R>
+__device__ __forceinline__ void twiddle_powers(double2 *w, double2 w1)
+{
+    w[1] = w1;
+#pragma unroll
+    for (int k = 2; k < R; ++k) w[k] = (k & 1) ? cmul(w[k - 1], w1) : cmul(w[k / 2], w[k / 2]);
+}
+
 // One in-place stage over all butterflies of a batch of 2^logC sequences.
 //   DIF (forward): v = DFT_R(v); v_k *= omega_L^{jk}
 //   DIT (inverse): v_k *= conj omega_L^{jk}; v = IDFT_R(v)
@@ -182,13 +192,17 @@ __device__ __forceinline__ void stage_run(const StageDesc &sd, uint32_t logC, co
         if (!INV) {
             Dft<R, false>::run(v);
             if (j) {
+                double2 w[R];
+                twiddle_powers<R>(w, twiddle(wlo, whi, j * sd.G));
 #pragma unroll
-                for (int k = 1; k < R; ++k) v[k] = cmul(v[k], twiddle(wlo, whi, j * k * sd.G));
+                for (int k = 1; k < R; ++k) v[k] = cmul(v[k], w[k]);
             }
         } else {
             if (j) {
+                double2 w[R];
+                twiddle_powers<R>(w, twiddle(wlo, whi, j * sd.G));
 #pragma unroll
-                for (int k = 1; k < R; ++k) v[k] = cmulc(v[k], twiddle(wlo, whi, j * k * sd.G));
+                for (int k = 1; k < R; ++k) v[k] = cmulc(v[k], w[k]);
             }
             Dft<R, true>::run(v);
         }

@@ -26,9 +26,7 @@ struct Geometry {
 struct RouteTables {
     double2 *W1lo, *W1hi;   // omega_N1^e = W1hi[e >> 6] * W1lo[e & 63]
     double2 *W2lo, *W2hi;   // omega_N2^e
-    double2 *zeta;          // exp(i pi a / N), a < N1  (twist, N = 2M)
-    double2 *theta;         // exp(i pi b / (2 N2)), b < N2 (= zeta^{N1 b})
-    double2 *Mlo, *Mhi;     // omega_M^e = Mhi[e >> 12] * Mlo[e & 4095]
+    double2 *thlo, *thhi;   // theta_b = exp(i pi b / (2 N2)) = zeta^{N1 b}, two-level
     uint32_t *rev2;         // K1 DIF output position p -> frequency index k_b
 };
 

@@ -32,6 +32,7 @@
 //  * The seed goes through K1 and K2's forward half once at create.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -44,7 +45,6 @@ namespace pa {
 namespace {
 
 constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic shared memory per CTA
-constexpr uint32_t kMlo = 4096;          // omega_M^e = Mhi[e >> 12] * Mlo[e & 4095]
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
@@ -53,12 +53,23 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// tau(a, kb) = zeta^a * omega_M^{a kb};  a*kb < M < 2^32
-__device__ __forceinline__ double2 tau(const RouteTables &T, uint32_t a, uint32_t kb)
+// The four-step twiddle and the twist's column factor, tau(a, k_b) =
+// zeta^a omega_M^{a k_b} = rho^a with rho = exp(2 pi i (1 - 4 k_b) / 4M), are a
+// power of one per-row constant: K2 builds rho^e (e < 64) and rho^{64 h} in
+// shared memory with sincospi of the exact integer exponent.
+__device__ __forceinline__ void rho_tables(double2 *rlo, double2 *rhi, uint32_t nhi, uint64_t M, uint32_t kb)
 {
-    uint32_t e = a * kb;
-    double2 w = cmul(__ldg(T.Mhi + (e >> 12)), __ldg(T.Mlo + (e & (kMlo - 1))));
-    return cmul(w, __ldg(T.zeta + a));
+    const int64_t M4 = 4 * (int64_t)M;
+    const int64_t step = 1 - 4 * (int64_t)kb;  // exponent of rho in units of 2 pi i / 4M
+    for (uint32_t i = threadIdx.x; i < 64 + nhi; i += blockDim.x) {
+        int64_t e = (i < 64) ? (int64_t)i : 64 * (int64_t)(i - 64);
+        int64_t E = (e % M4) * (step % M4) % M4;
+        if (E < 0) E += M4;
+        double s, c;
+        sincospi((double)E / (double)(2 * M), &s, &c);
+        if (i < 64) rlo[i] = make_double2(c, s);
+        else rhi[i - 64] = make_double2(c, s);
+    }
 }
 
 __device__ __forceinline__ void load_tables(double2 *wlo, double2 *whi, const double2 *glo,
@@ -73,8 +84,7 @@ __device__ __forceinline__ void load_tables(double2 *wlo, double2 *whi, const do
 // ------------------------------------------------------------------ tables
 __global__ void k_tables(Geometry g, RouteTables T)
 {
-    const uint64_t nMhi = (g.M + kMlo - 1) / kMlo;
-    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), std::max<uint64_t>(kMlo, nMhi));
+    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < tot;
          e += (uint64_t)gridDim.x * blockDim.x) {
         double s, c;
@@ -92,13 +102,15 @@ __global__ void k_tables(Geometry g, RouteTables T)
             sincospi(2.0 * (double)(e * 64) / (double)g.N2, &s, &c);
             T.W2hi[e] = make_double2(c, -s);
         }
-        if (e < g.N1) {  // zeta^a = exp(i pi a / N), N = 2M
-            sincospi((double)e / (double)(2 * g.M), &s, &c);
-            T.zeta[e] = make_double2(c, s);
+        if (e < 64) {  // theta_b = exp(i pi b / (2 N2)) = thhi[b >> 6] * thlo[b & 63]
+            sincospi((double)e / (double)(2 * (uint64_t)g.N2), &s, &c);
+            T.thlo[e] = make_double2(c, s);
+        }
+        if (e < g.f2.nhi) {
+            sincospi((double)(64 * e) / (double)(2 * (uint64_t)g.N2), &s, &c);
+            T.thhi[e] = make_double2(c, s);
         }
         if (e < g.N2) {
-            sincospi((double)e / (double)(2 * (uint64_t)g.N2), &s, &c);
-            T.theta[e] = make_double2(c, s);
             // DIF output position e -> frequency index
             uint32_t rem = (uint32_t)e, L = g.N2, mult = 1, k = 0;
             for (int i = 0; i < g.f2.S; ++i) {
@@ -109,14 +121,6 @@ __global__ void k_tables(Geometry g, RouteTables T)
                 L = Ls;
             }
             T.rev2[e] = k;
-        }
-        if (e < kMlo) {
-            sincospi(2.0 * (double)e / (double)g.M, &s, &c);
-            T.Mlo[e] = make_double2(c, -s);
-        }
-        if (e < nMhi) {
-            sincospi(2.0 * (double)(e * kMlo) / (double)g.M, &s, &c);
-            T.Mhi[e] = make_double2(c, -s);
         }
     }
 }
@@ -129,8 +133,8 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
 {
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
-    double2 *wlo = sm + g.tile1, *whi = wlo + 64;
-    uint32_t *rowbits = reinterpret_cast<uint32_t *>(whi + g.f2.nhi);
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
+    uint32_t *rowbits = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
     const uint32_t a0 = blockIdx.x * C;
     const int64_t lo = (int64_t)off, hi = (int64_t)(off + nbits);
 
@@ -140,6 +144,7 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
             zero_out[i] = 0u;
     }
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     // per row b: C real-part bits (low half) and C imaginary-part bits (high half)
     const uint32_t cmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
     for (uint32_t b = threadIdx.x; b < g.N2; b += blockDim.x) {
@@ -152,13 +157,10 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
     auto ld_bits = [&](uint32_t b, uint32_t c) {
         uint32_t rb = rowbits[b];
         double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (16 + c)) & 1u);
-        double2 th = __ldg(T.theta + b);
+        double2 th = twiddle(thlo, thhi, b);
         return make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
     };
-    auto st_out = [&](uint32_t p, uint32_t c, double2 v) {
-        uint32_t a = a0 + c;
-        buf[(uint64_t)p * g.N1 + a] = cmul(v, tau(T, a, __ldg(T.rev2 + p)));
-    };
+    auto st_out = [&](uint32_t p, uint32_t c, double2 v) { buf[(uint64_t)p * g.N1 + a0 + c] = v; };
     if (g.f2.S == 0) {
         for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) st_out(0, c, ld_bits(0, c));
         return;
@@ -207,24 +209,33 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
 {
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
-    double2 *wlo = sm + g.tile2, *whi = wlo + 64;
+    double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi, *rhi = rlo + 64;
     const uint32_t row = blockIdx.x;
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *sp = spec + (uint64_t)row * N1;
     for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
     load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi);
+    rho_tables(rlo, rhi, g.f1.nhi, g.M, __ldg(T.rev2 + row));
     cp_async_wait_all();
     __syncthreads();
     auto lds = [&](uint32_t idx, uint32_t) { return sm[pidx(idx)]; };
     auto sts = [&](uint32_t idx, uint32_t, double2 v) { sm[pidx(idx)] = v; };
+    // tau on the way in (first DIF stage), conj tau on the way out (last DIT stage)
+    auto ld_tau = [&](uint32_t a, uint32_t) { return cmul(sm[pidx(a)], twiddle(rlo, rhi, a)); };
     const FftPlan &P = g.f1;
+    if (P.S <= 1) {  // N1 <= 8: apply tau elementwise
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = ld_tau(e, 0);
+        __syncthreads();
+    }
     if (mode == 1) {
         auto st_spec = [&](uint32_t idx, uint32_t, double2 v) { sp[idx] = cscale(v, scale); };
         if (P.S == 0) {
             if (threadIdx.x == 0) st_spec(0, 0, sm[0]);
-            return;
+        } else if (P.S == 1) {
+            dif_pass(P, 0, sm, wlo, whi, lds, st_spec);
+        } else {
+            dif_pass(P, 0, sm, wlo, whi, ld_tau, st_spec);
         }
-        dif_pass(P, 0, sm, wlo, whi, lds, st_spec);
         return;
     }
     if (P.S == 0) {
@@ -232,12 +243,13 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
         return;
     }
     for (int i = 0; i < P.S - 1; ++i) {
-        stage_any<false>(P.st[i], 0, wlo, whi, lds, sts);
+        if (i == 0) stage_any<false>(P.st[0], 0, wlo, whi, ld_tau, sts);
+        else stage_any<false>(P.st[i], 0, wlo, whi, lds, sts);
         __syncthreads();
     }
     fused_mid_any(P.st[P.S - 1], sm, sp);
     __syncthreads();
-    auto st_row = [&](uint32_t idx, uint32_t, double2 v) { rp[idx] = v; };
+    auto st_row = [&](uint32_t a, uint32_t, double2 v) { rp[a] = cmulc(v, twiddle(rlo, rhi, a)); };
     for (int i = P.S - 2; i >= 1; --i) {
         stage_any<true>(P.st[i], 0, wlo, whi, lds, sts);
         __syncthreads();
@@ -245,7 +257,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     if (P.S >= 2) {
         stage_any<true>(P.st[0], 0, wlo, whi, lds, st_row);
     } else {
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) rp[e] = sm[pidx(e)];
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) st_row(e, 0, sm[pidx(e)]);
     }
 }
 
@@ -256,18 +268,17 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
 {
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
-    double2 *wlo = sm + g.tile1, *whi = wlo + 64;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
     for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
         cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     cp_async_wait_all();
     __syncthreads();
 
-    auto ld_tau = [&](uint32_t p, uint32_t c) {
-        return cmulc(sm[pidx((p << logC) + c)], tau(T, a0 + c, __ldg(T.rev2 + p)));
-    };
+    auto ld_sm = [&](uint32_t p, uint32_t c) { return sm[pidx((p << logC) + c)]; };
     const int64_t t0 = (int64_t)n - 1;  // output window [t0, t0 + m)
     double rmax = 0.0;
     const uint32_t lane = threadIdx.x & 31;
@@ -290,7 +301,7 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
         }
     };
     auto st_epi = [&](uint32_t b, uint32_t c, double2 v) {
-        double2 wv = cmulc(v, __ldg(T.theta + b));
+        double2 wv = cmulc(v, twiddle(thlo, thhi, b));
         int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
         // real part -> t = u, imaginary part -> t = u + M
         bool inr = u >= t0 && u < t0 + (int64_t)m;
@@ -306,11 +317,11 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     if (g.f2.S == 0) {
         if (threadIdx.x < 32) {
             bool act = threadIdx.x < C;
-            double2 v = act ? ld_tau(0, threadIdx.x) : make_double2(0, 0);
+            double2 v = act ? ld_sm(0, threadIdx.x) : make_double2(0, 0);
             if (act) st_epi(0, threadIdx.x, v);
         }
     } else {
-        dit_pass(g.f2, logC, sm, wlo, whi, ld_tau, st_epi);
+        dit_pass(g.f2, logC, sm, wlo, whi, ld_sm, st_epi);
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, d));
@@ -381,9 +392,9 @@ double colgroup_bw(uint32_t C)
 
 static uint32_t smem_k13(uint32_t N2, uint32_t C, uint32_t nhi2)
 {
-    return tile_bytes((uint64_t)N2 * C) + (64 + nhi2) * 16 + ((N2 * 4 + 15) / 16) * 16;
+    return tile_bytes((uint64_t)N2 * C) + 2 * (64 + nhi2) * 16 + ((N2 * 4 + 15) / 16) * 16;
 }
-static uint32_t smem_k2(uint32_t N1, uint32_t nhi1) { return tile_bytes(N1) + (64 + nhi1) * 16; }
+static uint32_t smem_k2(uint32_t N1, uint32_t nhi1) { return tile_bytes(N1) + 2 * (64 + nhi1) * 16; }
 
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
 {
@@ -425,6 +436,20 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
                 g->N2 = N2;
                 g->C = C;
             }
+        }
+    }
+    // developer override for plan experiments: PA_FORCE_PLAN="N1,N2,C"
+    if (const char *fp = getenv("PA_FORCE_PLAN")) {
+        unsigned f1 = 0, f2 = 0, fc = 0;
+        FftPlan tmp;
+        if (sscanf(fp, "%u,%u,%u", &f1, &f2, &fc) == 3 && (uint64_t)f1 * f2 >= Mmin && fc >= 1 &&
+            fc <= 16 && (fc & (fc - 1)) == 0 && f1 % fc == 0 && make_plan(f1, &tmp) && make_plan(f2, &tmp) &&
+            smem_k2(f1, (f1 + 63) / 64) <= kSmemLimit && smem_k13(f2, fc, (f2 + 63) / 64) <= kSmemLimit) {
+            g->N1 = f1;
+            g->N2 = f2;
+            g->C = fc;
+            g->M = (uint64_t)f1 * f2;
+            found = true;
         }
     }
     if (!found) {
@@ -473,10 +498,9 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     }
     RouteA &a = h->a;
     RouteTables &T = a.T;
-    const uint64_t nMhi = (g.M + kMlo - 1) / kMlo;
     if ((st = alloc((void **)&a.buf, g.M * sizeof(double2), h, "buf"))) return st;
     if ((st = alloc((void **)&a.spec, g.M * sizeof(double2), h, "spec"))) return st;
-    size_t ntab = 64 + g.f1.nhi + 64 + g.f2.nhi + g.N1 + g.N2 + kMlo + nMhi;
+    size_t ntab = 64 + g.f1.nhi + 2 * (64 + g.f2.nhi);
     if ((st = alloc((void **)&a.tables, ntab * sizeof(double2), h, "tables"))) return st;
     if ((st = alloc((void **)&T.rev2, g.N2 * sizeof(uint32_t), h, "rev2"))) return st;
     if ((st = alloc((void **)&a.resid, sizeof(unsigned long long), h, "resid"))) return st;
@@ -485,10 +509,8 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     T.W1hi = p; p += g.f1.nhi;
     T.W2lo = p; p += 64;
     T.W2hi = p; p += g.f2.nhi;
-    T.zeta = p; p += g.N1;
-    T.theta = p; p += g.N2;
-    T.Mlo = p; p += kMlo;
-    T.Mhi = p; p += nMhi;
+    T.thlo = p; p += 64;
+    T.thhi = p; p += g.f2.nhi;
 
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k1_fwd_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -500,7 +522,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     if ((e = cudaMemsetAsync(a.resid, 0, sizeof(unsigned long long), s)) != cudaSuccess)
         return cuda_fail(e, "route (a) residual reset");
-    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), std::max<uint64_t>(kMlo, nMhi));
+    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
     k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
     // seed spectrum: K1 + forward half of K2, scaled by 1/M
     k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(seed, h->off, h->L, a.buf, g, T, nullptr, 0);
