@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py -- Toeplitz privacy-amplification throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+One step = one pass of the whole hot path (pa_hash: y = T x over GF(2)) over one
+synthetic n-bit key against a seed bound at pa_create, inputs resident in HBM.
+The workload at N = 1 is BASELINE.json configs[1] (C2: n = 1,000,003 key bits,
+m = 250,000 output bits).  For N > 1 (torchrun, one process per GPU) every rank
+hashes its own key of the same shape (independent keys -- weak scaling, no
+collective on the data path); the timed region is bracketed by a barrier and
+torch.cuda.synchronize() and the maximum over ranks is reported.
+
+Timing: W untimed warm-up steps, then K steps, each timed with CUDA events on the
+launching stream; the L2 is flushed (a 256 MiB buffer larger than the 126 MB L2
+is zeroed) before every step, outside the events.  value = n * keys / sum of step
+times (decimal Gbit/s of input key).  A second pass of K steps with libpa's
+per-launch event profiling gives the per-kernel times behind `roofline`.  `e2e`
+is the same metric through the public API with host buffers (pa_hash_host:
+pinned host key -> device -> hash -> host output, synchronised, every step).
+`cpu_baseline` is the CPU oracle (oracle/, OpenMP on all host cores) on the same
+workload.  --impl reference times that oracle as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import pa_synth as syn  # noqa: E402
+
+METRIC = "PA throughput, input Gbit/s vs input length n, 1/2/4/8 B200; % of HBM roofline"
+FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(syn.CONFIGS))
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C1/C3/C4 side measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline")
+    return ap.parse_args()
+
+
+def workload_desc(name):
+    c = syn.CONFIGS[name]
+    return f"{name}: {c['desc']} (n={c['n']}, m={c['m']})"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and clock-event reasons with NVML while the timed region runs."""
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+            0x10: "sync_boost", 0x1: "gpu_idle"}
+
+    def __init__(self, torch_device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(torch_device).uuid)
+            try:
+                self._h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(torch_device)
+            self._nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.error = repr(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for b, name in self.BITS.items():
+                    if r & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._h is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._h is not None:
+            self._t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def peak_hbm():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config, kernel):
+    """dram__bytes_read+write per launch of `kernel` from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+    try:
+        for d in json.load(open(path)):
+            if d.get("kernel") == kernel:
+                return float(d["dram_read"] + d["dram_write"]) * 1e9
+    except Exception:
+        pass
+    return None
+
+
+def alg_bytes(kernel, info):
+    """Algorithmic HBM bytes of one launch: M complex doubles = 16 M bytes."""
+    M = info["n1"] * info["n2"]
+    n, m = info["n"], info["m"]
+    return {"k1_fwd_columns": 16 * M + n / 8.0,            # key bits in, work array out
+            "k2_rows": 48 * M,                              # row in, spectrum in, row out
+            "k3_inv_columns": 16 * M + m / 8.0}.get(kernel)  # work array in, output bits out
+
+
+def dev_words(torch, w64, device):
+    w = np.ascontiguousarray(w64).view(np.int32)
+    pad = (-w.size) % 4
+    if pad:
+        w = np.concatenate([w, np.zeros(pad, np.int32)])
+    return torch.from_numpy(w.copy()).to(device)
+
+
+def time_steps(torch, fn, steps, flush):
+    """Per-step CUDA-event times (ms) with an L2 flush before each step (untimed)."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in ev:
+        flush.zero_()
+        e0.record()
+        fn()
+        e1.record()
+    torch.cuda.synchronize()
+    return [e0.elapsed_time(e1) for e0, e1 in ev]
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_02372_b200 as pa
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    name = args.config
+    n, m, sw, kw = syn.config_inputs(name, key_index=rank)
+    h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+    key = dev_words(torch, kw, dev)
+    out = h.new_out()
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        h.hash(key, out)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = time_steps(torch, step, args.steps, flush)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tot_ms = float(sum(ms))
+    # correctness spot check of the last output against the oracle (sampled rows)
+    verified = None
+    if rank == 0:
+        import oracle
+        rows = np.unique(np.concatenate([np.arange(64), np.arange(m - 64, m),
+                                         np.random.default_rng(1).integers(0, m, 256)]))
+        got = oracle.unpack(out.cpu().numpy().view(np.uint32), m)[rows]
+        verified = bool(np.array_equal(got, oracle.toeplitz_rows(n, m, sw, kw, rows)))
+
+    # profiled pass: per-kernel CUDA-event times of the same K steps
+    pa.pa_profile_enable(h.handle, True)
+    pa.pa_profile_read(h.handle)
+    prof_ms = time_steps(torch, step, args.steps, flush)
+    kern = pa.pa_profile_read(h.handle)
+    pa.pa_profile_enable(h.handle, False)
+
+    # end to end through the public API with host buffers
+    key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
+    out_h = torch.empty(pa.words32(m), dtype=torch.int32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    e2e_ms = time_steps(torch, lambda: h.hash_host(key_h, out_h), e2e_steps, flush)
+
+    # max over ranks
+    t = torch.tensor([tot_ms, float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms, e2e_mean = float(t[0]), float(t[1])
+
+    line = None
+    if rank == 0:
+        info = h.info
+        units = world * args.steps
+        value = n * units / (tot_ms * 1e-3) / 1e9
+        e2e_value = n * world / (e2e_mean * 1e-3) / 1e9
+        # roofline of the dominant kernel
+        roof = None
+        per = {k: v[1] / max(1, v[0]) for k, v in kern.items()}
+        if per:
+            top = max(per, key=per.get)
+            peak, peak_src = peak_hbm()
+            if top == "k_toeplitz_bitpacked":
+                # ALU bound: 2 ALU ops (SHF + LOP3) per 32 bit-products, 64 lanes/clk/SM
+                bp = float(n) * m
+                achieved = bp / (per[top] * 1e-3) / 1e12
+                alu_peak = 1024 * 148 * (info.get("sm_max_mhz") or 1965) * 1e6 / 1e12
+                roof = {"kernel": top, "bound": "alu", "achieved": achieved, "peak": alu_peak,
+                        "unit": "Tbit-products/s", "frac": achieved / alu_peak, "traffic": None,
+                        "peak_source": "derived: 148 SMs x 64 ALU lanes/clk x 16 bit-products/op x 1.965 GHz"}
+            else:
+                b = alg_bytes(top, info)
+                achieved = b / (per[top] * 1e-3) / 1e9
+                traffic = ncu_traffic(name, top)
+                roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": b,
+                        "avg_launch_us": per[top] * 1e3, "peak_source": peak_src,
+                        "note": "achieved = algorithmic bytes / CUDA-event launch time; the working "
+                                "set of small configs is partly L2-resident, so frac can exceed HBM"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if info["route"] == 1 else "u32",
+            "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits (SURVEY 8(d) streams)",
+            "config": {"workload": workload_desc(name), "n": n, "m": m, "keys_per_rank": 1,
+                       "route": h.route, "transform_len": info["transform_len"], "n1": info["n1"],
+                       "n2": info["n2"], "cols_per_cta": info["cols_per_cta"],
+                       "parallelism": f"independent keys x {world} GPU(s), no data-path collective",
+                       "l2": "flushed before every step (256 MiB memset, untimed)", "verified": verified},
+            "roofline": roof,
+            "kernels_us": {k: v[1] / max(1, v[0]) * 1e3 for k, v in kern.items()},
+            "profiled_ms_per_step": float(np.mean(prof_ms)),
+            "e2e": {"value": e2e_value, "unit": "Gbit/s", "h2d_bytes_per_step": 4 * pa.words32(n),
+                    "d2h_bytes_per_step": 4 * pa.words32(m), "steps": e2e_steps,
+                    "how": "pa_hash_host: pinned host key -> H2D -> 3 kernels -> D2H -> stream sync, CUDA events"},
+            "gpu_launches": args.steps * info["kernels_per_hash"],
+            "clocks": clk.result(),
+        }
+    h.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def sweep(torch, pa, dev, steps=10):
+    """Side measurements (rank 0, N = 1): other BASELINE configs, same protocol."""
+    res = {}
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    for name in ("C1", "C3", "C4"):
+        n, m, sw, kw = syn.config_inputs(name)
+        h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+        key = dev_words(torch, kw, dev)
+        out = h.new_out()
+        for _ in range(3):
+            h.hash(key, out)
+        ms = time_steps(torch, lambda: h.hash(key, out), steps, flush)
+        t = float(np.mean(ms))
+        res[name] = {"n": n, "m": m, "route": h.route, "ms_per_hash": t, "gbit_s": n / (t * 1e-3) / 1e9,
+                     "transform_len": h.info["transform_len"], "residual": h.residual()}
+        h.close()
+    return res
+
+
+def cpu_oracle_baseline(name, budget_s=12.0, max_rows=None):
+    """The CPU oracle (as it stands) on the same workload, all host cores."""
+    import oracle
+    n, m, sw, kw = syn.config_inputs(name)
+    cores = oracle.max_threads()
+    rows = np.arange(m if max_rows is None else min(m, max_rows), dtype=np.uint64)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.toeplitz_rows(n, m, sw, kw, rows)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 50:
+            break
+    per_row = el / (reps * rows.size)
+    t_full = per_row * m
+    return {"value": n / t_full / 1e9, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
+            "sample": f"{name} rows [0,{rows.size}) of m={m} x {reps} repeats ({el:.1f} s, "
+                      f"word-level direct GF(2) product, OpenMP); value extrapolated per full hash"
+                      if rows.size < m else
+                      f"{name} full hash (all {m} rows) x {reps} repeats ({el:.1f} s, word-level direct "
+                      f"GF(2) product, OpenMP)",
+            "seconds_per_hash": t_full}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    name = args.config
+    n, m, sw, kw = syn.config_inputs(name)
+    cores = oracle.max_threads()
+    # size each step so the whole run takes ~1-2 minutes: estimate one row's cost
+    probe = np.arange(min(m, 2000), dtype=np.uint64)
+    t0 = time.perf_counter()
+    oracle.toeplitz_rows(n, m, sw, kw, probe)
+    per_row = (time.perf_counter() - t0) / probe.size
+    budget = 90.0 / max(1, args.steps + args.warmup)
+    nrows = int(max(64, min(m, budget / max(per_row, 1e-9))))
+    rows = np.arange(nrows, dtype=np.uint64)
+    for _ in range(args.warmup):
+        oracle.toeplitz_rows(n, m, sw, kw, rows)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.toeplitz_rows(n, m, sw, kw, rows)
+        ts.append(time.perf_counter() - t0)
+    t_full = float(np.sum(ts)) / args.steps * (m / nrows)
+    value = n / t_full / 1e9
+    sample = (f"{name}: rows [0,{nrows}) of m={m} per step (full hash extrapolated x{m / nrows:.2f}), "
+              f"word-level direct GF(2) oracle, OpenMP {cores} threads")
+    return {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "impl": "reference",
+            "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits",
+            "config": {"workload": workload_desc(name), "n": n, "m": m, "keys_per_rank": 1},
+            "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        line = run_reference(args)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    line = run_ours(args)
+    if line is None:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1:
+        import torch
+
+        import paper_1805_02372_b200 as pa
+        if not args.no_sweep:
+            line["sweep"] = sweep(torch, pa, torch.device("cuda", 0))
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_oracle_baseline(args.config)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -135,6 +135,20 @@ pa_status pa_residual(pa_handle h, double *max_residual, void *stream);
 
 pa_status pa_get_info(pa_handle h, pa_info *info);
 
+/* Per-kernel device timing (for bench.py's roofline): while enabled, every
+ * kernel libpa launches for this handle is bracketed by a CUDA event pair on
+ * the launching stream.  pa_profile_read synchronises those events, returns
+ * up to `max` entries {kernel name, launches, total milliseconds} accumulated
+ * since the previous read, and resets the counters. */
+typedef struct pa_kernel_time {
+    char name[32];
+    uint64_t launches;
+    double total_ms;
+} pa_kernel_time;
+
+pa_status pa_profile_enable(pa_handle h, int enable);
+pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32_t *count);
+
 /* Stream-ordered release of everything the handle owns.  Safe on NULL. */
 void pa_destroy(pa_handle h);
 

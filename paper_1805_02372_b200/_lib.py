@@ -31,7 +31,8 @@ PA_RESIDUAL_LIMIT = 0.25
 
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
-            "pa_destroy", "pa_last_error", "pa_status_string", "pa_version"]
+            "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
+            "pa_profile_read"]
 
 
 class PaError(RuntimeError):
@@ -53,6 +54,10 @@ class pa_info(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class pa_kernel_time(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -77,6 +82,9 @@ _sig = {
     "pa_last_error": (ctypes.c_char_p, []),
     "pa_status_string": (ctypes.c_char_p, [_st]),
     "pa_version": (ctypes.c_uint32, []),
+    "pa_profile_enable": (_st, [_H, ctypes.c_int]),
+    "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
+                              ctypes.POINTER(ctypes.c_uint32)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -157,3 +165,15 @@ def pa_get_info(h: int) -> dict:
 
 def pa_destroy(h: int) -> None:
     _lib.pa_destroy(h)
+
+
+def pa_profile_enable(h: int, enable: bool) -> None:
+    _check(_lib.pa_profile_enable(h, 1 if enable else 0))
+
+
+def pa_profile_read(h: int) -> dict:
+    """{kernel name: (launches, total_ms)} accumulated since the last read."""
+    arr = (pa_kernel_time * 8)()
+    n = ctypes.c_uint32()
+    _check(_lib.pa_profile_read(h, arr, 8, ctypes.byref(n)))
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(n.value)}

@@ -1,6 +1,9 @@
 """Build libpa.so (the C-ABI library of include/pa.h) for sm_100a, in-tree.
 
-    python -m paper_1805_02372_b200.build [--verbose]
+    python paper_1805_02372_b200/build.py [--force] [--verbose]
+
+(run as a script or load it by path: importing the package itself loads
+libpa.so, so the builder must not depend on the package being importable)
 
 Compiles every .cu under csrc/ with nvcc
 (-gencode arch=compute_100a,code=sm_100a -lineinfo -O3) and links one shared

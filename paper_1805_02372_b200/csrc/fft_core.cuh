@@ -171,13 +171,15 @@ __device__ __forceinline__ void twiddle_powers(double2 *w, double2 w1)
     for (int k = 2; k < R; ++k) w[k] = (k & 1) ? cmul(w[k - 1], w1) : cmul(w[k / 2], w[k / 2]);
 }
 
-// One in-place stage over all butterflies of a batch of 2^logC sequences.
+// One in-place stage over all butterflies of a batch of 2^logC sequences held
+// in padded shared memory (element idx of sequence c at pidx((idx << logC) + c)).
 //   DIF (forward): v = DFT_R(v); v_k *= omega_L^{jk}
 //   DIT (inverse): v_k *= conj omega_L^{jk}; v = IDFT_R(v)
-// ld(idx, c) returns element idx of sequence c; st(idx, c, v) stores it.
-template <int R, bool INV, class LD, class ST>
-__device__ __forceinline__ void stage_run(const StageDesc &sd, uint32_t logC, const double2 *wlo,
-                                          const double2 *whi, LD &ld, ST &st)
+// Not inlined: one copy per (R, direction) per kernel keeps the code small
+// enough for the instruction cache.
+template <int R, bool INV>
+__device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
+                                        const double2 *whi)
 {
     const uint32_t nb = sd.nb << logC;
     const uint32_t cm = (1u << logC) - 1;
@@ -185,10 +187,11 @@ __device__ __forceinline__ void stage_run(const StageDesc &sd, uint32_t logC, co
         const uint32_t c = q & cm, t = q >> logC;
         const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
         const uint32_t j = t - g * sd.Ls;
-        const uint32_t base = g * sd.L + j;
+        const uint32_t base = ((g * sd.L + j) << logC) + c;
+        const uint32_t stride = sd.Ls << logC;
         double2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = ld(base + r * sd.Ls, c);
+        for (int r = 0; r < R; ++r) v[r] = sm[pidx(base + r * stride)];
         if (!INV) {
             Dft<R, false>::run(v);
             if (j) {
@@ -207,65 +210,42 @@ __device__ __forceinline__ void stage_run(const StageDesc &sd, uint32_t logC, co
             Dft<R, true>::run(v);
         }
 #pragma unroll
-        for (int r = 0; r < R; ++r) st(base + r * sd.Ls, c, v[r]);
+        for (int r = 0; r < R; ++r) sm[pidx(base + r * stride)] = v[r];
     }
 }
 
-template <bool INV, class LD, class ST>
-__device__ __forceinline__ void stage_any(const StageDesc &sd, uint32_t logC, const double2 *wlo,
-                                          const double2 *whi, LD &ld, ST &st)
+template <bool INV>
+__device__ __forceinline__ void stage_any(double2 *sm, const StageDesc &sd, uint32_t logC, const double2 *wlo,
+                                          const double2 *whi)
 {
     switch (sd.R) {
-    case 2: stage_run<2, INV>(sd, logC, wlo, whi, ld, st); break;
-    case 3: stage_run<3, INV>(sd, logC, wlo, whi, ld, st); break;
-    case 4: stage_run<4, INV>(sd, logC, wlo, whi, ld, st); break;
-    case 5: stage_run<5, INV>(sd, logC, wlo, whi, ld, st); break;
-    case 7: stage_run<7, INV>(sd, logC, wlo, whi, ld, st); break;
-    default: stage_run<8, INV>(sd, logC, wlo, whi, ld, st); break;
+    case 2: stage_smem<2, INV>(sm, sd, logC, wlo, whi); break;
+    case 3: stage_smem<3, INV>(sm, sd, logC, wlo, whi); break;
+    case 4: stage_smem<4, INV>(sm, sd, logC, wlo, whi); break;
+    case 5: stage_smem<5, INV>(sm, sd, logC, wlo, whi); break;
+    case 7: stage_smem<7, INV>(sm, sd, logC, wlo, whi); break;
+    default: stage_smem<8, INV>(sm, sd, logC, wlo, whi); break;
     }
 }
 
-// A whole forward DIF over stages [0, S): stage 0 loads with ld0, the last stores
-// with stN, the rest go through shared memory `sm` (batch layout).  Ends without
-// a barrier after the last stage (its stores may go anywhere).
-template <class LD0, class STN>
-__device__ __forceinline__ void dif_pass(const FftPlan &P, uint32_t logC, double2 *sm, const double2 *wlo,
-                                         const double2 *whi, LD0 &ld0, STN &stN)
+// Stages [i0, i1) of the forward DIF (natural -> digit-reversed), barrier after each.
+__device__ __forceinline__ void dif_stages(double2 *sm, const FftPlan &P, int i0, int i1, uint32_t logC,
+                                           const double2 *wlo, const double2 *whi)
 {
-    auto lds = [&](uint32_t idx, uint32_t c) { return sm[pidx((idx << logC) + c)]; };
-    auto sts = [&](uint32_t idx, uint32_t c, double2 v) { sm[pidx((idx << logC) + c)] = v; };
-    if (P.S == 1) {
-        stage_any<false>(P.st[0], logC, wlo, whi, ld0, stN);
-        return;
-    }
-    stage_any<false>(P.st[0], logC, wlo, whi, ld0, sts);
-    __syncthreads();
-    for (int i = 1; i < P.S - 1; ++i) {
-        stage_any<false>(P.st[i], logC, wlo, whi, lds, sts);
+    for (int i = i0; i < i1; ++i) {
+        stage_any<false>(sm, P.st[i], logC, wlo, whi);
         __syncthreads();
     }
-    stage_any<false>(P.st[P.S - 1], logC, wlo, whi, lds, stN);
 }
 
-// A whole inverse DIT (stages S-1 .. 0): the first (stage S-1) loads with ld0,
-// stage 0 stores with stN.
-template <class LD0, class STN>
-__device__ __forceinline__ void dit_pass(const FftPlan &P, uint32_t logC, double2 *sm, const double2 *wlo,
-                                         const double2 *whi, LD0 &ld0, STN &stN)
+// Stages i1-1 down to i0 of the inverse DIT (digit-reversed -> natural), barrier after each.
+__device__ __forceinline__ void dit_stages(double2 *sm, const FftPlan &P, int i0, int i1, uint32_t logC,
+                                           const double2 *wlo, const double2 *whi)
 {
-    auto lds = [&](uint32_t idx, uint32_t c) { return sm[pidx((idx << logC) + c)]; };
-    auto sts = [&](uint32_t idx, uint32_t c, double2 v) { sm[pidx((idx << logC) + c)] = v; };
-    if (P.S == 1) {
-        stage_any<true>(P.st[0], logC, wlo, whi, ld0, stN);
-        return;
-    }
-    stage_any<true>(P.st[P.S - 1], logC, wlo, whi, ld0, sts);
-    __syncthreads();
-    for (int i = P.S - 2; i >= 1; --i) {
-        stage_any<true>(P.st[i], logC, wlo, whi, lds, sts);
+    for (int i = i1 - 1; i >= i0; --i) {
+        stage_any<true>(sm, P.st[i], logC, wlo, whi);
         __syncthreads();
     }
-    stage_any<true>(P.st[0], logC, wlo, whi, lds, stN);
 }
 
 }  // namespace pa

@@ -2,6 +2,7 @@
 // selection and dispatch.  No exceptions cross this boundary.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -68,6 +69,69 @@ static pa_status check_dev_ptr(const void *p, const char *name, int device)
     return PA_OK;
 }
 
+static cudaEvent_t prof_event(Profiler &P)
+{
+    if (P.npool > 0) return P.pool[--P.npool];
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(pa_ctx *h, int k, cudaStream_t s)
+{
+    Profiler &P = h->prof;
+    if (!P.on) return;
+    if (P.npend == P.cap) {
+        int nc = P.cap ? 2 * P.cap : 64;
+        Profiler::Pending *np = (Profiler::Pending *)realloc(P.pend, nc * sizeof *np);
+        if (!np) return;
+        P.pend = np;
+        P.cap = nc;
+    }
+    Profiler::Pending &q = P.pend[P.npend++];
+    q.k = k;
+    q.e0 = prof_event(P);
+    q.e1 = nullptr;
+    cudaEventRecord(q.e0, s);
+}
+
+void prof_end(pa_ctx *h, cudaStream_t s)
+{
+    Profiler &P = h->prof;
+    if (!P.on || P.npend == 0 || P.pend[P.npend - 1].e1) return;
+    Profiler::Pending &q = P.pend[P.npend - 1];
+    q.e1 = prof_event(P);
+    cudaEventRecord(q.e1, s);
+}
+
+static void prof_release(Profiler &P, cudaEvent_t e)
+{
+    if (!e) return;
+    if (P.npool == P.poolcap) {
+        int nc = P.poolcap ? 2 * P.poolcap : 128;
+        cudaEvent_t *np = (cudaEvent_t *)realloc(P.pool, nc * sizeof *np);
+        if (!np) {
+            cudaEventDestroy(e);
+            return;
+        }
+        P.pool = np;
+        P.poolcap = nc;
+    }
+    P.pool[P.npool++] = e;
+}
+
+static void prof_free(Profiler &P)
+{
+    for (int i = 0; i < P.npend; ++i) {
+        if (P.pend[i].e0) cudaEventDestroy(P.pend[i].e0);
+        if (P.pend[i].e1) cudaEventDestroy(P.pend[i].e1);
+    }
+    for (int i = 0; i < P.npool; ++i) cudaEventDestroy(P.pool[i]);
+    free(P.pend);
+    free(P.pool);
+    P = Profiler{};
+}
+
 }  // namespace pa
 
 using namespace pa;
@@ -109,6 +173,7 @@ void pa_destroy(pa_handle h)
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(h->device);
+    prof_free(h->prof);
     ra_destroy(h);
     rb_destroy(h);
     if (h->stage_key) cudaFree(h->stage_key);
@@ -316,6 +381,54 @@ pa_status pa_residual(pa_handle h, double *max_residual, void *stream)
         set_error("FP64 residual %.3e exceeds PA_RESIDUAL_LIMIT %.2f", r, PA_RESIDUAL_LIMIT);
         return PA_ERR_PRECISION;
     }
+    return PA_OK;
+}
+
+pa_status pa_profile_enable(pa_handle h, int enable)
+{
+    if (!h) {
+        set_error("pa_profile_enable: handle is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    h->prof.on = enable != 0;
+    return PA_OK;
+}
+
+pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32_t *count)
+{
+    if (!h || (!out && max) || !count) {
+        set_error("pa_profile_read: NULL argument");
+        return PA_ERR_INVALID_ARG;
+    }
+    Profiler &P = h->prof;
+    for (int i = 0; i < P.npend; ++i) {
+        Profiler::Pending &q = P.pend[i];
+        if (q.e0 && q.e1) {
+            cudaError_t e = cudaEventSynchronize(q.e1);
+            if (e != cudaSuccess) return cuda_fail(e, "pa_profile_read");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, q.e0, q.e1);
+            P.launches[q.k] += 1;
+            P.total_ms[q.k] += ms;
+        }
+        prof_release(P, q.e0);
+        prof_release(P, q.e1);
+    }
+    P.npend = 0;
+    uint32_t n = 0;
+    for (int k = 0; k < Profiler::kKernels; ++k) {
+        if (!P.launches[k]) continue;
+        if (n < max) {
+            memset(out[n].name, 0, sizeof out[n].name);
+            strncpy(out[n].name, P.names[k], sizeof out[n].name - 1);
+            out[n].launches = P.launches[k];
+            out[n].total_ms = P.total_ms[k];
+        }
+        ++n;
+        P.launches[k] = 0;
+        P.total_ms[k] = 0;
+    }
+    *count = n < max ? n : max;
     return PA_OK;
 }
 

@@ -47,6 +47,23 @@ struct RouteB {
 
 }  // namespace pa
 
+namespace pa {
+// launch-bracketing CUDA events for pa_profile_* (kernel k = index into names)
+struct Profiler {
+    bool on = false;
+    static constexpr int kKernels = 8;
+    const char *names[kKernels] = {"k1_fwd_columns", "k2_rows", "k3_inv_columns",
+                                   "k_toeplitz_bitpacked", "", "", "", ""};
+    struct Pending { int k; cudaEvent_t e0, e1; };
+    Pending *pend = nullptr;
+    int npend = 0, cap = 0;
+    cudaEvent_t *pool = nullptr;
+    int npool = 0, poolcap = 0;
+    uint64_t launches[kKernels] = {};
+    double total_ms[kKernels] = {};
+};
+}  // namespace pa
+
 struct pa_ctx {
     int device = 0;
     uint64_t n = 0, m = 0, L = 0, off = 0;
@@ -57,6 +74,7 @@ struct pa_ctx {
     uint64_t kernels_per_hash = 0;
     // pointer-validation cache (pa_hash called repeatedly with the same buffers)
     const void *ok_key = nullptr, *ok_out = nullptr;
+    pa::Profiler prof;
     // staging for pa_hash_host
     uint32_t *stage_key = nullptr, *stage_out = nullptr;
 };
@@ -77,6 +95,9 @@ pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
 void rb_destroy(pa_ctx *h);
 
 void set_error(const char *fmt, ...);
+// bracket one kernel launch with profiling events (no-ops unless enabled)
+void prof_begin(pa_ctx *h, int k, cudaStream_t s);
+void prof_end(pa_ctx *h, cudaStream_t s);
 pa_status cuda_fail(cudaError_t e, const char *what);
 
 }  // namespace pa

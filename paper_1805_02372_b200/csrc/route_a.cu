@@ -137,6 +137,7 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
     uint32_t *rowbits = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
     const uint32_t a0 = blockIdx.x * C;
     const int64_t lo = (int64_t)off, hi = (int64_t)(off + nbits);
+    const uint32_t tot = g.N2 << logC;
 
     if (zero_out) {  // K3 ORs this hash's output bits in
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
@@ -146,7 +147,7 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     // per row b: C real-part bits (low half) and C imaginary-part bits (high half)
-    const uint32_t cmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
+    const uint32_t cmask = (1u << C) - 1u;
     for (uint32_t b = threadIdx.x; b < g.N2; b += blockDim.x) {
         int64_t P = (int64_t)a0 + (int64_t)g.N1 * b + lo;
         uint32_t re = bits32(w, P, lo, hi) & cmask;
@@ -154,24 +155,25 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
         rowbits[b] = re | (im << 16);
     }
     __syncthreads();
-    auto ld_bits = [&](uint32_t b, uint32_t c) {
+    // z(b, c) = (x[a + N1 b] + i x[a + N1 b + M]) * theta_b
+    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
+        uint32_t b = e >> logC, c = e & (C - 1);
         uint32_t rb = rowbits[b];
         double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (16 + c)) & 1u);
         double2 th = twiddle(thlo, thhi, b);
-        return make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
-    };
-    auto st_out = [&](uint32_t p, uint32_t c, double2 v) { buf[(uint64_t)p * g.N1 + a0 + c] = v; };
-    if (g.f2.S == 0) {
-        for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) st_out(0, c, ld_bits(0, c));
-        return;
+        sm[pidx(e)] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
     }
-    dif_pass(g.f2, logC, sm, wlo, whi, ld_bits, st_out);
+    __syncthreads();
+    dif_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    // row p of the work array = DIF output position p (k_b = rev2[p])
+    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
+        buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
 }
 
 // ------------------------------------------------------------------ K2
 // Fused last DIF stage (Ls = 1, no twiddles) * spectrum * first DIT stage.
 template <int R>
-__device__ __forceinline__ void fused_mid(const StageDesc &sd, double2 *sm, const double2 *__restrict__ sp)
+__device__ __noinline__ void fused_mid(StageDesc sd, double2 *sm, const double2 *__restrict__ sp)
 {
     for (uint32_t gq = threadIdx.x; gq < sd.nb; gq += blockDim.x) {
         const uint32_t base = gq * R;
@@ -201,8 +203,8 @@ __device__ __forceinline__ void fused_mid_any(const StageDesc &sd, double2 *sm, 
     }
 }
 
-// mode 0 (hash): in place, buf row -> DIF, * spec, DIT -> buf row.
-// mode 1 (create): buf row -> DIF -> * scale -> spec row.
+// mode 0 (hash): in place, buf row -> tau -> DIF, * spec, DIT -> conj tau -> buf row.
+// mode 1 (create): buf row -> tau -> DIF -> * scale -> spec row.
 __global__ void __launch_bounds__(512)
 k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, RouteTables T, int mode,
         double scale)
@@ -218,47 +220,24 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     rho_tables(rlo, rhi, g.f1.nhi, g.M, __ldg(T.rev2 + row));
     cp_async_wait_all();
     __syncthreads();
-    auto lds = [&](uint32_t idx, uint32_t) { return sm[pidx(idx)]; };
-    auto sts = [&](uint32_t idx, uint32_t, double2 v) { sm[pidx(idx)] = v; };
-    // tau on the way in (first DIF stage), conj tau on the way out (last DIT stage)
-    auto ld_tau = [&](uint32_t a, uint32_t) { return cmul(sm[pidx(a)], twiddle(rlo, rhi, a)); };
+    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
+    __syncthreads();
     const FftPlan &P = g.f1;
-    if (P.S <= 1) {  // N1 <= 8: apply tau elementwise
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = ld_tau(e, 0);
-        __syncthreads();
-    }
     if (mode == 1) {
-        auto st_spec = [&](uint32_t idx, uint32_t, double2 v) { sp[idx] = cscale(v, scale); };
-        if (P.S == 0) {
-            if (threadIdx.x == 0) st_spec(0, 0, sm[0]);
-        } else if (P.S == 1) {
-            dif_pass(P, 0, sm, wlo, whi, lds, st_spec);
-        } else {
-            dif_pass(P, 0, sm, wlo, whi, ld_tau, st_spec);
-        }
+        dif_stages(sm, P, 0, P.S, 0, wlo, whi);
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sp[e] = cscale(sm[pidx(e)], scale);
         return;
     }
     if (P.S == 0) {
-        if (threadIdx.x == 0) rp[0] = cmul(sm[0], sp[0]);
-        return;
-    }
-    for (int i = 0; i < P.S - 1; ++i) {
-        if (i == 0) stage_any<false>(P.st[0], 0, wlo, whi, ld_tau, sts);
-        else stage_any<false>(P.st[i], 0, wlo, whi, lds, sts);
-        __syncthreads();
-    }
-    fused_mid_any(P.st[P.S - 1], sm, sp);
-    __syncthreads();
-    auto st_row = [&](uint32_t a, uint32_t, double2 v) { rp[a] = cmulc(v, twiddle(rlo, rhi, a)); };
-    for (int i = P.S - 2; i >= 1; --i) {
-        stage_any<true>(P.st[i], 0, wlo, whi, lds, sts);
-        __syncthreads();
-    }
-    if (P.S >= 2) {
-        stage_any<true>(P.st[0], 0, wlo, whi, lds, st_row);
+        if (threadIdx.x == 0) sm[0] = cmul(sm[0], sp[0]);
     } else {
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) st_row(e, 0, sm[pidx(e)]);
+        dif_stages(sm, P, 0, P.S - 1, 0, wlo, whi);
+        fused_mid_any(P.st[P.S - 1], sm, sp);
+        __syncthreads();
+        dit_stages(sm, P, 0, P.S - 1, 0, wlo, whi);
     }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) rp[e] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
 }
 
 // ------------------------------------------------------------------ K3
@@ -277,51 +256,40 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     cp_async_wait_all();
     __syncthreads();
+    dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
 
-    auto ld_sm = [&](uint32_t p, uint32_t c) { return sm[pidx((p << logC) + c)]; };
-    const int64_t t0 = (int64_t)n - 1;  // output window [t0, t0 + m)
-    double rmax = 0.0;
+    // epilogue: element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
+    const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;  // output window [t0, t1)
     const uint32_t lane = threadIdx.x & 31;
-    auto emit = [&](int64_t i0, bool odd, uint32_t c) {
-        // i0 = output bit index of this element; runs of C lanes hold C consecutive bits
-        bool valid = odd && i0 >= 0 && i0 < (int64_t)m;
-        uint32_t bal = __ballot_sync(__activemask(), valid);
-        if (c == 0) {
-            uint32_t run = (bal >> lane) & ((C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u));
-            if (run) {
+    const uint32_t runmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
+    double rmax = 0.0;
+    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
+        const uint32_t b = e >> logC, c = e & (C - 1);
+        const double2 wv = cmulc(sm[pidx(e)], twiddle(thlo, thhi, b));
+        const int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            const int64_t tt = part ? u + (int64_t)g.M : u;
+            const double v = part ? wv.y : wv.x;
+            const bool in = tt >= t0 && tt < t1;
+            const double r = rint(v);
+            if (in) rmax = fmax(rmax, fabs(v - r));
+            const bool bit = in && (((long long)r) & 1);
+            const uint32_t bal = __ballot_sync(__activemask(), bit);
+            // lanes c = 0..C-1 of a run hold C consecutive output bits starting at i0
+            uint32_t run = (bal >> (lane - c)) & runmask;
+            if (c == 0 && run) {
+                int64_t i0 = tt - t0;
                 if (i0 < 0) {
                     run >>= (int)(-i0);
                     i0 = 0;
                 }
-                uint64_t wd = (uint64_t)i0 >> 5;
-                int sh = (int)(i0 & 31);
+                const uint64_t wd = (uint64_t)i0 >> 5;
+                const int sh = (int)(i0 & 31);
                 atomicOr(out + wd, run << sh);
                 if (sh && (run >> (32 - sh))) atomicOr(out + wd + 1, run >> (32 - sh));
             }
         }
-    };
-    auto st_epi = [&](uint32_t b, uint32_t c, double2 v) {
-        double2 wv = cmulc(v, twiddle(thlo, thhi, b));
-        int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
-        // real part -> t = u, imaginary part -> t = u + M
-        bool inr = u >= t0 && u < t0 + (int64_t)m;
-        double rr = rint(wv.x);
-        if (inr) rmax = fmax(rmax, fabs(wv.x - rr));
-        emit(u - t0, inr && (((long long)rr) & 1), c);
-        int64_t ui = u + (int64_t)g.M;
-        bool ini = ui >= t0 && ui < t0 + (int64_t)m;
-        double ri = rint(wv.y);
-        if (ini) rmax = fmax(rmax, fabs(wv.y - ri));
-        emit(ui - t0, ini && (((long long)ri) & 1), c);
-    };
-    if (g.f2.S == 0) {
-        if (threadIdx.x < 32) {
-            bool act = threadIdx.x < C;
-            double2 v = act ? ld_sm(0, threadIdx.x) : make_double2(0, 0);
-            if (act) st_epi(0, threadIdx.x, v);
-        }
-    } else {
-        dit_pass(g.f2, logC, sm, wlo, whi, ld_sm, st_epi);
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, d));
@@ -536,9 +504,15 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
 {
     RouteA &a = h->a;
     const Geometry &g = a.g;
+    prof_begin(h, 0, s);
     k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(key, 0, h->n, a.buf, g, a.T, out, zero_words);
+    prof_end(h, s);
+    prof_begin(h, 1, s);
     k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 0, 1.0);
+    prof_end(h, s);
+    prof_begin(h, 2, s);
     k3_inv_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.buf, g, a.T, h->n, h->m, out, a.resid);
+    prof_end(h, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (a) hash launches");
     return PA_OK;

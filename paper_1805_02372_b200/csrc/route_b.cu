@@ -122,7 +122,9 @@ pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
         gy = (KW + KC - 1) / KC;
     }
     dim3 grid((unsigned)gx, (unsigned)gy);
+    prof_begin(h, 3, s);
     k_toeplitz_bitpacked<<<grid, kThreadsB, 0, s>>>(key, h->n, h->m, h->b.sr, out, Q, KW, KC);
+    prof_end(h, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (b) kernel launch");
     return PA_OK;

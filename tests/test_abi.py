@@ -17,11 +17,15 @@ def _declared():
     return sorted(set(re.findall(r"\b(pa_[a-z0-9_]+)\s*\(", src)))
 
 
-@pytest.fixture(scope="module")
+@pytest.fixture(scope="module", autouse=True)
 def lib():
-    from paper_1805_02372_b200 import build
-    build.build()
-    return ctypes.CDLL(build.LIB)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "pa_build", os.path.join(ROOT, "paper_1805_02372_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    b.build()
+    return ctypes.CDLL(b.LIB)
 
 
 def test_header_declares_the_north_star_calls():
