@@ -75,7 +75,9 @@ typedef struct pa_options {
     int32_t route;            /* pa_route */
     uint64_t seed_bit_offset; /* the handle uses seed bits [off, off+n+m-1) of the
                                  caller's seed buffer (row/column shards) */
-    uint32_t reserved[8];     /* must be zero */
+    uint32_t allow_wide;      /* 1 = accept m > n (column shards of the Eq. (4) split,
+                                 P:107-110, have n_g < m); default 0 keeps 1 <= m <= n */
+    uint32_t reserved[7];     /* must be zero */
 } pa_options;
 
 /* Runtime facts about a handle (all lengths in bits or elements). */
@@ -95,7 +97,7 @@ pa_status pa_options_init(pa_options *opt);
 
 /* Create a hashing context for n-bit keys and m-bit outputs with the
  * (n+m-1)-bit seed at `seed_bits` (device, ceil((off+n+m-1)/32) uint32 words
- * readable).  Requires 1 <= m <= n (SPEC reading R7).  The seed is consumed
+ * readable).  Requires 1 <= m <= n (reading R7) unless opt->allow_wide.  The seed is consumed
  * on `stream` during create (route (a) transforms it once into a cached
  * spectrum; route (b) stores it bit-reversed); the caller may free it after
  * the stream passes this call.  On success *h owns all device memory it

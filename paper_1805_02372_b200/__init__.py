@@ -56,13 +56,14 @@ class Hasher:
     """One pa_handle: fixed (n, m, seed); hash any number of n-bit keys."""
 
     def __init__(self, n: int, m: int, seed: torch.Tensor, route: str = "auto",
-                 seed_bit_offset: int = 0, stream=None):
+                 seed_bit_offset: int = 0, stream=None, allow_wide: bool = False):
         _need_cuda(seed, "seed", seed_bit_offset + n + m - 1)
         self.n, self.m = int(n), int(m)
         self.device = seed.device
         opt = pa_options_init()
         opt.route = ROUTES[route]
         opt.seed_bit_offset = int(seed_bit_offset)
+        opt.allow_wide = 1 if allow_wide else 0
         with torch.cuda.device(self.device):
             self._h = pa_create_ex(self.n, self.m, seed.data_ptr(), opt, _stream_ptr(stream))
         self.info = pa_get_info(self._h)

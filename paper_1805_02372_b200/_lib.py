@@ -43,7 +43,8 @@ class PaError(RuntimeError):
 
 class pa_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("route", ctypes.c_int32),
-                ("seed_bit_offset", ctypes.c_uint64), ("reserved", ctypes.c_uint32 * 8)]
+                ("seed_bit_offset", ctypes.c_uint64), ("allow_wide", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 7)]
 
 
 class pa_info(ctypes.Structure):

@@ -190,15 +190,6 @@ pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *s
         return PA_ERR_INVALID_ARG;
     }
     *out = nullptr;
-    if (n == 0 || m == 0 || m > n) {
-        set_error("need 1 <= m <= n, got n = %llu, m = %llu", (unsigned long long)n,
-                  (unsigned long long)m);
-        return PA_ERR_INVALID_ARG;
-    }
-    if (n > (1ull << 40)) {
-        set_error("n = %llu bits exceeds the supported 2^40", (unsigned long long)n);
-        return PA_ERR_UNSUPPORTED;
-    }
     pa_options o;
     pa_options_init(&o);
     if (opt) {
@@ -209,11 +200,25 @@ pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *s
         }
         o = *opt;
     }
+    if (n == 0 || m == 0 || (m > n && !o.allow_wide)) {
+        set_error("need 1 <= m <= n (or opt->allow_wide), got n = %llu, m = %llu",
+                  (unsigned long long)n, (unsigned long long)m);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (n > (1ull << 40) || m > (1ull << 40)) {
+        set_error("n = %llu, m = %llu: lengths beyond 2^40 bits are unsupported",
+                  (unsigned long long)n, (unsigned long long)m);
+        return PA_ERR_UNSUPPORTED;
+    }
     if (o.route < PA_ROUTE_AUTO || o.route > PA_ROUTE_BITPACKED) {
         set_error("opt->route = %d is not a pa_route", o.route);
         return PA_ERR_INVALID_ARG;
     }
-    for (int i = 0; i < 8; ++i)
+    if (o.allow_wide > 1) {
+        set_error("opt->allow_wide = %u must be 0 or 1", o.allow_wide);
+        return PA_ERR_INVALID_ARG;
+    }
+    for (int i = 0; i < 7; ++i)
         if (o.reserved[i]) {
             set_error("opt->reserved[%d] = %u must be 0", i, o.reserved[i]);
             return PA_ERR_INVALID_ARG;

@@ -1,0 +1,171 @@
+"""Multi-GPU partitioning of one Toeplitz hash (one process per GPU, torch.distributed).
+
+Three exact decompositions of y = T x (Eq. (1)):
+
+* Output-row split (BASELINE.json configs[3]): rank g owns rows [r0, r1) and its
+  own handle on the seed window s[r0 : r1 + n - 1] (pa_options.seed_bit_offset
+  = r0), hashes the whole key, and the m-bit result is assembled with one NCCL
+  all-gather (every rank ends with all of y).
+* Input-column split (the paper's Eq. (4) block division, with the
+  Eq. (7) modulo-2 merge): rank g owns key bits [c0, c1) and the seed
+  window s[n - c1 : n - c0 + m - 1]; partial m-bit hashes are XOR-reduced.  NCCL
+  has no XOR reduction (nccl.h: Sum/Prod/Max/Min/Avg), so the merge is an
+  all-gather of the packed partials followed by an XOR fold (exact, order-free).
+* Independent keys (configs[4]): keys are dealt round-robin; no collective on
+  the data path.
+
+The split arithmetic (`row_ranges`, `col_ranges`, window offsets, bit packing of
+shard keys) is host logic; all hashing runs in libpa on each rank's GPU.  With
+the gloo backend and CPU tensors the same driver runs in CI through an injected
+`hash_fn` (see tests/test_dist_cpu.py) -- never on the product path.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+WORD = 32
+
+
+def split_even(total: int, parts: int) -> list[tuple[int, int]]:
+    """[a, b) ranges covering [0, total) in `parts` nearly equal contiguous pieces."""
+    q, r = divmod(total, parts)
+    out, a = [], 0
+    for g in range(parts):
+        b = a + q + (1 if g < r else 0)
+        out.append((a, b))
+        a = b
+    return out
+
+
+def row_ranges(m: int, world: int) -> list[tuple[int, int]]:
+    """Output rows per rank, each a multiple of 32 except the last (word-aligned
+    gather: every rank's slice starts on a uint32 boundary of y)."""
+    words = (m + WORD - 1) // WORD
+    out = []
+    for a, b in split_even(words, world):
+        out.append((min(m, a * WORD), min(m, b * WORD)))
+    return out
+
+
+def row_seed_offset(r0: int) -> int:
+    """Row block [r0, r1) uses seed bits [r0, r1 + n - 1): T[i][j] = s[i-j+n-1]."""
+    return r0
+
+
+def col_ranges(n: int, m: int, world: int) -> list[tuple[int, int]]:
+    """Key-bit blocks per rank (n_g may be < m: the handles use pa_options.allow_wide)."""
+    return split_even(n, world)
+
+
+def col_seed_offset(n: int, c0: int, c1: int) -> int:
+    """Key block [c0, c1) (n_g = c1 - c0 bits) uses seed bits [n - c1, n - c0 + m - 1)."""
+    return n - c1
+
+
+def extract_bits(words: np.ndarray, start: int, count: int) -> np.ndarray:
+    """Bits [start, start+count) of an LSB-first uint32/uint64 array, repacked into uint32
+    words starting at bit 0 (host-side shard preparation)."""
+    b = np.unpackbits(np.ascontiguousarray(words).view(np.uint8), bitorder="little")[start:start + count]
+    pad = np.zeros(((count + WORD - 1) // WORD) * WORD, np.uint8)
+    pad[:count] = b
+    return np.packbits(pad, bitorder="little").view(np.uint32)
+
+
+def _words4(nbits: int) -> int:
+    w = (nbits + WORD - 1) // WORD
+    return (w + 3) // 4 * 4
+
+
+class _LibpaHash:
+    """hash_fn backed by libpa on this rank's GPU (the product path)."""
+
+    def __init__(self):
+        from . import Hasher
+        self._Hasher = Hasher
+        self._cache = {}
+
+    def __call__(self, n, m, seed_t, seed_off, key_t):
+        k = (n, m, seed_t.data_ptr(), seed_off)
+        h = self._cache.get(k)
+        if h is None:
+            h = self._Hasher(n, m, seed_t, seed_bit_offset=seed_off, allow_wide=m > n)
+            self._cache[k] = h
+        return h.hash(key_t)
+
+    def close(self):
+        for h in self._cache.values():
+            h.close()
+        self._cache.clear()
+
+
+def hash_rows(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=None,
+              hash_fn: Callable | None = None) -> torch.Tensor:
+    """Output-row split: returns all ceil(m/32) words of y on every rank."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    ranges = row_ranges(m, world)
+    r0, r1 = ranges[rank]
+    hf = hash_fn or _LibpaHash()
+    span = (ranges[0][1] - ranges[0][0]) // WORD  # words per slice (all but the last equal)
+    span = max(span, max((b - a + WORD - 1) // WORD for a, b in ranges))
+    mine = torch.zeros(span, dtype=torch.int32, device=key_t.device)
+    if r1 > r0:
+        part = hf(n, r1 - r0, seed_t, row_seed_offset(r0), key_t)
+        w = (r1 - r0 + WORD - 1) // WORD
+        mine[:w] = part[:w]
+    gathered = torch.empty(world * span, dtype=torch.int32, device=key_t.device)
+    dist.all_gather_into_tensor(gathered, mine, group=group)
+    words = (m + WORD - 1) // WORD
+    out = torch.zeros(words, dtype=torch.int32, device=key_t.device)
+    for g, (a, b) in enumerate(ranges):
+        if b > a:
+            wa, wb = a // WORD, (b + WORD - 1) // WORD
+            out[wa:wb] = gathered[g * span: g * span + (wb - wa)]
+    if hash_fn is None:
+        hf.close()
+    return out
+
+
+def hash_cols(n: int, m: int, seed_t: torch.Tensor, key_words: np.ndarray, group=None,
+              hash_fn: Callable | None = None, device=None) -> torch.Tensor:
+    """Input-column split with XOR merge: returns all ceil(m/32) words of y on every rank.
+    key_words: the full key (host, LSB-first); each rank uploads only its block."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    c0, c1 = col_ranges(n, m, world)[rank]
+    words = (m + WORD - 1) // WORD
+    dev = device if device is not None else seed_t.device
+    hf = hash_fn or _LibpaHash()
+    mine = torch.zeros(words, dtype=torch.int32, device=dev)
+    if c1 > c0:
+        blk = extract_bits(key_words, c0, c1 - c0)
+        kt = torch.zeros(_words4(c1 - c0), dtype=torch.int32)
+        kt[:blk.size] = torch.from_numpy(blk.view(np.int32))
+        part = hf(c1 - c0, m, seed_t, col_seed_offset(n, c0, c1), kt.to(dev))
+        mine[:] = part[:words]
+    gathered = torch.empty(world * words, dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(gathered, mine, group=group)
+    out = gathered.view(world, words)[0].clone()
+    for g in range(1, world):
+        out ^= gathered.view(world, words)[g]
+    if hash_fn is None:
+        hf.close()
+    return out
+
+
+def hash_keys(n: int, m: int, seed_t: torch.Tensor, keys: torch.Tensor, group=None,
+              hash_fn: Callable | None = None) -> tuple[list[int], torch.Tensor]:
+    """Independent keys: rank g hashes keys g, g+W, g+2W, ... of `keys` ((count, words)).
+    Returns (indices, outputs) for this rank; no data-path collective."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    idx = list(range(rank, keys.shape[0], world))
+    hf = hash_fn or _LibpaHash()
+    outs = torch.zeros((len(idx), _words4(m)), dtype=torch.int32, device=keys.device)
+    for i, k in enumerate(idx):
+        o = hf(n, m, seed_t, 0, keys[k].contiguous())
+        outs[i, :o.numel()] = o[: outs.shape[1]]
+    if hash_fn is None:
+        hf.close()
+    return idx, outs

@@ -56,7 +56,7 @@ def test_version_and_status_strings():
 
 def test_struct_layouts_match_header():
     import paper_1805_02372_b200._lib as L
-    assert ctypes.sizeof(L.pa_options) == 4 + 4 + 8 + 32
+    assert ctypes.sizeof(L.pa_options) == 4 + 4 + 8 + 4 + 28
     assert ctypes.sizeof(L.pa_info) == 8 * 2 + 4 * 2 + 8 * 6
     o = L.pa_options_init()
     assert o.struct_size == ctypes.sizeof(L.pa_options) and o.route == 0

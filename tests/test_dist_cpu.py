@@ -1,0 +1,92 @@
+"""Multi-process (gloo, world_size 2 and 3, CPU) tests of the multi-GPU split logic in
+paper_1805_02372_b200.dist: row split + all-gather, column split + XOR merge, and
+independent-key dealing reassemble exactly the single-device hash.  The per-rank
+hash is injected (the CPU oracle) -- this tests the partition arithmetic and the
+collectives, the GPU kernels are covered by tests/test_parity_gpu.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import pa_synth as syn
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_hash(n, m, seed_t, seed_off, key_t):
+    """hash_fn with libpa's calling convention, computed by the oracle on the CPU."""
+    from paper_1805_02372_b200.dist import extract_bits
+    sw = extract_bits(seed_t.numpy().view(np.uint32), seed_off, n + m - 1)
+    kw = extract_bits(key_t.numpy().view(np.uint32), 0, n)
+    y = oracle.toeplitz_words(n, m, sw, kw)
+    w = (m + 31) // 32
+    return torch.from_numpy(y.view(np.int32)[:w].copy())
+
+
+def _worker(rank, world, port, n, m, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1805_02372_b200 import dist as pd
+        sw = syn.random_bits(syn.seed_stream(77), n + m - 1)
+        kw = syn.random_bits(syn.key_stream(77, 0), n)
+        seed_t = torch.from_numpy(sw.view(np.int32).copy())
+        key_t = torch.from_numpy(kw.view(np.int32).copy())
+        rows = pd.hash_rows(n, m, seed_t, key_t, hash_fn=oracle_hash)
+        cols = pd.hash_cols(n, m, seed_t, kw, hash_fn=oracle_hash, device=torch.device("cpu"))
+        keys = torch.stack([torch.from_numpy(syn.random_bits(syn.key_stream(78, k), n).view(np.int32).copy())
+                            for k in range(5)])
+        idx, outs = pd.hash_keys(n, m, seed_t, keys, hash_fn=oracle_hash)
+        q.put((rank, rows.numpy().copy(), cols.numpy().copy(), idx, outs.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,m", [(2, 3001, 700), (2, 4096, 1024), (3, 2000, 1500), (3, 1000, 999)])
+def test_splits_reassemble(world, n, m):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sw = syn.random_bits(syn.seed_stream(77), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(77, 0), n)
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    for rank, rows, cols, idx, outs in res:
+        assert np.array_equal(oracle.unpack(rows.view(np.uint32), m), want), ("rows", rank)
+        assert np.array_equal(oracle.unpack(cols.view(np.uint32), m), want), ("cols", rank)
+        for i, k in enumerate(idx):
+            wk = oracle.unpack(oracle.toeplitz_words(n, m, sw, syn.random_bits(syn.key_stream(78, k), n)), m)
+            assert np.array_equal(oracle.unpack(outs[i].view(np.uint32), m), wk), ("keys", rank, k)
+    dealt = sorted(k for r in res for k in r[3])
+    assert dealt == list(range(5))
+
+
+def test_range_helpers():
+    from paper_1805_02372_b200 import dist as pd
+    for m in (1, 31, 32, 33, 1000, 20_000_000):
+        for w in (1, 2, 3, 8):
+            rr = pd.row_ranges(m, w)
+            assert rr[0][0] == 0 and rr[-1][1] == m
+            assert all(a % 32 == 0 or a == b == m for a, b in rr)
+            assert all(rr[i][1] == rr[i + 1][0] for i in range(w - 1))
+    cr = pd.col_ranges(10, 3, 4)
+    assert cr[0][0] == 0 and cr[-1][1] == 10 and sum(b - a for a, b in cr) == 10
+    assert pd.col_seed_offset(100, 20, 50) == 50
