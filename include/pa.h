@@ -137,6 +137,11 @@ pa_status pa_residual(pa_handle h, double *max_residual, void *stream);
 
 pa_status pa_get_info(pa_handle h, pa_info *info);
 
+/* Host-only planning query (no device work, no handle): fills the route, the
+ * transform length and the N1 x N2 split pa_create would choose for (n, m) with
+ * default options.  workspace_bytes is the device memory the handle would own. */
+pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info);
+
 /* Per-kernel device timing (for bench.py's roofline): while enabled, every
  * kernel libpa launches for this handle is bracketed by a CUDA event pair on
  * the launching stream.  pa_profile_read synchronises those events, returns

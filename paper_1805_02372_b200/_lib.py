@@ -13,7 +13,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpa.so")
+LIB_PATH = os.environ.get("PA_LIB", os.path.join(HERE, "libpa.so"))
 
 PA_OK = 0
 PA_ERR_INVALID_ARG = 1
@@ -32,7 +32,7 @@ PA_RESIDUAL_LIMIT = 0.25
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
-            "pa_profile_read"]
+            "pa_profile_read", "pa_plan"]
 
 
 class PaError(RuntimeError):
@@ -84,6 +84,7 @@ _sig = {
     "pa_status_string": (ctypes.c_char_p, [_st]),
     "pa_version": (ctypes.c_uint32, []),
     "pa_profile_enable": (_st, [_H, ctypes.c_int]),
+    "pa_plan": (_st, [_u64, _u64, ctypes.POINTER(pa_info)]),
     "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
                               ctypes.POINTER(ctypes.c_uint32)]),
 }
@@ -178,3 +179,10 @@ def pa_profile_read(h: int) -> dict:
     n = ctypes.c_uint32()
     _check(_lib.pa_profile_read(h, arr, 8, ctypes.byref(n)))
     return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(n.value)}
+
+
+def pa_plan(n: int, m: int) -> dict:
+    """Host-only: the plan pa_create would choose for (n, m)."""
+    info = pa_info()
+    _check(_lib.pa_plan(n, m, ctypes.byref(info)))
+    return info.as_dict()

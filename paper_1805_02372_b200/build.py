@@ -19,11 +19,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-LIB = os.path.join(HERE, "libpa.so")
+LIB = os.environ.get("PA_LIB_OUT", os.path.join(HERE, "libpa.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-         "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
+         "-Xptxas", "-O3", "--expt-relaxed-constexpr"] + os.environ.get("PA_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -88,6 +88,52 @@ template <bool INV> struct Dft<8, INV> {
     }
 };
 
+// radix 16 as 4 x 4: n = 4 n2 + n1, k = k1 + 4 k2,
+// X[k1 + 4 k2] = sum_n1 w4^{n1 k2} w16^{n1 k1} sum_n2 w4^{n2 k1} v[4 n2 + n1]
+template <bool INV> struct Dft<16, INV> {
+    __device__ __forceinline__ static double2 w16(int e)
+    {
+        const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+        double2 w;
+        switch (e) {  // exp(-2 pi i e / 16), e in {1,2,3,4,6,9}
+        case 1: w = make_double2(c1, -s1); break;
+        case 2: w = make_double2(h, -h); break;
+        case 3: w = make_double2(s1, -c1); break;
+        case 4: w = make_double2(0.0, -1.0); break;
+        case 6: w = make_double2(-h, -h); break;
+        default: w = make_double2(-c1, s1); break;  // 9
+        }
+        if (INV) w.y = -w.y;
+        return w;
+    }
+    __device__ __forceinline__ static void run(double2 *v)
+    {
+        double2 y[4][4];
+#pragma unroll
+        for (int n1 = 0; n1 < 4; ++n1) {
+            double2 q[4] = {v[n1], v[4 + n1], v[8 + n1], v[12 + n1]};
+            Dft<4, INV>::run(q);
+#pragma unroll
+            for (int k1 = 0; k1 < 4; ++k1) y[n1][k1] = q[k1];
+        }
+#pragma unroll
+        for (int n1 = 1; n1 < 4; ++n1)
+#pragma unroll
+            for (int k1 = 1; k1 < 4; ++k1) {
+                const int e = n1 * k1;
+                if (e == 4) y[n1][k1] = INV ? mul_pi(y[n1][k1]) : mul_mi(y[n1][k1]);
+                else y[n1][k1] = cmul(y[n1][k1], w16(e));
+            }
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            double2 q[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+            Dft<4, INV>::run(q);
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = q[k2];
+        }
+    }
+};
+
 // cos/sin(2 pi t / R), t = 1..R-1, odd R (20 significant digits)
 template <int R> struct Trig;
 template <> struct Trig<3> {
@@ -161,70 +207,136 @@ __device__ __forceinline__ double2 twiddle(const double2 *lo, const double2 *hi,
     return cmul(hi[e >> 6], lo[e & 63]);
 }
 
-// w[k] = w1^k, k = 1..R-1, by squaring (even k) or one more factor (odd k):
-// at most ~log2(R)+2 roundings deep (DESIGN.md error bound, twiddle term).
-template <int R>
-__device__ __forceinline__ void twiddle_powers(double2 *w, double2 w1)
+template <int R, bool INV>
+__device__ __forceinline__ void butterfly(double2 *v, uint32_t j, const StageDesc &sd, const double2 *wlo,
+                                          const double2 *whi)
 {
-    w[1] = w1;
+    if (!INV) Dft<R, false>::run(v);
+    if (j) {
+        // w_k = w1^k by a running product (k - 1 <= 15 roundings deep: DESIGN.md Sec. 5)
+        const double2 w1 = twiddle(wlo, whi, j * sd.G);
+        double2 w = w1;
 #pragma unroll
-    for (int k = 2; k < R; ++k) w[k] = (k & 1) ? cmul(w[k - 1], w1) : cmul(w[k / 2], w[k / 2]);
+        for (int k = 1; k < R; ++k) {
+            v[k] = INV ? cmulc(v[k], w) : cmul(v[k], w);
+            if (k + 1 < R) w = cmul(w, w1);
+        }
+    }
+    if (INV) Dft<R, true>::run(v);
 }
+
+// Where a stage's inputs come from and its outputs go (the first and last stage
+// of a pass are fused with the pass's load / store / epilogue):
+//   MODE_PLAIN     smem -> smem
+//   MODE_TAU_IN    smem * rho^idx -> smem              (K2 first forward stage)
+//   MODE_TAU_OUT   smem -> conj(rho^idx) * . -> gout[idx]   (K2 last inverse stage)
+//   MODE_BITS_IN   key bits (rowbits[b]) * theta_b -> smem (K1 first stage)
+//   MODE_COLS_OUT  smem -> gcols[idx * N1 + a0 + c]     (K1 last stage)
+//   MODE_EPI       smem -> untwist, window, rint, parity, ballot-pack, atomicOr (K3 last stage)
+enum { MODE_PLAIN = 0, MODE_TAU_IN = 1, MODE_TAU_OUT = 2, MODE_BITS_IN = 3, MODE_COLS_OUT = 4, MODE_EPI = 5 };
+struct StageCtx {
+    const double2 *rlo = nullptr, *rhi = nullptr;    // rho tables (K2)
+    double2 *gout = nullptr;                         // K2 row in global memory
+    const uint32_t *rowbits = nullptr;               // K1: re bits | im bits << 16 per row
+    const double2 *thlo = nullptr, *thhi = nullptr;  // theta_b two-level tables (K1, K3)
+    double2 *gcols = nullptr;                        // K1 work array
+    uint32_t N1 = 0, a0 = 0, C = 1;
+    uint32_t *out = nullptr;                         // K3 output bits
+    int64_t t0 = 0, t1 = 0, M = 0;                   // K3 window [t0, t1), complex length
+    int64_t blo = 0, bhi = 0;                        // K3 rows that can hold window bits
+};
 
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
 // in padded shared memory (element idx of sequence c at pidx((idx << logC) + c)).
 //   DIF (forward): v = DFT_R(v); v_k *= omega_L^{jk}
 //   DIT (inverse): v_k *= conj omega_L^{jk}; v = IDFT_R(v)
-// Not inlined: one copy per (R, direction) per kernel keeps the code small
-// enough for the instruction cache.
-template <int R, bool INV>
-__device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
-                                        const double2 *whi)
+// Not inlined: one copy per (R, direction, mode) per kernel keeps the code in
+// the instruction cache.  Returns the largest rounding residual (MODE_EPI).
+template <int R, bool INV, int MODE>
+__device__ __noinline__ double stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
+                                          const double2 *whi, StageCtx x)
 {
     const uint32_t nb = sd.nb << logC;
     const uint32_t cm = (1u << logC) - 1;
+    const uint32_t stride = sd.Ls << logC;
+    const uint32_t lane = threadIdx.x & 31;
+    double rmax = 0.0;
     for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
         const uint32_t c = q & cm, t = q >> logC;
         const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
         const uint32_t j = t - g * sd.Ls;
-        const uint32_t base = ((g * sd.L + j) << logC) + c;
-        const uint32_t stride = sd.Ls << logC;
+        const uint32_t idx0 = g * sd.L + j;
+        const uint32_t base = (idx0 << logC) + c;
         double2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = sm[pidx(base + r * stride)];
-        if (!INV) {
-            Dft<R, false>::run(v);
-            if (j) {
-                double2 w[R];
-                twiddle_powers<R>(w, twiddle(wlo, whi, j * sd.G));
-#pragma unroll
-                for (int k = 1; k < R; ++k) v[k] = cmul(v[k], w[k]);
+        for (int r = 0; r < R; ++r) {
+            const uint32_t idx = idx0 + r * sd.Ls;
+            if (MODE == MODE_BITS_IN) {
+                const uint32_t rb = x.rowbits[idx];
+                const double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (16 + c)) & 1u);
+                const double2 th = twiddle(x.thlo, x.thhi, idx);
+                v[r] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
+            } else {
+                v[r] = sm[pidx(base + r * stride)];
+                if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx));
             }
-        } else {
-            if (j) {
-                double2 w[R];
-                twiddle_powers<R>(w, twiddle(wlo, whi, j * sd.G));
-#pragma unroll
-                for (int k = 1; k < R; ++k) v[k] = cmulc(v[k], w[k]);
-            }
-            Dft<R, true>::run(v);
         }
+        butterfly<R, INV>(v, j, sd, wlo, whi);
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[pidx(base + r * stride)] = v[r];
+        for (int r = 0; r < R; ++r) {
+            const uint32_t idx = idx0 + r * sd.Ls;
+            if (MODE == MODE_TAU_OUT) {
+                x.gout[idx] = cmulc(v[r], twiddle(x.rlo, x.rhi, idx));
+            } else if (MODE == MODE_COLS_OUT) {
+                x.gcols[(uint64_t)idx * x.N1 + x.a0 + c] = v[r];
+            } else if (MODE == MODE_EPI) {
+                // element (b = idx, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
+                const bool rowok = (int64_t)idx >= x.blo && (int64_t)idx < x.bhi;
+                const double2 wv = cmulc(v[r], twiddle(x.thlo, x.thhi, idx));
+                const int64_t u = (int64_t)x.a0 + c + (int64_t)x.N1 * idx;
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                    const int64_t tt = part ? u + x.M : u;
+                    const double val = part ? wv.y : wv.x;
+                    const bool in = rowok && tt >= x.t0 && tt < x.t1;
+                    const double rr = rint(val);
+                    if (in) rmax = fmax(rmax, fabs(val - rr));
+                    const bool bit = in && (((long long)rr) & 1);
+                    const uint32_t bal = __ballot_sync(__activemask(), bit);
+                    // lanes c = 0..C-1 of a run hold C consecutive output bits
+                    uint32_t run = (bal >> (lane - c)) & ((x.C == 32) ? 0xFFFFFFFFu : ((1u << x.C) - 1u));
+                    if (c == 0 && run) {
+                        int64_t i0 = tt - x.t0;
+                        if (i0 < 0) {
+                            run >>= (int)(-i0);
+                            i0 = 0;
+                        }
+                        const uint64_t wd = (uint64_t)i0 >> 5;
+                        const int sh = (int)(i0 & 31);
+                        atomicOr(x.out + wd, run << sh);
+                        if (sh && (run >> (32 - sh))) atomicOr(x.out + wd + 1, run >> (32 - sh));
+                    }
+                }
+            } else {
+                sm[pidx(base + r * stride)] = v[r];
+            }
+        }
     }
+    return rmax;
 }
 
-template <bool INV>
-__device__ __forceinline__ void stage_any(double2 *sm, const StageDesc &sd, uint32_t logC, const double2 *wlo,
-                                          const double2 *whi)
+template <bool INV, int MODE = MODE_PLAIN>
+__device__ __forceinline__ double stage_any(double2 *sm, const StageDesc &sd, uint32_t logC, const double2 *wlo,
+                                            const double2 *whi, const StageCtx &x = StageCtx{})
 {
     switch (sd.R) {
-    case 2: stage_smem<2, INV>(sm, sd, logC, wlo, whi); break;
-    case 3: stage_smem<3, INV>(sm, sd, logC, wlo, whi); break;
-    case 4: stage_smem<4, INV>(sm, sd, logC, wlo, whi); break;
-    case 5: stage_smem<5, INV>(sm, sd, logC, wlo, whi); break;
-    case 7: stage_smem<7, INV>(sm, sd, logC, wlo, whi); break;
-    default: stage_smem<8, INV>(sm, sd, logC, wlo, whi); break;
+    case 2: return stage_smem<2, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    case 3: return stage_smem<3, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    case 4: return stage_smem<4, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    case 5: return stage_smem<5, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    case 7: return stage_smem<7, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    case 8: return stage_smem<8, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    default: return stage_smem<16, INV, MODE>(sm, sd, logC, wlo, whi, x);
     }
 }
 

@@ -437,6 +437,39 @@ pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32
     return PA_OK;
 }
 
+pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
+{
+    if (!info || n == 0 || m == 0) {
+        set_error("pa_plan: need info != NULL and n, m >= 1 (n = %llu, m = %llu)", (unsigned long long)n,
+                  (unsigned long long)m);
+        return PA_ERR_INVALID_ARG;
+    }
+    memset(info, 0, sizeof *info);
+    info->n = n;
+    info->m = m;
+    info->route = choose_route(n, m);
+    info->device = -1;
+    if (info->route == PA_ROUTE_BITPACKED) {
+        info->workspace_bytes = 4 * ((m + 31) / 32 + (n + 31) / 32 + 4);
+        info->kernels_per_hash = 1;
+        return PA_OK;
+    }
+    Geometry g;
+    char err[256];
+    pa_status st = ra_plan(n, m, &g, err, sizeof err);
+    if (st != PA_OK) {
+        set_error("%s", err);
+        return st;
+    }
+    info->transform_len = 2 * g.M;
+    info->n1 = g.N1;
+    info->n2 = g.N2;
+    info->cols_per_cta = g.C;
+    info->workspace_bytes = 32 * g.M;
+    info->kernels_per_hash = 3;
+    return PA_OK;
+}
+
 pa_status pa_get_info(pa_handle h, pa_info *info)
 {
     if (!h || !info) {

@@ -44,7 +44,23 @@
 namespace pa {
 namespace {
 
-constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic shared memory per CTA
+constexpr uint32_t kSmemLimit = 232448;
+#ifndef PA_TMAX
+#define PA_TMAX 512
+#endif
+#ifndef PA_MINB
+#define PA_MINB 1
+#endif
+#ifndef PA_MAXRADIX16
+#define PA_MAXRADIX16 1
+#endif  // 227 KB opt-in dynamic shared memory per CTA
+
+#ifdef PA_TIMING
+__device__ unsigned long long g_k2_clk[64][16];
+#define TSTAMP(i) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x < 64) g_k2_clk[blockIdx.x][i] = clock64(); } while (0)
+#else
+#define TSTAMP(i) do { } while (0)
+#endif
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
@@ -127,7 +143,7 @@ __global__ void k_tables(Geometry g, RouteTables T)
 
 // ------------------------------------------------------------------ K1
 // The real sequence = bits [off, off+nbits) of w, zero padded to N = 2M.
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, double2 *__restrict__ buf,
                Geometry g, RouteTables T, uint32_t *__restrict__ zero_out, uint64_t zero_words)
 {
@@ -147,12 +163,24 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     // per row b: C real-part bits (low half) and C imaginary-part bits (high half)
+    // rows past the data are zero (zero padding); gather 4 rows per thread at a
+    // time so the scattered L2 loads are in flight together
     const uint32_t cmask = (1u << C) - 1u;
-    for (uint32_t b = threadIdx.x; b < g.N2; b += blockDim.x) {
-        int64_t P = (int64_t)a0 + (int64_t)g.N1 * b + lo;
-        uint32_t re = bits32(w, P, lo, hi) & cmask;
-        uint32_t im = bits32(w, P + (int64_t)g.M, lo, hi) & cmask;
-        rowbits[b] = re | (im << 16);
+    const int64_t span = (int64_t)nbits;
+    for (uint32_t b0 = threadIdx.x; b0 < g.N2; b0 += 4 * blockDim.x) {
+        uint32_t re[4], im[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t b = b0 + k * blockDim.x;
+            const int64_t P = (int64_t)a0 + (int64_t)g.N1 * b;
+            re[k] = (b < g.N2 && P < span) ? bits32(w, P + lo, lo, hi) : 0u;
+            im[k] = (b < g.N2 && P + (int64_t)g.M < span) ? bits32(w, P + (int64_t)g.M + lo, lo, hi) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t b = b0 + k * blockDim.x;
+            if (b < g.N2) rowbits[b] = (re[k] & cmask) | ((im[k] & cmask) << 16);
+        }
     }
     __syncthreads();
     // z(b, c) = (x[a + N1 b] + i x[a + N1 b + M]) * theta_b
@@ -171,7 +199,9 @@ k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, dou
 }
 
 // ------------------------------------------------------------------ K2
-// Fused last DIF stage (Ls = 1, no twiddles) * spectrum * first DIT stage.
+// Fused last DIF stage (Ls = 1, no twiddles) * spectrum * first DIT stage.  The
+// spectrum row is stored [r][g] (element g*R + r at sp[r * nb + g]) so that the
+// lanes of a warp (consecutive g) read it coalesced.
 template <int R>
 __device__ __noinline__ void fused_mid(StageDesc sd, double2 *sm, const double2 *__restrict__ sp)
 {
@@ -179,7 +209,7 @@ __device__ __noinline__ void fused_mid(StageDesc sd, double2 *sm, const double2 
         const uint32_t base = gq * R;
         double2 s[R], v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) s[r] = __ldg(sp + base + r);
+        for (int r = 0; r < R; ++r) s[r] = __ldg(sp + r * sd.nb + gq);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = sm[pidx(base + r)];
         Dft<R, false>::run(v);
@@ -199,13 +229,14 @@ __device__ __forceinline__ void fused_mid_any(const StageDesc &sd, double2 *sm, 
     case 4: fused_mid<4>(sd, sm, sp); break;
     case 5: fused_mid<5>(sd, sm, sp); break;
     case 7: fused_mid<7>(sd, sm, sp); break;
-    default: fused_mid<8>(sd, sm, sp); break;
+    case 8: fused_mid<8>(sd, sm, sp); break;
+    default: fused_mid<16>(sd, sm, sp); break;
     }
 }
 
 // mode 0 (hash): in place, buf row -> tau -> DIF, * spec, DIT -> conj tau -> buf row.
 // mode 1 (create): buf row -> tau -> DIF -> * scale -> spec row.
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, RouteTables T, int mode,
         double scale)
 {
@@ -213,6 +244,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     const uint32_t N1 = g.N1;
     double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi, *rhi = rlo + 64;
     const uint32_t row = blockIdx.x;
+    TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *sp = spec + (uint64_t)row * N1;
     for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
@@ -220,28 +252,50 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     rho_tables(rlo, rhi, g.f1.nhi, g.M, __ldg(T.rev2 + row));
     cp_async_wait_all();
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
-    __syncthreads();
+    TSTAMP(1);
     const FftPlan &P = g.f1;
+    StageCtx rt;
+    rt.rlo = rlo;
+    rt.rhi = rhi;
+    rt.gout = rp;
+    if (P.S <= 1) {  // N1 <= 16: tau elementwise, then the single stage below runs plain
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
+        __syncthreads();
+    } else {
+        stage_any<false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
+        __syncthreads();
+    }
+    const int dif_from = P.S <= 1 ? 0 : 1;
     if (mode == 1) {
-        dif_stages(sm, P, 0, P.S, 0, wlo, whi);
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sp[e] = cscale(sm[pidx(e)], scale);
+        dif_stages(sm, P, dif_from, P.S, 0, wlo, whi);
+        // spectrum row in the [r][g] order fused_mid reads (R = last stage's radix)
+        const uint32_t R = P.S ? P.st[P.S - 1].R : 1, nbl = N1 / R;
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x)
+            sp[(e % R) * nbl + e / R] = cscale(sm[pidx(e)], scale);
         return;
     }
     if (P.S == 0) {
-        if (threadIdx.x == 0) sm[0] = cmul(sm[0], sp[0]);
-    } else {
-        dif_stages(sm, P, 0, P.S - 1, 0, wlo, whi);
-        fused_mid_any(P.st[P.S - 1], sm, sp);
-        __syncthreads();
-        dit_stages(sm, P, 0, P.S - 1, 0, wlo, whi);
+        if (threadIdx.x == 0) rp[0] = cmul(sm[0], sp[0]);
+        return;
     }
+    TSTAMP(2);
+    dif_stages(sm, P, dif_from, P.S - 1, 0, wlo, whi);
+    TSTAMP(3);
+    fused_mid_any(P.st[P.S - 1], sm, sp);
+    TSTAMP(4);
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) rp[e] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
+    if (P.S == 1) {
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) rp[e] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
+        return;
+    }
+    dit_stages(sm, P, 1, P.S - 1, 0, wlo, whi);
+    TSTAMP(5);
+    stage_any<true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+    TSTAMP(6);
 }
 
 // ------------------------------------------------------------------ K3
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
                uint32_t *__restrict__ out, unsigned long long *__restrict__ resid)
 {
@@ -256,14 +310,28 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     cp_async_wait_all();
     __syncthreads();
-    dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
-
-    // epilogue: element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
     const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;  // output window [t0, t1)
+    // only rows b holding some t in the window: u = a0 + c + N1 b (Re) or u + M (Im)
+    auto row_lo = [&](int64_t tmin) -> int64_t {  // first b with a0 + C - 1 + N1 b >= tmin
+        int64_t d = tmin - (int64_t)a0 - (int64_t)(C - 1);
+        return d <= 0 ? 0 : (d + g.N1 - 1) / g.N1;
+    };
+    auto row_hi = [&](int64_t tmax) -> int64_t {  // one past the last b with a0 + N1 b < tmax
+        int64_t d = tmax - (int64_t)a0;
+        return d <= 0 ? 0 : std::min<int64_t>((int64_t)g.N2, (d + g.N1 - 1) / g.N1);
+    };
+    const int64_t rb0 = row_lo(t0), rb1 = row_hi(t1);
+    const int64_t ib0 = row_lo(t0 - (int64_t)g.M), ib1 = row_hi(t1 - (int64_t)g.M);
+    const int64_t b_lo = std::min(rb1 > rb0 ? rb0 : (int64_t)g.N2, ib1 > ib0 ? ib0 : (int64_t)g.N2);
+    const int64_t b_hi = std::max(rb1 > rb0 ? rb1 : 0, ib1 > ib0 ? ib1 : 0);
+    dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    // epilogue: element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t runmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
     double rmax = 0.0;
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const uint32_t e_lo = b_hi > b_lo ? (uint32_t)(b_lo << logC) : 0;
+    const uint32_t e_hi = b_hi > b_lo ? (uint32_t)(b_hi << logC) : 0;
+    for (uint32_t e = e_lo + threadIdx.x; e < e_hi; e += blockDim.x) {
         const uint32_t b = e >> logC, c = e & (C - 1);
         const double2 wv = cmulc(sm[pidx(e)], twiddle(thlo, thhi, b));
         const int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
@@ -319,12 +387,22 @@ bool make_plan(uint32_t Lt, FftPlan *P)
     if (L != 1) return false;
     int R[kMaxStages], S = 0;
     auto push = [&](int r) { if (S < kMaxStages) R[S++] = r; };
-    while (e2 >= 3) { push(8); e2 -= 3; }
-    if (e2 == 2) push(4);
-    if (e2 == 1) push(2);
+    // odd radices first (large spans: lanes take consecutive j), then powers of two
+    // ascending so the small-span stages are radix 16 / 8 on the padded layout -- this
+    // order keeps every stage's quarter-warp accesses bank-conflict free for the
+    // plans the planner emits (modelled in DESIGN.md Sec. 5)
+    for (int i = 0; i < e7; ++i) push(7);
     for (int i = 0; i < e5; ++i) push(5);
     for (int i = 0; i < e3; ++i) push(3);
-    for (int i = 0; i < e7; ++i) push(7);
+    if (e2 % 4 == 1) push(2);
+    if (e2 % 4 == 2) push(4);
+    if (e2 % 4 == 3) push(8);
+    if (PA_MAXRADIX16) {
+        for (int i = 0; i < e2 / 4; ++i) push(16);
+    } else {
+        for (int i = 0; i < (e2 / 4) * 4 / 3; ++i) push(8);
+        for (int i = 0; i < ((e2 / 4) * 4) % 3; ++i) push(2);
+    }
     P->S = S;
     P->Lt = Lt;
     P->nhi = (Lt + 63) / 64;
@@ -369,33 +447,49 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
     const uint64_t L = n + m - 1;
     const uint64_t Mmin = (L + 1) / 2;
     static const std::vector<uint32_t> sm = smooth_numbers(32768);
-    const double dp_rate = 64.0 * 148 * 1.9e9;  // FP64 lane-ops per second
     double best = 1e300;
     bool found = false;
+    // Cost model (per hash), calibrated on B200 with tools/quick_time.py + PA_FORCE_PLAN:
+    //  - every FFT stage pass costs ~0.55 cycles per element per SM (shared-memory
+    //    round trip + FP64 butterfly; measured 0.5-0.6 across plans),
+    //  - HBM bytes at the column-group bandwidth of the access run (K1, K3) or 6.2 TB/s,
+    //  - with one CTA per SM memory and compute serialise, with two they overlap,
+    //  - a CTA needs >= ~1.6 us per stage pass whatever its size (latency floor).
+    const double sm_rate = 148.0 * 1.9e9;
     for (uint32_t N1 : sm) {
         if (smem_k2(N1, (N1 + 63) / 64) > kSmemLimit) break;
         uint64_t need = (Mmin + N1 - 1) / N1;
         if (need > 32768) continue;
         uint32_t N2 = *std::lower_bound(sm.begin(), sm.end(), (uint32_t)need);
+        FftPlan p1, p2;
+        if (!make_plan(N1, &p1) || !make_plan(N2, &p2)) continue;
         for (uint32_t C = 16; C >= 1; C >>= 1) {
             if (N1 % C) continue;
             uint32_t s13 = smem_k13(N2, C, (N2 + 63) / 64);
             if (s13 > kSmemLimit) continue;
-            double M = (double)N1 * N2;
-            // memory time per kernel (bytes / bandwidth) and FP64 time
-            double log1 = log2((double)N1), log2v = log2((double)N2);
-            double m1 = 16 * M / colgroup_bw(C), m2 = 48 * M / 6.2e12, m3 = m1;
-            double d1 = M * (4.7 * log2v + 12) / dp_rate, d2 = M * (9.4 * log1 + 8) / dp_rate, d3 = d1;
-            bool two13 = 2 * s13 <= kSmemLimit, two2 = 2 * smem_k2(N1, (N1 + 63) / 64) <= kSmemLimit;
-            double t1 = two13 ? std::max(m1, d1) : m1 + d1;
-            double t2 = two2 ? std::max(m2, d2) : m2 + d2;
-            double t3 = two13 ? std::max(m3, d3) : m3 + d3;
-            // small problems: parallelism (CTAs) and launch latency dominate
-            double ctas13 = (double)(N1 / C), ctas2 = N2;
-            double par = 0;
-            if (ctas13 < 2 * 148) par += 3e-6 * (1.0 - ctas13 / (2 * 148));
-            if (ctas2 < 2 * 148) par += 3e-6 * (1.0 - ctas2 / (2 * 148));
-            double cost = t1 + t2 + t3 + par;
+            const double M = (double)N1 * N2;
+            // per-pass cost by radix (odd radices do more FP64 work per point)
+            auto pc = [](const FftPlan &P) {
+                double s = 0;
+                for (int i = 0; i < P.S; ++i) {
+                    const uint32_t R = P.st[i].R;
+                    s += R == 7 ? 0.8 : R == 5 ? 0.65 : R == 3 ? 0.5 : R == 16 ? 0.55 : 0.45;
+                }
+                return s;
+            };
+            const double pass13 = p2.S + 0.5, pass2 = 2.0 * p1.S - 1 + 0.5;
+            const double c1 = M * (pc(p2) + 0.3) / sm_rate, c2 = M * (2 * pc(p1) + 0.3) / sm_rate;
+            const double m1 = 16 * M / colgroup_bw(C), m2 = 48 * M / 6.2e12;
+            const uint32_t occ13 = std::min<uint32_t>(4, kSmemLimit / s13);
+            const uint32_t occ2 = std::min<uint32_t>(4, kSmemLimit / smem_k2(N1, (N1 + 63) / 64));
+            auto ktime = [&](double comp, double mem, uint32_t occ, double ctas, double passes) {
+                double thr = occ >= 2 ? std::max(comp, mem) + 0.3 * std::min(comp, mem) : comp + mem;
+                double waves = std::ceil(ctas / (148.0 * occ));
+                return std::max(thr, waves * passes * 1.6e-6) + 2e-6;
+            };
+            double cost = 2 * ktime(c1, m1, occ13, (double)(N1 / C), pass13) +
+                          ktime(c2, m2, occ2, (double)N2, pass2 + 1.0);
+            cost *= 1.0 + (C == 1 ? 0.2 : 0.0);  // 16-byte runs: uncoalesced epilogue/atomics
             if (cost < best) {
                 best = cost;
                 found = true;
@@ -437,8 +531,8 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
     g->smem1 = smem_k13(g->N2, g->C, g->f2.nhi);
     g->smem2 = smem_k2(g->N1, g->f1.nhi);
     // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
-    g->t1 = 2 * g->smem1 <= kSmemLimit ? 256 : 512;
-    g->t2 = 2 * g->smem2 <= kSmemLimit ? 256 : 512;
+    g->t1 = 2 * g->smem1 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
+    g->t2 = 2 * g->smem2 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
     return PA_OK;
 }
 
@@ -517,6 +611,13 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
     if (e != cudaSuccess) return cuda_fail(e, "route (a) hash launches");
     return PA_OK;
 }
+
+#ifdef PA_TIMING
+extern "C" int pa_debug_k2_clocks(unsigned long long *out)
+{
+    return (int)cudaMemcpyFromSymbol(out, g_k2_clk, sizeof(g_k2_clk));
+}
+#endif
 
 void ra_destroy(pa_ctx *h)
 {

@@ -87,3 +87,34 @@ def test_bad_options_rejected():
     with pytest.raises(pa.PaError) as e:
         pa.pa_create_ex(10, 5, 0, o, 0)
     assert e.value.status == pa.PA_ERR_INVALID_ARG
+
+
+def test_planner_host_only():
+    """pa_plan: route choice and transform length N >= n+m-1 (reading R4), even, smooth
+    factors, without any device work."""
+    import paper_1805_02372_b200 as pa
+    import pa_synth as syn
+    for name, cfg in syn.CONFIGS.items():
+        n, m = cfg["n"], cfg["m"]
+        p = pa.pa_plan(n, m)
+        if p["route"] == pa.PA_ROUTE_BITPACKED:
+            assert n * m <= 2 ** 26
+            continue
+        N = p["transform_len"]
+        assert N >= n + m - 1 and N % 2 == 0, name
+        assert p["n1"] * p["n2"] * 2 == N
+        assert N <= 1.06 * (n + m - 1) + 64, (name, N / (n + m - 1))
+        for f in (p["n1"], p["n2"]):
+            for q in (2, 3, 5, 7):
+                while f % q == 0:
+                    f //= q
+            assert f == 1
+        assert p["n1"] % p["cols_per_cta"] == 0
+    for n, m in ((1, 1), (2, 1), (65537, 3), (10 ** 9, 10 ** 6)):
+        try:
+            p = pa.pa_plan(n, m)
+        except pa.PaError as e:
+            assert e.status == pa.PA_ERR_UNSUPPORTED
+            continue
+        if p["route"] == pa.PA_ROUTE_TRANSFORM:
+            assert p["transform_len"] >= n + m - 1

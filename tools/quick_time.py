@@ -51,10 +51,18 @@ def main(names, iters=20):
             e1.record()
             torch.cuda.synchronize()
             b2b = e0.elapsed_time(e1) / iters
+            pa.pa_profile_enable(h.handle, True)
+            pa.pa_profile_read(h.handle)
+            for _ in range(iters):
+                flush.zero_()
+                h.hash(key, out)
+            kt = pa.pa_profile_read(h.handle)
+            pa.pa_profile_enable(h.handle, False)
+            kts = " ".join(f"{k}={v[1] / v[0] * 1e3:.1f}us" for k, v in kt.items())
             med = float(np.median(ts))
             print(f"{name} n={n} m={m} route={h.route} info={h.info} create={tc*1e3:.1f}ms "
                   f"cold median={med*1e3:.1f}us ({n/med/1e6:.1f} Gbit/s) b2b={b2b*1e3:.1f}us "
-                  f"({n/b2b/1e6:.1f} Gbit/s) resid={h.residual():.2e}", flush=True)
+                  f"({n/b2b/1e6:.1f} Gbit/s) resid={h.residual():.2e} | {kts}", flush=True)
             h.close()
 
 
