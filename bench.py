@@ -143,7 +143,8 @@ def alg_bytes(kernel, info):
     """Algorithmic HBM bytes of one launch: M complex doubles = 16 M bytes."""
     M = info["n1"] * info["n2"]
     n, m = info["n"], info["m"]
-    return {"k1_fwd_columns": 16 * M + n / 8.0,            # key bits in, work array out
+    return {"k0_bits_transpose": n / 8.0 + M / 4.0,          # key bits in, 2M bits of streams out
+            "k1_fwd_columns": M / 4.0 + 16 * M,             # bit streams in, work array out
             "k2_rows": 48 * M,                              # row in, spectrum in, row out
             "k3_inv_columns": 16 * M + m / 8.0}.get(kernel)  # work array in, output bits out
 

@@ -465,8 +465,8 @@ pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
     info->n1 = g.N1;
     info->n2 = g.N2;
     info->cols_per_cta = g.C;
-    info->workspace_bytes = 32 * g.M;
-    info->kernels_per_hash = 3;
+    info->workspace_bytes = 32 * g.M + (uint64_t)(g.N1 / g.C) * g.kbw * 4;
+    info->kernels_per_hash = 4;
     return PA_OK;
 }
 

@@ -21,6 +21,7 @@ struct Geometry {
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)
     uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)
     uint32_t smem1, smem2;  // dynamic shared bytes: K1/K3, K2
+    uint32_t kbw;           // K0 bit-stream words per column group
 };
 
 struct RouteTables {
@@ -37,6 +38,7 @@ struct RouteA {
     double2 *tables = nullptr; // backing store of T's double2 tables
     RouteTables T{};
     unsigned long long *resid = nullptr; // max |v - rint v| (as double bits)
+    uint32_t *kb = nullptr;    // K0 output: per-column-group bit streams of the input
 };
 
 // ---------------------------------------------------------------- route (b)
@@ -53,7 +55,7 @@ struct Profiler {
     bool on = false;
     static constexpr int kKernels = 8;
     const char *names[kKernels] = {"k1_fwd_columns", "k2_rows", "k3_inv_columns",
-                                   "k_toeplitz_bitpacked", "", "", "", ""};
+                                   "k_toeplitz_bitpacked", "k0_bits_transpose", "", "", ""};
     struct Pending { int k; cudaEvent_t e0, e1; };
     Pending *pend = nullptr;
     int npend = 0, cap = 0;

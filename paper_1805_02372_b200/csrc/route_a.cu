@@ -56,10 +56,12 @@ constexpr uint32_t kSmemLimit = 232448;
 #endif  // 227 KB opt-in dynamic shared memory per CTA
 
 #ifdef PA_TIMING
-__device__ unsigned long long g_k2_clk[64][16];
-#define TSTAMP(i) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x < 64) g_k2_clk[blockIdx.x][i] = clock64(); } while (0)
+__device__ unsigned long long g_k2_clk[3][64][16];
+#define TSTAMPK(k, i) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x < 64) g_k2_clk[k][blockIdx.x][i] = clock64(); } while (0)
+#define TSTAMP(i) TSTAMPK(1, i)
 #else
 #define TSTAMP(i) do { } while (0)
+#define TSTAMPK(k, i) do { } while (0)
 #endif
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
@@ -141,61 +143,110 @@ __global__ void k_tables(Geometry g, RouteTables T)
     }
 }
 
+// ------------------------------------------------------------------ K0
+// Bit transpose of the zero-padded input into one bit stream per K1 column
+// group: group g (columns [gC, gC+C)) holds, for each row b < N2, the 2C bits
+// x[N1 b + gC + c] (c < C) then x[M + N1 b + gC + c] -- entry b of the stream,
+// EPW = 32 / 2C entries per uint32 word, g.kbw words per group.  A CTA transposes
+// a tile of 64 rows x 1024 columns through shared memory, so both the key reads
+// (128-byte row segments) and the stream writes are coalesced; K1 then loads its
+// group's bits with a few contiguous words instead of N2 scattered gathers.
+constexpr uint32_t kK0Rows = 64, kK0Cols = 1024;  // largest tile (shared arrays sized for it)
+
+// tile rows x cols: 64 x 1024 for large transforms, 16 x 256 for small ones (more CTAs)
+__host__ __device__ inline uint32_t k0_rows(const Geometry &g) { return g.N2 >= 2048 ? 64 : 16; }
+__host__ __device__ inline uint32_t k0_cols(const Geometry &g) { return g.N1 >= 8192 ? 1024 : 256; }
+
+__global__ void __launch_bounds__(256)
+k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, uint32_t *__restrict__ kb,
+                  Geometry g)
+{
+    __shared__ uint32_t tre[kK0Rows][kK0Cols / 32 + 1], tim[kK0Rows][kK0Cols / 32 + 1];
+    const uint32_t C = g.C, twoC = 2 * C, epw = 32 / twoC;
+    const uint32_t RB = k0_rows(g), CB = k0_cols(g), CW = CB / 32;
+    const uint32_t c0 = blockIdx.x * CB, b0 = blockIdx.y * RB;
+    const int64_t lo = (int64_t)off, hi = (int64_t)(off + nbits);
+    for (uint32_t i = threadIdx.x; i < RB * CW; i += blockDim.x) {
+        const uint32_t r = i / CW, k = i % CW;
+        const uint32_t b = b0 + r, col = c0 + 32 * k;
+        uint32_t re = 0, im = 0;
+        if (b < g.N2 && col < g.N1) {
+            const int64_t P = (int64_t)g.N1 * b + col;
+            re = bits32(w, P + lo, lo, hi);
+            im = bits32(w, P + (int64_t)g.M + lo, lo, hi);
+            const uint32_t valid = g.N1 - col;  // columns past N1 belong to the next row
+            if (valid < 32) {
+                re &= (1u << valid) - 1u;
+                im &= (1u << valid) - 1u;
+            }
+        }
+        tre[r][k] = re;
+        tim[r][k] = im;
+    }
+    __syncthreads();
+    const uint32_t groups = CB / C;                 // groups in this column tile
+    const uint32_t wpg = RB / epw;                  // stream words per group in this row tile
+    const uint32_t cmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
+    for (uint32_t i = threadIdx.x; i < groups * wpg; i += blockDim.x) {
+        const uint32_t gl = i / wpg, k = i % wpg;
+        const uint32_t gg = c0 / C + gl;
+        const uint32_t wb = b0 / epw + k;           // word index in the group's stream
+        if (gg >= g.N1 / C || wb * epw >= g.N2) continue;
+        const uint32_t cb = gl * C;                 // bit column within the tile
+        uint32_t word = 0;
+        for (uint32_t e = 0; e < epw; ++e) {
+            const uint32_t r = k * epw + e;
+            const uint32_t re = (tre[r][cb >> 5] >> (cb & 31)) & cmask;
+            const uint32_t im = (tim[r][cb >> 5] >> (cb & 31)) & cmask;
+            word |= (re | (im << C)) << (e * twoC);
+        }
+        kb[(uint64_t)gg * g.kbw + wb] = word;
+    }
+}
+
 // ------------------------------------------------------------------ K1
-// The real sequence = bits [off, off+nbits) of w, zero padded to N = 2M.
+// Column DIF of C adjacent columns; input = this group's bit stream from K0.
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
-k1_fwd_columns(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, double2 *__restrict__ buf,
-               Geometry g, RouteTables T, uint32_t *__restrict__ zero_out, uint64_t zero_words)
+k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
+               uint32_t *__restrict__ zero_out, uint64_t zero_words)
 {
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
     uint32_t *rowbits = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
     const uint32_t a0 = blockIdx.x * C;
-    const int64_t lo = (int64_t)off, hi = (int64_t)(off + nbits);
     const uint32_t tot = g.N2 << logC;
-
+    TSTAMPK(0, 0);
     if (zero_out) {  // K3 ORs this hash's output bits in
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
              i += (uint64_t)gridDim.x * blockDim.x)
             zero_out[i] = 0u;
     }
+    const uint32_t *src = kb + (uint64_t)blockIdx.x * g.kbw;
+    for (uint32_t i = threadIdx.x; i < g.kbw; i += blockDim.x) rowbits[i] = __ldg(src + i);
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
-    // per row b: C real-part bits (low half) and C imaginary-part bits (high half)
-    // rows past the data are zero (zero padding); gather 4 rows per thread at a
-    // time so the scattered L2 loads are in flight together
-    const uint32_t cmask = (1u << C) - 1u;
-    const int64_t span = (int64_t)nbits;
-    for (uint32_t b0 = threadIdx.x; b0 < g.N2; b0 += 4 * blockDim.x) {
-        uint32_t re[4], im[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t b = b0 + k * blockDim.x;
-            const int64_t P = (int64_t)a0 + (int64_t)g.N1 * b;
-            re[k] = (b < g.N2 && P < span) ? bits32(w, P + lo, lo, hi) : 0u;
-            im[k] = (b < g.N2 && P + (int64_t)g.M < span) ? bits32(w, P + (int64_t)g.M + lo, lo, hi) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t b = b0 + k * blockDim.x;
-            if (b < g.N2) rowbits[b] = (re[k] & cmask) | ((im[k] & cmask) << 16);
-        }
-    }
+    TSTAMPK(0, 1);
     __syncthreads();
-    // z(b, c) = (x[a + N1 b] + i x[a + N1 b + M]) * theta_b
+    TSTAMPK(0, 2);
+    // z(b, c) = (x[a + N1 b] + i x[a + N1 b + M]) * theta_b; entry b of the stream holds
+    // the C real-part bits then the C imaginary-part bits of row b
+    const uint32_t twoC = 2 * C, epw = 32 / twoC;
     for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        uint32_t b = e >> logC, c = e & (C - 1);
-        uint32_t rb = rowbits[b];
-        double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (16 + c)) & 1u);
-        double2 th = twiddle(thlo, thhi, b);
+        const uint32_t b = e >> logC, c = e & (C - 1);
+        const uint32_t rb = rowbits[b / epw] >> ((b % epw) * twoC);
+        const double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (C + c)) & 1u);
+        const double2 th = twiddle(thlo, thhi, b);
         sm[pidx(e)] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
     }
     __syncthreads();
+    TSTAMPK(0, 3);
     dif_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    TSTAMPK(0, 4);
     // row p of the work array = DIF output position p (k_b = rev2[p])
     for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
         buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
+    TSTAMPK(0, 5);
 }
 
 // ------------------------------------------------------------------ K2
@@ -304,6 +355,7 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
+    TSTAMPK(2, 0);
     for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
         cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
@@ -324,7 +376,9 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     const int64_t ib0 = row_lo(t0 - (int64_t)g.M), ib1 = row_hi(t1 - (int64_t)g.M);
     const int64_t b_lo = std::min(rb1 > rb0 ? rb0 : (int64_t)g.N2, ib1 > ib0 ? ib0 : (int64_t)g.N2);
     const int64_t b_hi = std::max(rb1 > rb0 ? rb1 : 0, ib1 > ib0 ? ib1 : 0);
+    TSTAMPK(2, 1);
     dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    TSTAMPK(2, 2);
     // epilogue: element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t runmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
@@ -359,6 +413,7 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
             }
         }
     }
+    TSTAMPK(2, 3);
 #pragma unroll
     for (int d = 16; d; d >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, d));
     if (lane == 0 && rmax > 0.0) atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
@@ -436,9 +491,14 @@ double colgroup_bw(uint32_t C)
 
 }  // namespace
 
+static uint32_t kb_words(uint32_t N2, uint32_t C)  // K0 stream words per group (16-byte multiple)
+{
+    const uint32_t epw = 16 / C;
+    return ((N2 + epw - 1) / epw + 3) / 4 * 4;
+}
 static uint32_t smem_k13(uint32_t N2, uint32_t C, uint32_t nhi2)
 {
-    return tile_bytes((uint64_t)N2 * C) + 2 * (64 + nhi2) * 16 + ((N2 * 4 + 15) / 16) * 16;
+    return tile_bytes((uint64_t)N2 * C) + 2 * (64 + nhi2) * 16 + kb_words(N2, C) * 4;
 }
 static uint32_t smem_k2(uint32_t N1, uint32_t nhi1) { return tile_bytes(N1) + 2 * (64 + nhi1) * 16; }
 
@@ -460,7 +520,11 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
         if (smem_k2(N1, (N1 + 63) / 64) > kSmemLimit) break;
         uint64_t need = (Mmin + N1 - 1) / N1;
         if (need > 32768) continue;
-        uint32_t N2 = *std::lower_bound(sm.begin(), sm.end(), (uint32_t)need);
+        // every smooth N2 within +12% of the minimum: a longer but radix-16-friendly
+        // length often needs fewer passes than the tightest fit
+        auto it0 = std::lower_bound(sm.begin(), sm.end(), (uint32_t)need);
+        for (auto it = it0; it != sm.end() && *it <= need * 1.12 + 16; ++it) {
+        const uint32_t N2 = *it;
         FftPlan p1, p2;
         if (!make_plan(N1, &p1) || !make_plan(N2, &p2)) continue;
         for (uint32_t C = 16; C >= 1; C >>= 1) {
@@ -499,6 +563,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
                 g->C = C;
             }
         }
+        }
     }
     // developer override for plan experiments: PA_FORCE_PLAN="N1,N2,C"
     if (const char *fp = getenv("PA_FORCE_PLAN")) {
@@ -529,6 +594,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
     g->tile1 = tile_bytes((uint64_t)g->N2 * g->C) / 16;
     g->tile2 = tile_bytes(g->N1) / 16;
     g->smem1 = smem_k13(g->N2, g->C, g->f2.nhi);
+    g->kbw = kb_words(g->N2, g->C);
     g->smem2 = smem_k2(g->N1, g->f1.nhi);
     // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
     g->t1 = 2 * g->smem1 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
@@ -566,6 +632,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     if ((st = alloc((void **)&a.tables, ntab * sizeof(double2), h, "tables"))) return st;
     if ((st = alloc((void **)&T.rev2, g.N2 * sizeof(uint32_t), h, "rev2"))) return st;
     if ((st = alloc((void **)&a.resid, sizeof(unsigned long long), h, "resid"))) return st;
+    if ((st = alloc((void **)&a.kb, (size_t)(g.N1 / g.C) * g.kbw * 4, h, "kb"))) return st;
     double2 *p = a.tables;
     T.W1lo = p; p += 64;
     T.W1hi = p; p += g.f1.nhi;
@@ -587,10 +654,12 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
     k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
     // seed spectrum: K1 + forward half of K2, scaled by 1/M
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(seed, h->off, h->L, a.buf, g, T, nullptr, 0);
+    const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
+    k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g);
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, T, nullptr, 0);
     k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, T, 1, 1.0 / (double)g.M);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) create launches");
-    h->kernels_per_hash = 3;
+    h->kernels_per_hash = 4;
     return PA_OK;
 }
 
@@ -598,8 +667,12 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
 {
     RouteA &a = h->a;
     const Geometry &g = a.g;
+    const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
+    prof_begin(h, 4, s);
+    k0_bits_transpose<<<g0, 256, 0, s>>>(key, 0, h->n, a.kb, g);
+    prof_end(h, s);
     prof_begin(h, 0, s);
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(key, 0, h->n, a.buf, g, a.T, out, zero_words);
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, out, zero_words);
     prof_end(h, s);
     prof_begin(h, 1, s);
     k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 0, 1.0);
@@ -622,7 +695,7 @@ extern "C" int pa_debug_k2_clocks(unsigned long long *out)
 void ra_destroy(pa_ctx *h)
 {
     RouteA &a = h->a;
-    void *ptrs[] = {a.buf, a.spec, a.tables, a.T.rev2, a.resid};
+    void *ptrs[] = {a.buf, a.spec, a.tables, a.T.rev2, a.resid, a.kb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     a = RouteA{};
