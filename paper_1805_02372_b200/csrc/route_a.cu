@@ -59,10 +59,35 @@ constexpr uint32_t kSmemLimit = 232448;
 __device__ unsigned long long g_k2_clk[3][64][16];
 #define TSTAMPK(k, i) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x < 64) g_k2_clk[k][blockIdx.x][i] = clock64(); } while (0)
 #define TSTAMP(i) TSTAMPK(1, i)
+__device__ unsigned long long g_trace[4][8192][3];  // per kernel (K0..K3), per CTA: smid, start, end ns
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid()
+{
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
+}
+#define TRACE_BEGIN(k) unsigned long long _t0 = gtimer()
+#define TRACE_END(k) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 8192) { \
+    unsigned _b = blockIdx.x + gridDim.x * blockIdx.y; g_trace[k][_b][0] = smid(); g_trace[k][_b][1] = _t0; \
+    g_trace[k][_b][2] = gtimer(); } } while (0)
 #else
 #define TSTAMP(i) do { } while (0)
 #define TSTAMPK(k, i) do { } while (0)
+#define TRACE_BEGIN(k) do { } while (0)
+#define TRACE_END(k) do { } while (0)
 #endif
+
+// Programmatic dependent launch: the prologue (tables, per-row constants) of a
+// kernel overlaps the tail of the previous one; grid_dep_wait() blocks until the
+// previous grid has completed and its memory is visible.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
@@ -161,6 +186,7 @@ __global__ void __launch_bounds__(256)
 k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, uint32_t *__restrict__ kb,
                   Geometry g)
 {
+    TRACE_BEGIN(0);
     __shared__ uint32_t tre[kK0Rows][kK0Cols / 32 + 1], tim[kK0Rows][kK0Cols / 32 + 1];
     const uint32_t C = g.C, twoC = 2 * C, epw = 32 / twoC;
     const uint32_t RB = k0_rows(g), CB = k0_cols(g), CW = CB / 32;
@@ -202,6 +228,7 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
         }
         kb[(uint64_t)gg * g.kbw + wb] = word;
     }
+    TRACE_END(0);
 }
 
 // ------------------------------------------------------------------ K1
@@ -216,7 +243,11 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     uint32_t *rowbits = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
+    TRACE_BEGIN(1);
     TSTAMPK(0, 0);
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    grid_dep_wait();  // K0's bit streams
     if (zero_out) {  // K3 ORs this hash's output bits in
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
              i += (uint64_t)gridDim.x * blockDim.x)
@@ -224,8 +255,6 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     }
     const uint32_t *src = kb + (uint64_t)blockIdx.x * g.kbw;
     for (uint32_t i = threadIdx.x; i < g.kbw; i += blockDim.x) rowbits[i] = __ldg(src + i);
-    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
-    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     TSTAMPK(0, 1);
     __syncthreads();
     TSTAMPK(0, 2);
@@ -242,11 +271,13 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     __syncthreads();
     TSTAMPK(0, 3);
     dif_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    grid_dep_launch();  // K2 may start its prologue
     TSTAMPK(0, 4);
     // row p of the work array = DIF output position p (k_b = rev2[p])
     for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
         buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
     TSTAMPK(0, 5);
+    TRACE_END(1);
 }
 
 // ------------------------------------------------------------------ K2
@@ -295,12 +326,14 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     const uint32_t N1 = g.N1;
     double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi, *rhi = rlo + 64;
     const uint32_t row = blockIdx.x;
+    TRACE_BEGIN(2);
     TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *sp = spec + (uint64_t)row * N1;
-    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
     load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi);
     rho_tables(rlo, rhi, g.f1.nhi, g.M, __ldg(T.rev2 + row));
+    grid_dep_wait();  // K1's work array
+    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
     cp_async_wait_all();
     __syncthreads();
     TSTAMP(1);
@@ -340,9 +373,11 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
         return;
     }
     dit_stages(sm, P, 1, P.S - 1, 0, wlo, whi);
+    grid_dep_launch();  // K3 may start its prologue
     TSTAMP(5);
     stage_any<true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
     TSTAMP(6);
+    TRACE_END(2);
 }
 
 // ------------------------------------------------------------------ K3
@@ -355,11 +390,13 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
+    TRACE_BEGIN(3);
     TSTAMPK(2, 0);
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-        cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    grid_dep_wait();  // K2's rows
+    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
+        cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
     cp_async_wait_all();
     __syncthreads();
     const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;  // output window [t0, t1)
@@ -417,6 +454,7 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
 #pragma unroll
     for (int d = 16; d; d >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, d));
     if (lane == 0 && rmax > 0.0) atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
+    TRACE_END(3);
 }
 
 // ------------------------------------------------------------------ host plan
@@ -477,18 +515,6 @@ bool make_plan(uint32_t Lt, FftPlan *P)
 
 uint32_t tile_bytes(uint64_t elems) { return (uint32_t)((elems + (elems >> 4) + 1) * 16); }
 
-// Measured on B200 (tools/microbench.cu): column-group copy bandwidth by run length.
-double colgroup_bw(uint32_t C)
-{
-    switch (C) {
-    case 1: return 2.3e12;
-    case 2: return 4.2e12;
-    case 4: return 4.7e12;
-    case 8: return 5.6e12;
-    default: return 5.5e12;
-    }
-}
-
 }  // namespace
 
 static uint32_t kb_words(uint32_t N2, uint32_t C)  // K0 stream words per group (16-byte multiple)
@@ -531,29 +557,19 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
             if (N1 % C) continue;
             uint32_t s13 = smem_k13(N2, C, (N2 + 63) / 64);
             if (s13 > kSmemLimit) continue;
+            // measured: every FFT stage pass (and the load / store / twiddle passes around
+            // them) costs ~0.62 cycles per element per SM, largely independent of the radix
             const double M = (double)N1 * N2;
-            // per-pass cost by radix (odd radices do more FP64 work per point)
-            auto pc = [](const FftPlan &P) {
-                double s = 0;
-                for (int i = 0; i < P.S; ++i) {
-                    const uint32_t R = P.st[i].R;
-                    s += R == 7 ? 0.8 : R == 5 ? 0.65 : R == 3 ? 0.5 : R == 16 ? 0.55 : 0.45;
-                }
-                return s;
-            };
-            const double pass13 = p2.S + 0.5, pass2 = 2.0 * p1.S - 1 + 0.5;
-            const double c1 = M * (pc(p2) + 0.3) / sm_rate, c2 = M * (2 * pc(p1) + 0.3) / sm_rate;
-            const double m1 = 16 * M / colgroup_bw(C), m2 = 48 * M / 6.2e12;
-            const uint32_t occ13 = std::min<uint32_t>(4, kSmemLimit / s13);
-            const uint32_t occ2 = std::min<uint32_t>(4, kSmemLimit / smem_k2(N1, (N1 + 63) / 64));
-            auto ktime = [&](double comp, double mem, uint32_t occ, double ctas, double passes) {
-                double thr = occ >= 2 ? std::max(comp, mem) + 0.3 * std::min(comp, mem) : comp + mem;
+            const double pass13 = p2.S + 2.0, pass2 = 2.0 * p1.S + 1.0;
+            const double cfac = C == 1 ? 1.5 : C == 2 ? 1.0 : 0.95;  // short HBM runs (K1/K3)
+            const uint32_t occ13 = std::min<uint32_t>(2, kSmemLimit / s13);
+            const uint32_t occ2 = std::min<uint32_t>(2, kSmemLimit / smem_k2(N1, (N1 + 63) / 64));
+            auto ktime = [&](double passes, double fac, uint32_t occ, double ctas) {
+                double thr = M * passes * 0.62 * fac / sm_rate;
                 double waves = std::ceil(ctas / (148.0 * occ));
-                return std::max(thr, waves * passes * 1.6e-6) + 2e-6;
+                return std::max(thr, waves * passes * 1.3e-6) + 2e-6;
             };
-            double cost = 2 * ktime(c1, m1, occ13, (double)(N1 / C), pass13) +
-                          ktime(c2, m2, occ2, (double)N2, pass2 + 1.0);
-            cost *= 1.0 + (C == 1 ? 0.2 : 0.0);  // 16-byte runs: uncoalesced epilogue/atomics
+            double cost = 2 * ktime(pass13, cfac, occ13, (double)(N1 / C)) + ktime(pass2, 1.0, occ2, (double)N2);
             if (cost < best) {
                 best = cost;
                 found = true;
@@ -599,6 +615,8 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
     // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
     g->t1 = 2 * g->smem1 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
     g->t2 = 2 * g->smem2 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
+    if (const char *e = getenv("PA_FORCE_T1")) g->t1 = (uint32_t)atoi(e);  // developer overrides
+    if (const char *e = getenv("PA_FORCE_T2")) g->t2 = (uint32_t)atoi(e);
     return PA_OK;
 }
 
@@ -663,6 +681,23 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     return PA_OK;
 }
 
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words, cudaStream_t s)
 {
     RouteA &a = h->a;
@@ -672,13 +707,13 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
     k0_bits_transpose<<<g0, 256, 0, s>>>(key, 0, h->n, a.kb, g);
     prof_end(h, s);
     prof_begin(h, 0, s);
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, out, zero_words);
+    launch_pdl(k1_fwd_columns, g.N1 / g.C, g.t1, g.smem1, s, a.kb, a.buf, g, a.T, out, zero_words);
     prof_end(h, s);
     prof_begin(h, 1, s);
-    k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 0, 1.0);
+    launch_pdl(k2_rows, g.N2, g.t2, g.smem2, s, a.buf, a.spec, g, a.T, 0, 1.0);
     prof_end(h, s);
     prof_begin(h, 2, s);
-    k3_inv_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.buf, g, a.T, h->n, h->m, out, a.resid);
+    launch_pdl(k3_inv_columns, g.N1 / g.C, g.t1, g.smem1, s, a.buf, g, a.T, h->n, h->m, out, a.resid);
     prof_end(h, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (a) hash launches");
@@ -689,6 +724,10 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
 extern "C" int pa_debug_k2_clocks(unsigned long long *out)
 {
     return (int)cudaMemcpyFromSymbol(out, g_k2_clk, sizeof(g_k2_clk));
+}
+extern "C" int pa_debug_trace(unsigned long long *out)
+{
+    return (int)cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
 }
 #endif
 
