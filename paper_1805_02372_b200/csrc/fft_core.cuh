@@ -207,21 +207,40 @@ __device__ __forceinline__ double2 twiddle(const double2 *lo, const double2 *hi,
     return cmul(hi[e >> 6], lo[e & 63]);
 }
 
+// v[k] *= w1^k (or conj) for k = 1..R-1.  Powers 2..4 from w1, then a running
+// B = w1^{4a} and w1^{4a+b} = B * w1^b: the same multiply count as a running
+// product, at most ~5 complex multiplies deep (latency, and the DESIGN.md error
+// bound), and only six complex temporaries live (registers).
+template <int R, bool INV>
+__device__ __forceinline__ void apply_twiddles(double2 *v, double2 w1)
+{
+    double2 p[4];
+    p[1] = w1;
+    if (R > 2) p[2] = cmul(w1, w1);
+    if (R > 3) p[3] = cmul(p[2], w1);
+#pragma unroll
+    for (int b = 1; b < 4 && b < R; ++b) v[b] = INV ? cmulc(v[b], p[b]) : cmul(v[b], p[b]);
+    if (R > 4) {
+        const double2 w4 = cmul(p[2], p[2]);
+        double2 B = w4;
+#pragma unroll
+        for (int a = 1; 4 * a < R; ++a) {
+            if (a > 1) B = cmul(B, w4);
+#pragma unroll
+            for (int b = 0; b < 4 && 4 * a + b < R; ++b) {
+                const double2 w = b ? cmul(B, p[b]) : B;
+                v[4 * a + b] = INV ? cmulc(v[4 * a + b], w) : cmul(v[4 * a + b], w);
+            }
+        }
+    }
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void butterfly(double2 *v, uint32_t j, const StageDesc &sd, const double2 *wlo,
                                           const double2 *whi)
 {
     if (!INV) Dft<R, false>::run(v);
-    if (j) {
-        // w_k = w1^k by a running product (k - 1 <= 15 roundings deep: DESIGN.md Sec. 5)
-        const double2 w1 = twiddle(wlo, whi, j * sd.G);
-        double2 w = w1;
-#pragma unroll
-        for (int k = 1; k < R; ++k) {
-            v[k] = INV ? cmulc(v[k], w) : cmul(v[k], w);
-            if (k + 1 < R) w = cmul(w, w1);
-        }
-    }
+    if (j) apply_twiddles<R, INV>(v, twiddle(wlo, whi, j * sd.G));
     if (INV) Dft<R, true>::run(v);
 }
 

@@ -188,6 +188,7 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
 {
     TRACE_BEGIN(0);
     __shared__ uint32_t tre[kK0Rows][kK0Cols / 32 + 1], tim[kK0Rows][kK0Cols / 32 + 1];
+    grid_dep_launch();  // K1 may start its prologue (K0 is a single short wave)
     const uint32_t C = g.C, twoC = 2 * C, epw = 32 / twoC;
     const uint32_t RB = k0_rows(g), CB = k0_cols(g), CW = CB / 32;
     const uint32_t c0 = blockIdx.x * CB, b0 = blockIdx.y * RB;
