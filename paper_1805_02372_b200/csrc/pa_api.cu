@@ -325,6 +325,17 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
     pa_status st;
     if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
+    if (h->route == PA_ROUTE_TRANSFORM) {
+        // keys in chunks: all kernels take the key index from the grid
+        const uint32_t chunk = ra_batch_keys(h);
+        for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
+            const uint32_t c = count - k0 < chunk ? count - k0 : chunk;
+            st = ra_hash_batch(h, keys + k0 * key_stride_words, key_stride_words, outs + k0 * out_stride_words,
+                               out_stride_words, c, (h->m + 31) / 32, (cudaStream_t)stream);
+            if (st != PA_OK) return st;
+        }
+        return PA_OK;
+    }
     for (uint32_t k = 0; k < count; ++k) {
         st = hash_impl(h, keys + k * key_stride_words, outs + k * out_stride_words,
                        (h->m + 31) / 32, (cudaStream_t)stream, false);

@@ -39,6 +39,7 @@ struct RouteA {
     RouteTables T{};
     unsigned long long *resid = nullptr; // max |v - rint v| (as double bits)
     uint32_t *kb = nullptr;    // K0 output: per-column-group bit streams of the input
+    uint32_t cap = 0;          // keys the work buffers (buf, kb) hold
 };
 
 // ---------------------------------------------------------------- route (b)
@@ -88,6 +89,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                   cudaStream_t s);
+pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
+                        uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s);
+uint32_t ra_batch_keys(const pa_ctx *h);
 void ra_destroy(pa_ctx *h);
 
 // route (b)

@@ -57,7 +57,8 @@ constexpr uint32_t kSmemLimit = 232448;
 
 #ifdef PA_TIMING
 __device__ unsigned long long g_k2_clk[3][64][16];
-#define TSTAMPK(k, i) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x < 64) g_k2_clk[k][blockIdx.x][i] = clock64(); } while (0)
+#define TSTAMPK(k, i) do { __syncthreads(); const unsigned _lb = blockIdx.x + gridDim.x * blockIdx.y; \
+    if (threadIdx.x == 0 && _lb < 64) g_k2_clk[k][_lb][i] = clock64(); } while (0)
 #define TSTAMP(i) TSTAMPK(1, i)
 __device__ unsigned long long g_trace[4][8192][3];  // per kernel (K0..K3), per CTA: smid, start, end ns
 __device__ __forceinline__ unsigned long long gtimer()
@@ -184,8 +185,10 @@ __host__ __device__ inline uint32_t k0_cols(const Geometry &g) { return g.N1 >= 
 
 __global__ void __launch_bounds__(256)
 k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, uint32_t *__restrict__ kb,
-                  Geometry g)
+                  Geometry g, uint64_t key_stride)
 {
+    w += blockIdx.z * key_stride;                             // batch: key blockIdx.z
+    kb += (uint64_t)blockIdx.z * (g.N1 / g.C) * g.kbw;
     TRACE_BEGIN(0);
     __shared__ uint32_t tre[kK0Rows][kK0Cols / 32 + 1], tim[kK0Rows][kK0Cols / 32 + 1];
     grid_dep_launch();  // K1 may start its prologue (K0 is a single short wave)
@@ -236,8 +239,11 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
 // Column DIF of C adjacent columns; input = this group's bit stream from K0.
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
-               uint32_t *__restrict__ zero_out, uint64_t zero_words)
+               uint32_t *__restrict__ zero_out, uint64_t zero_words, uint64_t out_stride)
 {
+    kb += (uint64_t)blockIdx.y * (g.N1 / g.C) * g.kbw;        // batch: key blockIdx.y
+    buf += (uint64_t)blockIdx.y * g.M;
+    if (zero_out) zero_out += blockIdx.y * out_stride;
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
@@ -326,7 +332,10 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
     double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi, *rhi = rlo + 64;
-    const uint32_t row = blockIdx.x;
+    // grid (keys, rows): the CTAs of one spectrum row run back to back, so the row is
+    // read from HBM once per batch and served from L2 to the other keys
+    const uint32_t row = blockIdx.y;
+    buf += (uint64_t)blockIdx.x * g.M;
     TRACE_BEGIN(2);
     TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
@@ -384,8 +393,10 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
 // ------------------------------------------------------------------ K3
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
-               uint32_t *__restrict__ out, unsigned long long *__restrict__ resid)
+               uint32_t *__restrict__ out, unsigned long long *__restrict__ resid, uint64_t out_stride)
 {
+    buf += (uint64_t)blockIdx.y * g.M;                        // batch: key blockIdx.y
+    out += blockIdx.y * out_stride;
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
@@ -652,6 +663,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     if ((st = alloc((void **)&T.rev2, g.N2 * sizeof(uint32_t), h, "rev2"))) return st;
     if ((st = alloc((void **)&a.resid, sizeof(unsigned long long), h, "resid"))) return st;
     if ((st = alloc((void **)&a.kb, (size_t)(g.N1 / g.C) * g.kbw * 4, h, "kb"))) return st;
+    a.cap = 1;
     double2 *p = a.tables;
     T.W1lo = p; p += 64;
     T.W1hi = p; p += g.f1.nhi;
@@ -674,9 +686,9 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
     // seed spectrum: K1 + forward half of K2, scaled by 1/M
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
-    k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g);
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, T, nullptr, 0);
-    k2_rows<<<g.N2, g.t2, g.smem2, s>>>(a.buf, a.spec, g, T, 1, 1.0 / (double)g.M);
+    k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, T, nullptr, 0, 0);
+    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.spec, g, T, 1, 1.0 / (double)g.M);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) create launches");
     h->kernels_per_hash = 4;
     return PA_OK;
@@ -699,26 +711,76 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words, cudaStream_t s)
+// Work buffers for `count` keys in flight (grown on demand, kept for the next call).
+static pa_status ra_reserve(pa_ctx *h, uint32_t count)
 {
     RouteA &a = h->a;
+    if (count <= a.cap) return PA_OK;
     const Geometry &g = a.g;
-    const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
+    const size_t kbk = (size_t)(g.N1 / g.C) * g.kbw * 4;
+    double2 *nb = nullptr;
+    uint32_t *nk = nullptr;
+    cudaError_t e = cudaMalloc(&nb, (size_t)count * g.M * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&nk, (size_t)count * kbk);
+    if (e != cudaSuccess) {
+        if (nb) cudaFree(nb);
+        cudaGetLastError();
+        set_error("route (a): cannot allocate work buffers for %u keys (%llu bytes): %s", count,
+                  (unsigned long long)((size_t)count * (g.M * sizeof(double2) + kbk)), cudaGetErrorString(e));
+        return PA_ERR_NOMEM;
+    }
+    // the handle's own single-key buffers are freed when replaced (stream-ordered via sync)
+    cudaStreamSynchronize(0);
+    cudaDeviceSynchronize();
+    h->ws_bytes += (size_t)(count - a.cap) * (g.M * sizeof(double2) + kbk);
+    cudaFree(a.buf);
+    cudaFree(a.kb);
+    a.buf = nb;
+    a.kb = nk;
+    a.cap = count;
+    return PA_OK;
+}
+
+uint32_t ra_batch_keys(const pa_ctx *h)
+{
+    // keys per launch: enough CTAs to fill the GPU for small transforms, within 4 GiB
+    const Geometry &g = h->a.g;
+    const double per_key = (double)g.M * 16.0 + (double)(g.N1 / g.C) * g.kbw * 4;
+    uint32_t by_mem = (uint32_t)std::max(1.0, std::floor(4.0 * (1u << 30) / per_key));
+    uint32_t by_fill = (uint32_t)std::max<uint64_t>(1, (4 * 148 + g.N2 - 1) / g.N2);
+    return std::min<uint32_t>(64, std::min(by_mem, std::max<uint32_t>(by_fill, 4)));
+}
+
+pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
+                        uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s)
+{
+    pa_status st = ra_reserve(h, count);
+    if (st != PA_OK) return st;
+    RouteA &a = h->a;
+    const Geometry &g = a.g;
+    const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), count);
     prof_begin(h, 4, s);
-    k0_bits_transpose<<<g0, 256, 0, s>>>(key, 0, h->n, a.kb, g);
+    k0_bits_transpose<<<g0, 256, 0, s>>>(keys, 0, h->n, a.kb, g, key_stride);
     prof_end(h, s);
     prof_begin(h, 0, s);
-    launch_pdl(k1_fwd_columns, g.N1 / g.C, g.t1, g.smem1, s, a.kb, a.buf, g, a.T, out, zero_words);
+    launch_pdl(k1_fwd_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
+               out_stride);
     prof_end(h, s);
     prof_begin(h, 1, s);
-    launch_pdl(k2_rows, g.N2, g.t2, g.smem2, s, a.buf, a.spec, g, a.T, 0, 1.0);
+    launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.spec, g, a.T, 0, 1.0);
     prof_end(h, s);
     prof_begin(h, 2, s);
-    launch_pdl(k3_inv_columns, g.N1 / g.C, g.t1, g.smem1, s, a.buf, g, a.T, h->n, h->m, out, a.resid);
+    launch_pdl(k3_inv_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf, g, a.T, h->n, h->m, outs,
+               a.resid, out_stride);
     prof_end(h, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (a) hash launches");
     return PA_OK;
+}
+
+pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words, cudaStream_t s)
+{
+    return ra_hash_batch(h, key, 0, out, 0, 1, zero_words, s);
 }
 
 #ifdef PA_TIMING

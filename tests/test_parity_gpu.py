@@ -237,3 +237,26 @@ def test_tiny_transform_edge_cases():
             sw = syn.random_bits(1000 + sv, n + m - 1)
             kw = syn.random_bits(2000 + sv, n)
             check(n, m, sw, kw, "transform", full=True)
+
+
+@pytest.mark.parametrize("n,m,count", [(1_048_576, 104_857, 70), (3_000_000, 300_000, 9), (200_003, 50_000, 1)])
+def test_batch_native_many_keys(n, m, count):
+    """pa_hash_batch on the transform route runs keys in grid-batched chunks
+    (BASELINE.json configs[4] shape); every output equals its own oracle result."""
+    sw = syn.random_bits(syn.seed_stream(55), n + m - 1)
+    kw32 = (n + 31) // 32
+    stride = (kw32 + 3) // 4 * 4
+    keys = [syn.random_bits(syn.key_stream(55, k), n) for k in range(count)]
+    mat = np.zeros((count, stride), np.int32)
+    for k, w in enumerate(keys):
+        mat[k, :kw32] = w.view(np.int32)[:kw32]
+    with pa.Hasher(n, m, to_dev(sw), route="transform") as h:
+        outs = h.hash_batch(torch.from_numpy(mat).to(DEV)).cpu().numpy()
+        single = from_dev(h.hash(to_dev(keys[-1])), m)
+        assert h.residual() < 1e-3
+    rows = sample_rows(m, 3, 512)
+    for k in sorted({0, count // 2, count - 1}):
+        got = oracle.unpack(outs[k].view(np.uint32), m)
+        assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, keys[k], rows)), k
+        assert not oracle.unpack(outs[k].view(np.uint32), 32 * ((m + 31) // 32))[m:].any()
+    assert np.array_equal(oracle.unpack(outs[-1].view(np.uint32), m), single)
