@@ -107,6 +107,13 @@ pa_status pa_create(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_b
 pa_status pa_create_ex(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits,
                        const pa_options *opt, void *stream);
 
+/* Rebind the handle to a new seed (same n, m, seed_bit_offset): the paper's
+ * protocol draws a fresh uniform seed for every privacy-amplification round
+ * (Sec. 2.3 Step 1).  Stream-ordered: hashes enqueued before this call use
+ * the old seed, hashes after it the new one.  Route (a) recomputes the cached
+ * spectrum (one forward transform, ~half a hash); route (b) re-reverses the seed. */
+pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream);
+
 /* y = T x.  key_bits: device, ceil(n/32) uint32 words; bits >= n are ignored.
  * out_bits: device, ceil(m/32) uint32 words; every bit >= m is written 0.
  * Deterministic, bit-exact, stream-ordered, asynchronous. */
@@ -155,6 +162,13 @@ typedef struct pa_kernel_time {
 
 pa_status pa_profile_enable(pa_handle h, int enable);
 pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32_t *count);
+
+/* Modulo-2 addition of partial hashes (Eq. (7)): dst[w] = XOR over
+ * g < count of src[g * src_stride_words + w], w < words.  Device pointers,
+ * 16-byte aligned, src_stride_words a multiple of 4; dst may alias src's first
+ * vector.  Used by the multi-GPU input-column split after NCCL gathers partials. */
+pa_status pa_xor_fold(uint32_t *dst, const uint32_t *src, uint64_t words, uint32_t count,
+                      uint64_t src_stride_words, void *stream);
 
 /* Stream-ordered release of everything the handle owns.  Safe on NULL. */
 void pa_destroy(pa_handle h);

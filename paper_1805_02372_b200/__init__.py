@@ -23,7 +23,7 @@ from ._lib import (PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISI
                    PA_ERR_UNSUPPORTED, PA_OK, PA_RESIDUAL_LIMIT, PA_ROUTE_AUTO, PA_ROUTE_BITPACKED,
                    PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
                    pa_get_info, pa_hash, pa_hash_batch, pa_hash_host, pa_hash_u64, pa_last_error,
-                   pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_residual, pa_status_string,
+                   pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_set_seed, pa_xor_fold, pa_residual, pa_status_string,
                    pa_version)
 
 ROUTES = {"auto": PA_ROUTE_AUTO, "transform": PA_ROUTE_TRANSFORM, "bitpacked": PA_ROUTE_BITPACKED}
@@ -116,6 +116,12 @@ class Hasher:
         with torch.cuda.device(self.device):
             pa_hash_host(self._h, key_host.data_ptr(), out_host.data_ptr(), _stream_ptr(stream))
         return out_host
+
+    def set_seed(self, seed: torch.Tensor, stream=None) -> None:
+        """Fresh seed for the next hashes (pa_set_seed; same n, m, seed_bit_offset)."""
+        _need_cuda(seed, "seed", self.n + self.m - 1)
+        with torch.cuda.device(self.device):
+            pa_set_seed(self._h, seed.data_ptr(), _stream_ptr(stream))
 
     def residual(self, stream=None) -> float:
         with torch.cuda.device(self.device):

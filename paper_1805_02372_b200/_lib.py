@@ -32,7 +32,7 @@ PA_RESIDUAL_LIMIT = 0.25
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
-            "pa_profile_read", "pa_plan"]
+            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold"]
 
 
 class PaError(RuntimeError):
@@ -85,6 +85,8 @@ _sig = {
     "pa_version": (ctypes.c_uint32, []),
     "pa_profile_enable": (_st, [_H, ctypes.c_int]),
     "pa_plan": (_st, [_u64, _u64, ctypes.POINTER(pa_info)]),
+    "pa_set_seed": (_st, [_H, _p, _p]),
+    "pa_xor_fold": (_st, [_p, _p, _u64, ctypes.c_uint32, _u64, _p]),
     "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
                               ctypes.POINTER(ctypes.c_uint32)]),
 }
@@ -186,3 +188,12 @@ def pa_plan(n: int, m: int) -> dict:
     info = pa_info()
     _check(_lib.pa_plan(n, m, ctypes.byref(info)))
     return info.as_dict()
+
+
+def pa_set_seed(h: int, seed_ptr: int, stream: int = 0) -> None:
+    _check(_lib.pa_set_seed(h, seed_ptr, stream))
+
+
+def pa_xor_fold(dst_ptr: int, src_ptr: int, words: int, count: int, src_stride_words: int,
+                stream: int = 0) -> None:
+    _check(_lib.pa_xor_fold(dst_ptr, src_ptr, words, count, src_stride_words, stream))

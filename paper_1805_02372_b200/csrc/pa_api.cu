@@ -263,6 +263,18 @@ pa_status pa_create_u64(pa_handle *h, uint64_t n, uint64_t m, const uint64_t *se
     return pa_create_ex(h, n, m, (const uint32_t *)seed_bits, nullptr, stream);
 }
 
+pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream)
+{
+    if (!h) {
+        set_error("handle is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    pa_status st = check_dev_ptr(seed_bits, "seed_bits", h->device);
+    if (st != PA_OK) return st;
+    return h->route == PA_ROUTE_TRANSFORM ? ra_seed(h, seed_bits, (cudaStream_t)stream)
+                                          : rb_seed(h, seed_bits, (cudaStream_t)stream);
+}
+
 static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                            cudaStream_t s, bool validate)
 {

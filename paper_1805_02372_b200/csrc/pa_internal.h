@@ -87,6 +87,7 @@ namespace pa {
 // route (a)
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen);
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
+pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                   cudaStream_t s);
 pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
@@ -96,6 +97,7 @@ void ra_destroy(pa_ctx *h);
 
 // route (b)
 pa_status rb_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
+pa_status rb_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                   cudaStream_t s);
 void rb_destroy(pa_ctx *h);

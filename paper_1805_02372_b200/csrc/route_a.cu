@@ -673,6 +673,23 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     T.thhi = p; p += g.f2.nhi;
 
     cudaError_t e;
+    if ((e = cudaMemsetAsync(a.resid, 0, sizeof(unsigned long long), s)) != cudaSuccess)
+        return cuda_fail(e, "route (a) residual reset");
+    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
+    k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) table launch");
+    h->kernels_per_hash = 4;
+    return ra_seed(h, seed, s);
+}
+
+// Seed spectrum: K0 + K1 + forward half of K2 on the seed, scaled by 1/M.  Uses the
+// hash work buffers as scratch (stream-ordered with the hashes).
+pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
+{
+    RouteA &a = h->a;
+    const Geometry &g = a.g;
+    cudaError_t e;
+    // per call: the attribute is per device and a process may drive several
     if ((e = cudaFuncSetAttribute(k1_fwd_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -680,17 +697,11 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         (e = cudaFuncSetAttribute(k3_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess)
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
-    if ((e = cudaMemsetAsync(a.resid, 0, sizeof(unsigned long long), s)) != cudaSuccess)
-        return cuda_fail(e, "route (a) residual reset");
-    uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
-    k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
-    // seed spectrum: K1 + forward half of K2, scaled by 1/M
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, T, nullptr, 0, 0);
-    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.spec, g, T, 1, 1.0 / (double)g.M);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) create launches");
-    h->kernels_per_hash = 4;
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0);
+    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) seed transform launches");
     return PA_OK;
 }
 

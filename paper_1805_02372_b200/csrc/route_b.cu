@@ -95,12 +95,17 @@ pa_status rb_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         return PA_ERR_NOMEM;
     }
     h->ws_bytes += h->b.srw * sizeof(uint32_t);
+    h->kernels_per_hash = 1;
+    return rb_seed(h, seed, s);
+}
+
+pa_status rb_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
+{
     uint64_t gw = (h->b.srw + 255) / 256;
     int grid = (int)(gw < 4096 ? gw : 4096);
     k_reverse_seed<<<grid, 256, 0, s>>>(seed, h->off, h->L, h->b.sr, h->b.srw);
-    e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (b) seed reversal launch");
-    h->kernels_per_hash = 1;
     return PA_OK;
 }
 

@@ -9,8 +9,9 @@ Three exact decompositions of y = T x (Eq. (1)):
 * Input-column split (the paper's Eq. (4) block division, with the
   Eq. (7) modulo-2 merge): rank g owns key bits [c0, c1) and the seed
   window s[n - c1 : n - c0 + m - 1]; partial m-bit hashes are XOR-reduced.  NCCL
-  has no XOR reduction (nccl.h: Sum/Prod/Max/Min/Avg), so the merge is an
-  all-gather of the packed partials followed by an XOR fold (exact, order-free).
+  has no XOR reduction (nccl.h: Sum/Prod/Max/Min/Avg), so the merge is a
+  reduce-scatter built from all_to_all_single + libpa's XOR-fold kernel, then an
+  all-gather (exact, order-free).
 * Independent keys (configs[4]): keys are dealt round-robin; no collective on
   the data path.
 
@@ -129,30 +130,55 @@ def hash_rows(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=N
     return out
 
 
+def _xor_fold_libpa(parts: torch.Tensor) -> torch.Tensor:
+    """XOR of the rows of `parts` ((G, words) int32, CUDA) with libpa's k_xor_fold."""
+    from . import pa_xor_fold
+    G, words = parts.shape
+    out = torch.empty(words, dtype=torch.int32, device=parts.device)
+    pa_xor_fold(out.data_ptr(), parts.data_ptr(), words, G, parts.stride(0),
+                torch.cuda.current_stream(parts.device).cuda_stream)
+    return out
+
+
+def _xor_fold_host(parts: torch.Tensor) -> torch.Tensor:
+    """CPU tensors (gloo tests): the same fold with torch bitwise ops."""
+    out = parts[0].clone()
+    for g in range(1, parts.shape[0]):
+        out ^= parts[g]
+    return out
+
+
 def hash_cols(n: int, m: int, seed_t: torch.Tensor, key_words: np.ndarray, group=None,
-              hash_fn: Callable | None = None, device=None) -> torch.Tensor:
-    """Input-column split with XOR merge: returns all ceil(m/32) words of y on every rank.
-    key_words: the full key (host, LSB-first); each rank uploads only its block."""
+              hash_fn: Callable | None = None, device=None, xor_fn: Callable | None = None) -> torch.Tensor:
+    """Input-column split with the Eq. (7) XOR merge; returns all ceil(m/32) words of y on
+    every rank.  key_words: the full key (host, LSB-first); each rank uploads its block.
+
+    Merge = XOR reduce-scatter + all-gather: the packed partial (words padded to a
+    multiple of 4*G) is cut into G slices, one all_to_all_single sends slice g to rank g,
+    rank g XOR-folds the G copies of its slice (libpa k_xor_fold), and one
+    all_gather_into_tensor assembles y -- 2 * m/8 bytes per rank on the wire."""
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     c0, c1 = col_ranges(n, m, world)[rank]
     words = (m + WORD - 1) // WORD
     dev = device if device is not None else seed_t.device
     hf = hash_fn or _LibpaHash()
-    mine = torch.zeros(words, dtype=torch.int32, device=dev)
+    fold = xor_fn or (_xor_fold_libpa if dev.type == "cuda" else _xor_fold_host)
+    slice_w = ((words + world - 1) // world + 3) // 4 * 4
+    mine = torch.zeros(world * slice_w, dtype=torch.int32, device=dev)
     if c1 > c0:
         blk = extract_bits(key_words, c0, c1 - c0)
         kt = torch.zeros(_words4(c1 - c0), dtype=torch.int32)
         kt[:blk.size] = torch.from_numpy(blk.view(np.int32))
         part = hf(c1 - c0, m, seed_t, col_seed_offset(n, c0, c1), kt.to(dev))
-        mine[:] = part[:words]
-    gathered = torch.empty(world * words, dtype=torch.int32, device=dev)
-    dist.all_gather_into_tensor(gathered, mine, group=group)
-    out = gathered.view(world, words)[0].clone()
-    for g in range(1, world):
-        out ^= gathered.view(world, words)[g]
+        mine[:words] = part[:words]
+    recv = torch.empty_like(mine)
+    dist.all_to_all_single(recv, mine, group=group)
+    myslice = fold(recv.view(world, slice_w))
+    gathered = torch.empty(world * slice_w, dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(gathered, myslice, group=group)
     if hash_fn is None:
         hf.close()
-    return out
+    return gathered[:words].clone()
 
 
 def hash_keys(n: int, m: int, seed_t: torch.Tensor, keys: torch.Tensor, group=None,

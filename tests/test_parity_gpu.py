@@ -260,3 +260,69 @@ def test_batch_native_many_keys(n, m, count):
         assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, keys[k], rows)), k
         assert not oracle.unpack(outs[k].view(np.uint32), 32 * ((m + 31) // 32))[m:].any()
     assert np.array_equal(oracle.unpack(outs[-1].view(np.uint32), m), single)
+
+
+@pytest.mark.parametrize("route", ["transform", "bitpacked"])
+def test_fresh_seed_per_key(route):
+    """pa_set_seed: a new seed per round gives the same result as a
+    handle created on that seed, and hashes queued before the call keep the old one."""
+    n, m = 70_001, 17_000
+    s1 = syn.random_bits(syn.seed_stream(61), n + m - 1)
+    s2 = syn.random_bits(syn.seed_stream(62), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(61, 0), n)
+    with pa.Hasher(n, m, to_dev(s1), route=route) as h:
+        key = to_dev(kw)
+        y1 = h.hash(key)
+        h.set_seed(to_dev(s2))
+        y2 = h.hash(key)
+        torch.cuda.synchronize()
+        assert np.array_equal(from_dev(y1, m), oracle.unpack(oracle.toeplitz_words(n, m, s1, kw), m))
+        assert np.array_equal(from_dev(y2, m), oracle.unpack(oracle.toeplitz_words(n, m, s2, kw), m))
+
+
+def test_xor_fold_kernel():
+    """pa_xor_fold: XOR of G packed partials (the Eq. (7) merge)."""
+    rng = np.random.default_rng(5)
+    for G, words in ((1, 7), (5, 1027), (8, 4096)):
+        stride = (words + 3) // 4 * 4
+        src = rng.integers(-2**31, 2**31 - 1, size=(G, stride), dtype=np.int64).astype(np.int32)
+        want = np.bitwise_xor.reduce(src[:, :words], axis=0)
+        s = torch.from_numpy(src).to(DEV)
+        d = torch.full((stride,), 7, dtype=torch.int32, device=DEV)
+        pa.pa_xor_fold(d.data_ptr(), s.data_ptr(), words, G, stride, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy()[:words], want)
+
+
+def test_dist_driver_single_rank_nccl():
+    """dist.hash_rows / hash_cols / hash_keys through libpa and NCCL (world size 1 on
+    this box; the multi-rank split arithmetic is covered on CPU with gloo)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1805_02372_b200 import dist as pd
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        n, m = 300_007, 60_000
+        sw = syn.random_bits(syn.seed_stream(71), n + m - 1)
+        kw = syn.random_bits(syn.key_stream(71, 0), n)
+        want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+        seed_t = to_dev(sw)
+        rows = pd.hash_rows(n, m, seed_t, to_dev(kw))
+        cols = pd.hash_cols(n, m, seed_t, kw)
+        torch.cuda.synchronize()
+        assert np.array_equal(from_dev(rows, m), want)
+        assert np.array_equal(from_dev(cols, m), want)
+        keys = torch.stack([to_dev(syn.random_bits(syn.key_stream(72, k), n)) for k in range(3)])
+        idx, outs = pd.hash_keys(n, m, seed_t, keys)
+        assert idx == [0, 1, 2]
+        for k in idx:
+            wk = oracle.unpack(oracle.toeplitz_words(n, m, sw, syn.random_bits(syn.key_stream(72, k), n)), m)
+            assert np.array_equal(from_dev(outs[k], m), wk)
+    finally:
+        dist.destroy_process_group()
