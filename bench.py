@@ -127,16 +127,22 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config, kernel):
-    """dram__bytes_read+write per launch of `kernel` from the committed ncu summary."""
+def ncu_kernel(config, kernel):
+    """The committed `ncu --set full` summary of `kernel` (profiles/ncu_<config>.json)."""
     path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
     try:
         for d in json.load(open(path)):
             if d.get("kernel") == kernel:
-                return float(d["dram_read"] + d["dram_write"]) * 1e9
+                return d
     except Exception:
         pass
     return None
+
+
+def ncu_traffic(config, kernel):
+    """dram__bytes_read+write per launch of `kernel` from the committed ncu summary."""
+    d = ncu_kernel(config, kernel)
+    return None if d is None else float(d["dram_read"] + d["dram_write"]) * 1e9
 
 
 def alg_bytes(kernel, info):
@@ -260,11 +266,16 @@ def run_ours(args):
                 b = alg_bytes(top, info)
                 achieved = b / (per[top] * 1e-3) / 1e9
                 traffic = ncu_traffic(name, top)
+                nk = ncu_kernel(name, top) or {}
                 roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": b,
                         "avg_launch_us": per[top] * 1e3, "peak_source": peak_src,
-                        "note": "achieved = algorithmic bytes / CUDA-event launch time; the working "
-                                "set of small configs is partly L2-resident, so frac can exceed HBM"}
+                        "fp64_pipe_frac_ncu": (nk.get("fp64_pipe_pct") or 0) / 100 or None,
+                        "issue_active_frac_ncu": (nk.get("issue_pct") or 0) / 100 or None,
+                        "note": "achieved = algorithmic HBM bytes / CUDA-event launch time vs the measured "
+                                "copy bandwidth.  The FFT passes are bound by the FP64 pipe and issue "
+                                "latency, not HBM (fp64_pipe_frac_ncu / issue_active_frac_ncu from the "
+                                "committed ncu capture, profiles/ncu_<config>.json); DESIGN.md Sec. 9"}
         line = {
             "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,

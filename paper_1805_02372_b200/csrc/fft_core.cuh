@@ -1,4 +1,4 @@
-// fft_core.cuh -- FP64 complex mixed-radix (2,3,4,5,7,8) FFT building blocks for
+// fft_core.cuh -- FP64 complex mixed-radix (2,3,4,5,7,8,16) FFT building blocks for
 // libpa route (a).  In-place stages on a batch of C interleaved sequences held in
 // padded shared memory; the first and last stage of a pass may load from / store
 // to anything (bits, global memory, the parity epilogue) through functors.
@@ -244,25 +244,15 @@ __device__ __forceinline__ void butterfly(double2 *v, uint32_t j, const StageDes
     if (INV) Dft<R, true>::run(v);
 }
 
-// Where a stage's inputs come from and its outputs go (the first and last stage
-// of a pass are fused with the pass's load / store / epilogue):
+// Where a stage's inputs come from and its outputs go (K2 fuses its row twist into
+// the first forward and the last inverse stage):
 //   MODE_PLAIN     smem -> smem
-//   MODE_TAU_IN    smem * rho^idx -> smem              (K2 first forward stage)
+//   MODE_TAU_IN    smem * rho^idx -> smem                   (K2 first forward stage)
 //   MODE_TAU_OUT   smem -> conj(rho^idx) * . -> gout[idx]   (K2 last inverse stage)
-//   MODE_BITS_IN   key bits (rowbits[b]) * theta_b -> smem (K1 first stage)
-//   MODE_COLS_OUT  smem -> gcols[idx * N1 + a0 + c]     (K1 last stage)
-//   MODE_EPI       smem -> untwist, window, rint, parity, ballot-pack, atomicOr (K3 last stage)
-enum { MODE_PLAIN = 0, MODE_TAU_IN = 1, MODE_TAU_OUT = 2, MODE_BITS_IN = 3, MODE_COLS_OUT = 4, MODE_EPI = 5 };
+enum { MODE_PLAIN = 0, MODE_TAU_IN = 1, MODE_TAU_OUT = 2 };
 struct StageCtx {
-    const double2 *rlo = nullptr, *rhi = nullptr;    // rho tables (K2)
+    const double2 *rlo = nullptr, *rhi = nullptr;    // rho^e two-level tables (K2 row)
     double2 *gout = nullptr;                         // K2 row in global memory
-    const uint32_t *rowbits = nullptr;               // K1: re bits | im bits << 16 per row
-    const double2 *thlo = nullptr, *thhi = nullptr;  // theta_b two-level tables (K1, K3)
-    double2 *gcols = nullptr;                        // K1 work array
-    uint32_t N1 = 0, a0 = 0, C = 1;
-    uint32_t *out = nullptr;                         // K3 output bits
-    int64_t t0 = 0, t1 = 0, M = 0;                   // K3 window [t0, t1), complex length
-    int64_t blo = 0, bhi = 0;                        // K3 rows that can hold window bits
 };
 
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
@@ -270,16 +260,14 @@ struct StageCtx {
 //   DIF (forward): v = DFT_R(v); v_k *= omega_L^{jk}
 //   DIT (inverse): v_k *= conj omega_L^{jk}; v = IDFT_R(v)
 // Not inlined: one copy per (R, direction, mode) per kernel keeps the code in
-// the instruction cache.  Returns the largest rounding residual (MODE_EPI).
+// the instruction cache.
 template <int R, bool INV, int MODE>
-__device__ __noinline__ double stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
-                                          const double2 *whi, StageCtx x)
+__device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
+                                        const double2 *whi, StageCtx x)
 {
     const uint32_t nb = sd.nb << logC;
     const uint32_t cm = (1u << logC) - 1;
     const uint32_t stride = sd.Ls << logC;
-    const uint32_t lane = threadIdx.x & 31;
-    double rmax = 0.0;
     for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
         const uint32_t c = q & cm, t = q >> logC;
         const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
@@ -289,73 +277,34 @@ __device__ __noinline__ double stage_smem(double2 *sm, StageDesc sd, uint32_t lo
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const uint32_t idx = idx0 + r * sd.Ls;
-            if (MODE == MODE_BITS_IN) {
-                const uint32_t rb = x.rowbits[idx];
-                const double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (16 + c)) & 1u);
-                const double2 th = twiddle(x.thlo, x.thhi, idx);
-                v[r] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
-            } else {
-                v[r] = sm[pidx(base + r * stride)];
-                if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx));
-            }
+            v[r] = sm[pidx(base + r * stride)];
+            if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
         }
         butterfly<R, INV>(v, j, sd, wlo, whi);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const uint32_t idx = idx0 + r * sd.Ls;
             if (MODE == MODE_TAU_OUT) {
+                const uint32_t idx = idx0 + r * sd.Ls;
                 x.gout[idx] = cmulc(v[r], twiddle(x.rlo, x.rhi, idx));
-            } else if (MODE == MODE_COLS_OUT) {
-                x.gcols[(uint64_t)idx * x.N1 + x.a0 + c] = v[r];
-            } else if (MODE == MODE_EPI) {
-                // element (b = idx, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
-                const bool rowok = (int64_t)idx >= x.blo && (int64_t)idx < x.bhi;
-                const double2 wv = cmulc(v[r], twiddle(x.thlo, x.thhi, idx));
-                const int64_t u = (int64_t)x.a0 + c + (int64_t)x.N1 * idx;
-#pragma unroll
-                for (int part = 0; part < 2; ++part) {
-                    const int64_t tt = part ? u + x.M : u;
-                    const double val = part ? wv.y : wv.x;
-                    const bool in = rowok && tt >= x.t0 && tt < x.t1;
-                    const double rr = rint(val);
-                    if (in) rmax = fmax(rmax, fabs(val - rr));
-                    const bool bit = in && (((long long)rr) & 1);
-                    const uint32_t bal = __ballot_sync(__activemask(), bit);
-                    // lanes c = 0..C-1 of a run hold C consecutive output bits
-                    uint32_t run = (bal >> (lane - c)) & ((x.C == 32) ? 0xFFFFFFFFu : ((1u << x.C) - 1u));
-                    if (c == 0 && run) {
-                        int64_t i0 = tt - x.t0;
-                        if (i0 < 0) {
-                            run >>= (int)(-i0);
-                            i0 = 0;
-                        }
-                        const uint64_t wd = (uint64_t)i0 >> 5;
-                        const int sh = (int)(i0 & 31);
-                        atomicOr(x.out + wd, run << sh);
-                        if (sh && (run >> (32 - sh))) atomicOr(x.out + wd + 1, run >> (32 - sh));
-                    }
-                }
             } else {
                 sm[pidx(base + r * stride)] = v[r];
             }
         }
     }
-    return rmax;
 }
 
 template <bool INV, int MODE = MODE_PLAIN>
-__device__ __forceinline__ double stage_any(double2 *sm, const StageDesc &sd, uint32_t logC, const double2 *wlo,
-                                            const double2 *whi, const StageCtx &x = StageCtx{})
+__device__ __forceinline__ void stage_any(double2 *sm, const StageDesc &sd, uint32_t logC, const double2 *wlo,
+                                          const double2 *whi, const StageCtx &x = StageCtx{})
 {
     switch (sd.R) {
-    case 2: return stage_smem<2, INV, MODE>(sm, sd, logC, wlo, whi, x);
-    case 3: return stage_smem<3, INV, MODE>(sm, sd, logC, wlo, whi, x);
-    case 4: return stage_smem<4, INV, MODE>(sm, sd, logC, wlo, whi, x);
-    case 5: return stage_smem<5, INV, MODE>(sm, sd, logC, wlo, whi, x);
-    case 7: return stage_smem<7, INV, MODE>(sm, sd, logC, wlo, whi, x);
-    case 8: return stage_smem<8, INV, MODE>(sm, sd, logC, wlo, whi, x);
-    default: return stage_smem<16, INV, MODE>(sm, sd, logC, wlo, whi, x);
+    case 2: stage_smem<2, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
+    case 3: stage_smem<3, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
+    case 4: stage_smem<4, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
+    case 5: stage_smem<5, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
+    case 7: stage_smem<7, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
+    case 8: stage_smem<8, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
+    default: stage_smem<16, INV, MODE>(sm, sd, logC, wlo, whi, x); break;
     }
 }
 

@@ -51,9 +51,7 @@ constexpr uint32_t kSmemLimit = 232448;
 #ifndef PA_MINB
 #define PA_MINB 1
 #endif
-#ifndef PA_MAXRADIX16
-#define PA_MAXRADIX16 1
-#endif  // 227 KB opt-in dynamic shared memory per CTA
+  // 227 KB opt-in dynamic shared memory per CTA
 
 #ifdef PA_TIMING
 __device__ unsigned long long g_k2_clk[3][64][16];
@@ -502,12 +500,7 @@ bool make_plan(uint32_t Lt, FftPlan *P)
     if (e2 % 4 == 1) push(2);
     if (e2 % 4 == 2) push(4);
     if (e2 % 4 == 3) push(8);
-    if (PA_MAXRADIX16) {
-        for (int i = 0; i < e2 / 4; ++i) push(16);
-    } else {
-        for (int i = 0; i < (e2 / 4) * 4 / 3; ++i) push(8);
-        for (int i = 0; i < ((e2 / 4) * 4) % 3; ++i) push(2);
-    }
+    for (int i = 0; i < e2 / 4; ++i) push(16);
     P->S = S;
     P->Lt = Lt;
     P->nhi = (Lt + 63) / 64;
