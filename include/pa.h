@@ -131,6 +131,13 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
  * the stream before returning. key_host: ceil(n/32) words; out_host: ceil(m/32). */
 pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream);
 
+/* pa_hash_host without the final synchronisation: the copies and kernels are
+ * enqueued on `stream` (as one CUDA graph) and *out_host is valid once the stream
+ * reaches this point.  Lets a caller stream keys through a handle: successive calls
+ * on the same stream serialise on the GPU but not on the host.  key_host must stay
+ * unchanged and out_host unread until then. */
+pa_status pa_hash_host_async(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream);
+
 /* uint64-packed aliases (same bits on little-endian).  pa_hash_u64 writes all
  * ceil(m/64) output words, zero-filling the half-word past ceil(m/32). */
 pa_status pa_create_u64(pa_handle *h, uint64_t n, uint64_t m, const uint64_t *seed_bits,

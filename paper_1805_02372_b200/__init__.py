@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import (PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISION,  # noqa: F401
                    PA_ERR_UNSUPPORTED, PA_OK, PA_RESIDUAL_LIMIT, PA_ROUTE_AUTO, PA_ROUTE_BITPACKED,
                    PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
-                   pa_get_info, pa_hash, pa_hash_batch, pa_hash_host, pa_hash_u64, pa_last_error,
+                   pa_get_info, pa_hash, pa_hash_batch, pa_hash_host, pa_hash_host_async, pa_hash_u64, pa_last_error,
                    pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_set_seed, pa_xor_fold, pa_residual, pa_status_string,
                    pa_version)
 
@@ -122,6 +122,17 @@ class Hasher:
         _need_cuda(seed, "seed", self.n + self.m - 1)
         with torch.cuda.device(self.device):
             pa_set_seed(self._h, seed.data_ptr(), _stream_ptr(stream))
+
+    def hash_host_async(self, key_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> torch.Tensor:
+        """As hash_host but without the final synchronisation (pinned buffers; the
+        output is valid once `stream` reaches this call)."""
+        if key_host.is_cuda or out_host.is_cuda:
+            raise ValueError("hash_host_async takes CPU tensors")
+        if _nbits(key_host) < self.n or _nbits(out_host) < 32 * words32(self.m):
+            raise ValueError("host buffers too small")
+        with torch.cuda.device(self.device):
+            pa_hash_host_async(self._h, key_host.data_ptr(), out_host.data_ptr(), _stream_ptr(stream))
+        return out_host
 
     def residual(self, stream=None) -> float:
         with torch.cuda.device(self.device):

@@ -32,7 +32,7 @@ PA_RESIDUAL_LIMIT = 0.25
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
-            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold"]
+            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async"]
 
 
 class PaError(RuntimeError):
@@ -75,6 +75,7 @@ _sig = {
     "pa_hash": (_st, [_H, _p, _p, _p]),
     "pa_hash_batch": (_st, [_H, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
     "pa_hash_host": (_st, [_H, _p, _p, _p]),
+    "pa_hash_host_async": (_st, [_H, _p, _p, _p]),
     "pa_create_u64": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, _p]),
     "pa_hash_u64": (_st, [_H, _p, _p, _p]),
     "pa_residual": (_st, [_H, ctypes.POINTER(ctypes.c_double), _p]),
@@ -153,6 +154,10 @@ def pa_hash_batch(h: int, keys_ptr: int, key_stride_words: int, outs_ptr: int,
 
 def pa_hash_host(h: int, key_host_ptr: int, out_host_ptr: int, stream: int = 0) -> None:
     _check(_lib.pa_hash_host(h, key_host_ptr, out_host_ptr, stream))
+
+
+def pa_hash_host_async(h: int, key_host_ptr: int, out_host_ptr: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash_host_async(h, key_host_ptr, out_host_ptr, stream))
 
 
 def pa_residual(h: int, stream: int = 0) -> float:

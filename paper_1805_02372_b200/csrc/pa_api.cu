@@ -138,6 +138,8 @@ using namespace pa;
 
 extern "C" {
 
+static void drop_host_graph(pa_ctx *h);
+
 uint32_t pa_version(void) { return PA_VERSION; }
 
 const char *pa_last_error(void) { return g_err.c_str(); }
@@ -174,6 +176,7 @@ void pa_destroy(pa_handle h)
     cudaGetDevice(&prev);
     cudaSetDevice(h->device);
     prof_free(h->prof);
+    drop_host_graph(h);
     ra_destroy(h);
     rb_destroy(h);
     if (h->stage_key) cudaFree(h->stage_key);
@@ -338,7 +341,9 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
     if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
     if (h->route == PA_ROUTE_TRANSFORM) {
-        // keys in chunks: all kernels take the key index from the grid
+        // keys in chunks: all kernels take the key index from the grid.  Growing the
+        // work buffers reallocates them: a captured pa_hash_host graph must go.
+        if (count > 1 && h->a.cap < (count < ra_batch_keys(h) ? count : ra_batch_keys(h))) drop_host_graph(h);
         const uint32_t chunk = ra_batch_keys(h);
         for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
             const uint32_t c = count - k0 < chunk ? count - k0 : chunk;
@@ -356,7 +361,72 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
     return PA_OK;
 }
 
-pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream)
+static void drop_host_graph(pa_ctx *h)
+{
+    if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
+    if (h->host_graph) cudaGraphDestroy(h->host_graph);
+    h->host_exec = nullptr;
+    h->host_graph = nullptr;
+    h->h2d_node = h->d2h_node = nullptr;
+    h->g_key_host = nullptr;
+    h->g_out_host = nullptr;
+}
+
+// Capture H2D + the hash kernels + D2H once; later calls patch the two memcpy
+// nodes' host pointers and relaunch: one graph launch instead of six API calls.
+static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t *out_host, size_t kb, size_t ob)
+{
+    cudaStream_t cs;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "pa_hash_host capture stream");
+    pa_status st = PA_OK;
+    if ((e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) {
+        cudaStreamDestroy(cs);
+        return cuda_fail(e, "pa_hash_host begin capture");
+    }
+    cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, cs);
+    st = hash_impl(h, h->stage_key, h->stage_out, (h->m + 31) / 32, cs, false);
+    cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, cs);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (st != PA_OK || e != cudaSuccess || !g) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return st != PA_OK ? st : cuda_fail(e, "pa_hash_host end capture");
+    }
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    cudaGraphNode_t nodes[64];
+    if (nn > 64) nn = 64;
+    cudaGraphGetNodes(g, nodes, &nn);
+    cudaGraphNode_t h2d = nullptr, d2h = nullptr;
+    for (size_t i = 0; i < nn; ++i) {
+        cudaGraphNodeType ty;
+        cudaGraphNodeGetType(nodes[i], &ty);
+        if (ty != cudaGraphNodeTypeMemcpy) continue;
+        cudaMemcpy3DParms pr;
+        cudaGraphMemcpyNodeGetParams(nodes[i], &pr);
+        if (pr.kind == cudaMemcpyHostToDevice || pr.dstPtr.ptr == h->stage_key) h2d = nodes[i];
+        else d2h = nodes[i];
+    }
+    cudaGraphExec_t ex = nullptr;
+    if (!h2d || !d2h || (e = cudaGraphInstantiate(&ex, g, 0)) != cudaSuccess) {
+        cudaGraphDestroy(g);
+        cudaGetLastError();
+        return cuda_fail(e == cudaSuccess ? cudaErrorUnknown : e, "pa_hash_host graph instantiate");
+    }
+    h->host_graph = g;
+    h->host_exec = ex;
+    h->h2d_node = h2d;
+    h->d2h_node = d2h;
+    h->g_key_host = key_host;
+    h->g_out_host = out_host;
+    return PA_OK;
+}
+
+static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream,
+                                bool sync)
 {
     if (!h || !key_host || !out_host) {
         set_error("pa_hash_host: NULL argument (h=%p key_host=%p out_host=%p)", (void *)h,
@@ -377,14 +447,44 @@ pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host
         }
         h->ws_bytes += kb + ob;
     }
-    if ((e = cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        return cuda_fail(e, "pa_hash_host H2D");
-    pa_status st = hash_impl(h, h->stage_key, h->stage_out, (h->m + 31) / 32, s, false);
-    if (st != PA_OK) return st;
-    if ((e = cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-        return cuda_fail(e, "pa_hash_host D2H");
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host sync");
+    if (h->prof.on) {  // per-launch profiling events need the plain launches
+        if ((e = cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e, "pa_hash_host H2D");
+        pa_status st = hash_impl(h, h->stage_key, h->stage_out, (h->m + 31) / 32, s, false);
+        if (st != PA_OK) return st;
+        if ((e = cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+            return cuda_fail(e, "pa_hash_host D2H");
+    } else {
+        if (!h->host_exec) {
+            pa_status st = build_host_graph(h, key_host, out_host, kb, ob);
+            if (st != PA_OK) return st;
+        }
+        if (key_host != h->g_key_host) {
+            if ((e = cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->h2d_node, h->stage_key, key_host, kb,
+                                                        cudaMemcpyHostToDevice)) != cudaSuccess)
+                return cuda_fail(e, "pa_hash_host graph update (key)");
+            h->g_key_host = key_host;
+        }
+        if (out_host != h->g_out_host) {
+            if ((e = cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->d2h_node, out_host, h->stage_out, ob,
+                                                        cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return cuda_fail(e, "pa_hash_host graph update (out)");
+            h->g_out_host = out_host;
+        }
+        if ((e = cudaGraphLaunch(h->host_exec, s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host graph launch");
+    }
+    if (sync && (e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host sync");
     return PA_OK;
+}
+
+pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream)
+{
+    return hash_host_impl(h, key_host, out_host, stream, true);
+}
+
+pa_status pa_hash_host_async(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream)
+{
+    return hash_host_impl(h, key_host, out_host, stream, false);
 }
 
 pa_status pa_residual(pa_handle h, double *max_residual, void *stream)

@@ -80,6 +80,12 @@ struct pa_ctx {
     pa::Profiler prof;
     // staging for pa_hash_host
     uint32_t *stage_key = nullptr, *stage_out = nullptr;
+    // pa_hash_host as one CUDA graph (H2D, kernels, D2H); host pointers patched per call
+    cudaGraph_t host_graph = nullptr;
+    cudaGraphExec_t host_exec = nullptr;
+    cudaGraphNode_t h2d_node = nullptr, d2h_node = nullptr;
+    const void *g_key_host = nullptr;
+    void *g_out_host = nullptr;
 };
 
 namespace pa {

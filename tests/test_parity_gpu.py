@@ -326,3 +326,23 @@ def test_dist_driver_single_rank_nccl():
             assert np.array_equal(from_dev(outs[k], m), wk)
     finally:
         dist.destroy_process_group()
+
+
+def test_host_async_graph_repoints_buffers():
+    """pa_hash_host_async / pa_hash_host replay one captured CUDA graph; new host
+    buffers are patched into its copy nodes."""
+    n, m = 1_000_003, 250_000
+    sw = syn.random_bits(syn.seed_stream(81), n + m - 1)
+    keys = [syn.random_bits(syn.key_stream(81, k), n) for k in range(3)]
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        outs = []
+        for k, w in enumerate(keys):
+            kh = torch.from_numpy(w.view(np.int32).copy()).pin_memory()
+            oh = torch.zeros((m + 31) // 32, dtype=torch.int32).pin_memory()
+            (h.hash_host_async if k % 2 == 0 else h.hash_host)(kh, oh)
+            outs.append((kh, oh))
+        torch.cuda.synchronize()
+        rows = sample_rows(m, 9, 512)
+        for (kh, oh), w in zip(outs, keys):
+            got = oracle.unpack(oh.numpy().view(np.uint32), m)
+            assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, w, rows))
