@@ -170,6 +170,17 @@ typedef struct pa_kernel_time {
 pa_status pa_profile_enable(pa_handle h, int enable);
 pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32_t *count);
 
+/* Length-compatible hashing for keys whose single transform would be too long
+ * (Sec. 3, Fig. 1, Eq. (4)-(7)): T is cut into row blocks and
+ * key (column) blocks with n_b + m_b - 1 <= max_block_bits (0 = the largest block
+ * one handle supports); every block is a Toeplitz hash on the seed window at
+ * offset r0 + n - c1, and each row block's output is the XOR of its column
+ * blocks (Eq. (7)).  seed_bits: n+m-1 bits, key_bits: n bits, out_bits:
+ * ceil(m/32) words, all device.  Creates a temporary handle per block and
+ * synchronises `stream` before returning. */
+pa_status pa_hash_blocked(uint64_t n, uint64_t m, const uint32_t *seed_bits, const uint32_t *key_bits,
+                          uint32_t *out_bits, uint64_t max_block_bits, void *stream);
+
 /* Modulo-2 addition of partial hashes (Eq. (7)): dst[w] = XOR over
  * g < count of src[g * src_stride_words + w], w < words.  Device pointers,
  * 16-byte aligned, src_stride_words a multiple of 4; dst may alias src's first

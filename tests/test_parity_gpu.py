@@ -207,7 +207,8 @@ def test_batch_and_u64_and_host_paths():
         hh = pa.pa_create_u64(n, m, seed_t.data_ptr(), 0)
         try:
             out = torch.full(((m + 63) // 64 * 2,), -1, dtype=torch.int32, device=DEV)
-            pa.pa_hash_u64(hh, to_dev(keys[0]).data_ptr(), out.data_ptr(), 0)
+            key0 = to_dev(keys[0])  # keep alive across the call
+            pa.pa_hash_u64(hh, key0.data_ptr(), out.data_ptr(), 0)
             torch.cuda.synchronize()
             allb = oracle.unpack(out.cpu().numpy().view(np.uint32), 64 * ((m + 63) // 64))
             want = oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[0]), m)
@@ -346,3 +347,20 @@ def test_host_async_graph_repoints_buffers():
         for (kh, oh), w in zip(outs, keys):
             got = oracle.unpack(oh.numpy().view(np.uint32), m)
             assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, w, rows))
+
+
+@pytest.mark.parametrize("n,m,maxb", [(20_000, 7_000, 5_000), (50_001, 20_000, 16_384), (3001, 3000, 700),
+                                      (100_000, 10_000, 0)])
+def test_length_compatible_blocked(n, m, maxb):
+    """pa_hash_blocked: row x column block division with the Eq. (7) XOR merge equals
+    the single-transform hash (plan invariance)."""
+    sw = syn.random_bits(syn.seed_stream(91 + n), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(91, n), n)
+    out = torch.full(((m + 31) // 32 + 3,), -1, dtype=torch.int32, device=DEV)
+    seed_t, key_t = to_dev(sw), to_dev(kw)  # keep the tensors alive across the call
+    pa.pa_hash_blocked(n, m, seed_t.data_ptr(), key_t.data_ptr(), out.data_ptr(), maxb, 0)
+    torch.cuda.synchronize()
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    allb = oracle.unpack(out.cpu().numpy().view(np.uint32), 32 * ((m + 31) // 32))
+    assert np.array_equal(allb[:m], want)
+    assert not allb[m:].any()
