@@ -329,6 +329,21 @@ def sweep(torch, pa, dev, steps=10):
         res[name] = {"n": n, "m": m, "route": h.route, "ms_per_hash": t, "gbit_s": n / (t * 1e-3) / 1e9,
                      "transform_len": h.info["transform_len"], "residual": h.residual()}
         h.close()
+    # BASELINE configs[4] shape: independent keys against one seed through pa_hash_batch
+    for name, count in (("C5a", 256), ("C5c", 32)):
+        n, m, sw, kw = syn.config_inputs(name)
+        h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+        kw32 = (n + 31) // 32
+        stride = (kw32 + 3) // 4 * 4
+        keys = torch.zeros((count, stride), dtype=torch.int32, device=dev)
+        keys[:, :kw32] = dev_words(torch, kw, dev)[:kw32]
+        outs = h.new_out(count)
+        h.hash_batch(keys, outs)
+        ms = time_steps(torch, lambda: h.hash_batch(keys, outs), 3, flush)
+        t = float(np.mean(ms)) / count
+        res[name + "_batched"] = {"n": n, "m": m, "keys": count, "ms_per_key": t,
+                                  "gbit_s": n / (t * 1e-3) / 1e9, "transform_len": h.info["transform_len"]}
+        h.close()
     return res
 
 
