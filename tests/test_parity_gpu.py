@@ -364,3 +364,16 @@ def test_length_compatible_blocked(n, m, maxb):
     allb = oracle.unpack(out.cpu().numpy().view(np.uint32), 32 * ((m + 31) // 32))
     assert np.array_equal(allb[:m], want)
     assert not allb[m:].any()
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_worst_case_rounding_all_ones(name):
+    """All-ones key and seed maximise |x|_2 |s|_2 in the FP64 error bound (DESIGN.md
+    Sec. 5): every count is exactly n, so y[i] = n mod 2 for all i, and the recorded
+    residual must stay far below 0.5."""
+    n, m = syn.CONFIGS[name]["n"], syn.CONFIGS[name]["m"]
+    with pa.Hasher(n, m, to_dev(syn.ones_bits(n + m - 1))) as h:
+        got = from_dev(h.hash(to_dev(syn.ones_bits(n))), m)
+        res = h.residual()
+    assert np.all(got == (n & 1))
+    assert res < 1e-3, res
