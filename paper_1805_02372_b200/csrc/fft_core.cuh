@@ -253,6 +253,7 @@ enum { MODE_PLAIN = 0, MODE_TAU_IN = 1, MODE_TAU_OUT = 2 };
 struct StageCtx {
     const double2 *rlo = nullptr, *rhi = nullptr;    // rho^e two-level tables (K2 row)
     double2 *gout = nullptr;                         // K2 row in global memory
+    const double2 *gin = nullptr;                    // MODE_TAU_IN: read the row from here, not smem
 };
 
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
@@ -277,7 +278,8 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            v[r] = sm[pidx(base + r * stride)];
+            if (MODE == MODE_TAU_IN && x.gin) v[r] = x.gin[idx0 + r * sd.Ls];
+            else v[r] = sm[pidx(base + r * stride)];
             if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
         }
         butterfly<R, INV>(v, j, sd, wlo, whi);

@@ -341,8 +341,11 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi);
     rho_tables(rlo, rhi, g.f1.nhi, g.M, __ldg(T.rev2 + row));
     grid_dep_wait();  // K1's work array
-    for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
-    cp_async_wait_all();
+    const FftPlan &P0 = g.f1;
+    if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
+        cp_async_wait_all();
+    }
     __syncthreads();
     TSTAMP(1);
     const FftPlan &P = g.f1;
@@ -353,8 +356,13 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     if (P.S <= 1) {  // N1 <= 16: tau elementwise, then the single stage below runs plain
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
         __syncthreads();
-    } else {
+    } else if (mode == 1) {
         stage_any<false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
+        __syncthreads();
+    } else {
+        rt.gin = rp;  // hash path: the first stage reads the row straight from global memory
+        stage_any<false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
+        rt.gin = nullptr;
         __syncthreads();
     }
     const int dif_from = P.S <= 1 ? 0 : 1;
