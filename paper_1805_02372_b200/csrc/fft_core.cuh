@@ -249,11 +249,14 @@ __device__ __forceinline__ void butterfly(double2 *v, uint32_t j, const StageDes
 //   MODE_PLAIN     smem -> smem
 //   MODE_TAU_IN    smem * rho^idx -> smem                   (K2 first forward stage)
 //   MODE_TAU_OUT   smem -> conj(rho^idx) * . -> gout[idx]   (K2 last inverse stage)
-enum { MODE_PLAIN = 0, MODE_TAU_IN = 1, MODE_TAU_OUT = 2 };
+//   MODE_GCOL      gin[row * ld + c] -> smem               (K3 first inverse stage)
+//   MODE_GCOL_OUT  smem -> gout[row * ld + c]              (K1 last forward stage)
+enum { MODE_PLAIN = 0, MODE_TAU_IN = 1, MODE_TAU_OUT = 2, MODE_GCOL = 3, MODE_GCOL_OUT = 4 };
 struct StageCtx {
     const double2 *rlo = nullptr, *rhi = nullptr;    // rho^e two-level tables (K2 row)
     double2 *gout = nullptr;                         // K2 row in global memory
-    const double2 *gin = nullptr;                    // MODE_TAU_IN: read the row from here, not smem
+    const double2 *gin = nullptr;                    // MODE_TAU_IN / MODE_GCOL: global input
+    uint32_t ld = 0;                                 // MODE_GCOL(_OUT): row pitch in elements
 };
 
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
@@ -279,6 +282,7 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (MODE == MODE_TAU_IN && x.gin) v[r] = x.gin[idx0 + r * sd.Ls];
+            else if (MODE == MODE_GCOL) v[r] = x.gin[(uint64_t)(idx0 + r * sd.Ls) * x.ld + c];
             else v[r] = sm[pidx(base + r * stride)];
             if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
         }
@@ -288,6 +292,8 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
             if (MODE == MODE_TAU_OUT) {
                 const uint32_t idx = idx0 + r * sd.Ls;
                 x.gout[idx] = cmulc(v[r], twiddle(x.rlo, x.rhi, idx));
+            } else if (MODE == MODE_GCOL_OUT) {
+                x.gout[(uint64_t)(idx0 + r * sd.Ls) * x.ld + c] = v[r];
             } else {
                 sm[pidx(base + r * stride)] = v[r];
             }

@@ -275,12 +275,24 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     }
     __syncthreads();
     TSTAMPK(0, 3);
-    dif_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
-    grid_dep_launch();  // K2 may start its prologue
-    TSTAMPK(0, 4);
-    // row p of the work array = DIF output position p (k_b = rev2[p])
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-        buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
+    // row p of the work array = DIF output position p (k_b = rev2[p]).  The last forward
+    // stage writes it straight to global when the per-row chunk is >= 64 B (see K3)
+    const bool direct = g.f2.S > 1 && C >= 4;
+    if (direct) {
+        dif_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+        grid_dep_launch();  // K2 may start its prologue
+        StageCtx gx;
+        gx.gout = buf + a0;
+        gx.ld = g.N1;
+        stage_any<false, MODE_GCOL_OUT>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
+        TSTAMPK(0, 4);
+    } else {
+        dif_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+        grid_dep_launch();  // K2 may start its prologue
+        TSTAMPK(0, 4);
+        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
+            buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
+    }
     TSTAMPK(0, 5);
     TRACE_END(1);
 }
@@ -413,9 +425,15 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     grid_dep_wait();  // K2's rows
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-        cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
-    cp_async_wait_all();
+    // first inverse stage reads the columns straight from global when the per-row chunk is
+    // >= 64 B (C >= 4); with 32 B chunks (C = 2) the staged cp.async copy is faster (round 1:
+    // C4 K3 731 vs 986 us; C5c at C = 4 117 -> 111 us, C3 at C = 8 68 -> 64.5 us)
+    const bool direct = g.f2.S > 1 && C >= 4;
+    if (!direct) {
+        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
+            cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
+        cp_async_wait_all();
+    }
     __syncthreads();
     const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;  // output window [t0, t1)
     // only rows b holding some t in the window: u = a0 + c + N1 b (Re) or u + M (Im)
@@ -432,7 +450,16 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     const int64_t b_lo = std::min(rb1 > rb0 ? rb0 : (int64_t)g.N2, ib1 > ib0 ? ib0 : (int64_t)g.N2);
     const int64_t b_hi = std::max(rb1 > rb0 ? rb1 : 0, ib1 > ib0 ? ib1 : 0);
     TSTAMPK(2, 1);
-    dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    if (direct) {
+        StageCtx gx;
+        gx.gin = buf + a0;
+        gx.ld = g.N1;
+        stage_any<true, MODE_GCOL>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
+        __syncthreads();
+        dit_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+    } else {
+        dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    }
     TSTAMPK(2, 2);
     // epilogue: element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
     const uint32_t lane = threadIdx.x & 31;
