@@ -77,7 +77,18 @@ typedef struct pa_options {
                                  caller's seed buffer (row/column shards) */
     uint32_t allow_wide;      /* 1 = accept m > n (column shards of the Eq. (4) split,
                                  P:107-110, have n_g < m); default 0 keeps 1 <= m <= n */
-    uint32_t reserved[7];     /* must be zero */
+    uint32_t batch_keys;      /* keys per launch in pa_hash_batch (0 = library choice).  With
+                                 a caller workspace (pa_create_ws) it sizes the per-key work
+                                 buffers: 0 means 1 */
+    uint64_t max_transform_len; /* route (a): 0 = no limit.  Otherwise the key is cut into
+                                 column blocks (Eq. (4)) so that no block's real
+                                 transform length exceeds this; each block is hashed on its
+                                 own seed window (offset n - n_g - c0) and the partial outputs
+                                 are XOR-merged in place (Eq. (7)).  Blocks start at
+                                 multiples of 128 key bits.  PA_ERR_UNSUPPORTED if even a
+                                 128-bit block's transform (>= 128 + m - 1) exceeds it.  Ignored
+                                 by route (b) */
+    uint32_t reserved[3];     /* must be zero */
 } pa_options;
 
 /* Runtime facts about a handle (all lengths in bits or elements). */
@@ -90,9 +101,10 @@ typedef struct pa_info {
     uint64_t cols_per_cta;    /* route (a): columns per CTA in the strided passes */
     uint64_t workspace_bytes; /* device bytes owned by the handle */
     uint64_t kernels_per_hash;/* kernel launches enqueued by one pa_hash */
+    uint64_t column_blocks;   /* key blocks of the Eq. (4) split (1 = unsplit) */
 } pa_info;
 
-/* Fill *opt with defaults (route AUTO, offset 0, residual recorded). */
+/* Fill *opt with defaults (route AUTO, offset 0, library batch width, no split). */
 pa_status pa_options_init(pa_options *opt);
 
 /* Create a hashing context for n-bit keys and m-bit outputs with the
@@ -107,12 +119,44 @@ pa_status pa_create(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_b
 pa_status pa_create_ex(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits,
                        const pa_options *opt, void *stream);
 
+/* Caller-owned device memory (torch allocates, libpa carves): pa_workspace_size
+ * returns the exact bytes pa_create_ws needs for (n, m, *opt) (opt may be NULL =
+ * defaults) -- host-only, no device work.  pa_create_ws is pa_create_ex with every
+ * device buffer of the handle (seed spectrum, tables, per-key work buffers for
+ * opt->batch_keys keys, pa_hash_host staging) placed in `workspace` (device pointer
+ * on the current device, 256-byte aligned, >= the size, PA_ERR_NOMEM naming both
+ * numbers if smaller).  The caller keeps ownership: the workspace must outlive the
+ * handle and not be touched while it lives; pa_destroy does not free it. */
+pa_status pa_workspace_size(uint64_t n, uint64_t m, const pa_options *opt, uint64_t *bytes);
+pa_status pa_create_ws(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits,
+                       const pa_options *opt, void *workspace, uint64_t workspace_bytes,
+                       void *stream);
+
 /* Rebind the handle to a new seed (same n, m, seed_bit_offset): the paper's
  * protocol draws a fresh uniform seed for every privacy-amplification round
  * (Sec. 2.3 Step 1).  Stream-ordered: hashes enqueued before this call use
  * the old seed, hashes after it the new one.  Route (a) recomputes the cached
  * spectrum (one forward transform, ~half a hash); route (b) re-reverses the seed. */
 pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream);
+
+/* Fresh seed per key (Sec. 2.3 Step 1: every privacy-amplification round draws a
+ * new uniform seed): for k < count, rebind the handle to seed k (seeds +
+ * k*seed_stride_words, n+m-1 bits at the handle's seed_bit_offset) and hash key k into
+ * output k -- pa_set_seed + pa_hash per key, i.e. three transforms per key on route (a).
+ * Strides in uint32 words, multiples of 4.  Afterwards the handle holds the last seed. */
+pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_stride_words,
+                              const uint32_t *keys, uint64_t key_stride_words, uint32_t *outs,
+                              uint64_t out_stride_words, uint32_t count, void *stream);
+
+/* Seed layout converter (reading R2).  Eq. (1) names the n+l-1
+ * seed symbols t_0 .. t_{n+l-2} of the n x l matrix T of r = u T: T_{i,j} =
+ * t_{i-j} on and below the diagonal, t_{j-i+n-1} above it.  This library's T[i][j] =
+ * s[i-j+n-1] (y = T x) is the same hash when s[u] = t_{n-1-u} for u < n and s[u] = t_u
+ * for n <= u < n+m-1: the first n symbols reversed.  t_bits -> s_bits, both device,
+ * ceil((n+m-1)/32) words, LSB-first; bits past n+m-1 of s_bits are written 0.  The
+ * buffers must not overlap (PA_ERR_INVALID_ARG).  Stream-ordered. */
+pa_status pa_seed_from_paper_eq1(uint32_t *s_bits, const uint32_t *t_bits, uint64_t n, uint64_t m,
+                                 void *stream);
 
 /* y = T x.  key_bits: device, ceil(n/32) uint32 words; bits >= n are ignored.
  * out_bits: device, ceil(m/32) uint32 words; every bit >= m is written 0.

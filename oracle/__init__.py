@@ -21,6 +21,9 @@ toeplitz_bits_many(n, m, seed01, keys01)  same, many keys (exhaustive pin)
 toeplitz_rows(n, m, seed_w, key_w, rows)  64-bit word variant, sampled rows
 toeplitz_words(n, m, seed_w, key_w)       word variant, full packed output
 unpack(words, nbits) / pack(bits)         the oracle's own (numpy) bit packing
+eq1_matrix(t01, n, l)                     Eq. (1)'s n x l Toeplitz matrix, literally
+eq1_hash(t01, u01, n, l)                  the paper's r = u T over GF(2)
+seed_from_eq1(t01, n, m)                  Eq. (1) symbol order -> the diagonal order above
 
 Parity status: every function here is pinned by tests/test_oracle.py against
 brute force, hand-worked examples, closed forms, GF(2) polynomial
@@ -166,3 +169,42 @@ def toeplitz_words(n: int, m: int, seed_words, key_words, threads: int = 0) -> n
     if rc != 0:
         raise MemoryError("oracle_toeplitz_words failed")
     return out
+
+
+# ---------------------------------------------------------------- the paper's Eq. (1) form
+def eq1_matrix(t01, n: int, l: int) -> np.ndarray:
+    """Eq. (1) written out, generalised to n x l ("the Toeplitz matrix
+    is not necessarily square"; T is n x l in Sec. 2.3):
+
+        T[i, j] = t_{i-j}        for i >= j   (lower triangle and diagonal)
+        T[i, j] = t_{j-i+n-1}    for j >  i   (upper triangle)
+
+    t01 holds the n+l-1 symbols t_0 .. t_{n+l-2}."""
+    t = np.asarray(t01, dtype=np.uint8)
+    if t.size != n + l - 1:
+        raise ValueError(f"t has {t.size} symbols, Eq. (1) with n = {n}, l = {l} needs {n + l - 1}")
+    T = np.zeros((n, l), dtype=np.uint8)
+    for i in range(n):
+        for j in range(l):
+            T[i, j] = t[i - j] if i >= j else t[j - i + n - 1]
+    return T
+
+
+def eq1_hash(t01, u01, n: int, l: int) -> np.ndarray:
+    """r = u T over GF(2) (Sec. 2.3 Step 2): u the n-bit corrected key as a row
+    vector, T = eq1_matrix(t01, n, l); returns the l bits of r."""
+    u = np.asarray(u01, dtype=np.int64)
+    if u.size != n:
+        raise ValueError(f"u has {u.size} bits, need {n}")
+    return ((u @ eq1_matrix(t01, n, l).astype(np.int64)) & 1).astype(np.uint8)
+
+
+def seed_from_eq1(t01, n: int, m: int) -> np.ndarray:
+    """DESIGN.md reading R2: the diagonal-order seed s with y = T x, T[i][j] = s[i-j+n-1],
+    equal to Eq. (1)'s r = u T: s[k] = t_{n-1-k} for k < n, s[k] = t_k for n <= k < n+m-1."""
+    t = np.asarray(t01, dtype=np.uint8)
+    if t.size != n + m - 1:
+        raise ValueError(f"t has {t.size} symbols, need {n + m - 1}")
+    s = t.copy()
+    s[:n] = t[:n][::-1]
+    return s

@@ -24,7 +24,7 @@ from ._lib import (PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISI
                    PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
                    pa_get_info, pa_hash, pa_hash_batch, pa_hash_blocked, pa_hash_host, pa_hash_host_async, pa_hash_u64, pa_last_error,
                    pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_set_seed, pa_xor_fold, pa_residual, pa_status_string,
-                   pa_version)
+                   pa_version, pa_workspace_size, pa_create_ws, pa_hash_fresh_batch, pa_seed_from_paper_eq1)
 
 ROUTES = {"auto": PA_ROUTE_AUTO, "transform": PA_ROUTE_TRANSFORM, "bitpacked": PA_ROUTE_BITPACKED}
 
@@ -52,20 +52,61 @@ def _need_cuda(t: torch.Tensor, name: str, nbits: int) -> None:
         raise ValueError(f"{name} holds {_nbits(t)} bits, {nbits} required")
 
 
+def make_options(route: str = "auto", seed_bit_offset: int = 0, allow_wide: bool = False, batch_keys: int = 0,
+                 max_transform_len: int = 0):
+    """pa_options from keyword arguments (see include/pa.h for each field)."""
+    opt = pa_options_init()
+    opt.route = ROUTES[route]
+    opt.seed_bit_offset = int(seed_bit_offset)
+    opt.allow_wide = 1 if allow_wide else 0
+    opt.batch_keys = int(batch_keys)
+    opt.max_transform_len = int(max_transform_len)
+    return opt
+
+
+def workspace_size(n: int, m: int, **options) -> int:
+    """Device bytes a Hasher(n, m, ..., workspace=...) needs (pa_workspace_size)."""
+    return pa_workspace_size(int(n), int(m), make_options(**options))
+
+
+def seed_from_paper_eq1(t_words: torch.Tensor, n: int, m: int, out: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """Eq. (1)-ordered seed t -> this library's diagonal order (pa_seed_from_paper_eq1)."""
+    L = n + m - 1
+    _need_cuda(t_words, "t_words", L)
+    if out is None:
+        out = torch.empty(((words32(L) + 3) // 4 * 4,), dtype=torch.int32, device=t_words.device)
+    _need_cuda(out, "out", L)
+    with torch.cuda.device(t_words.device):
+        pa_seed_from_paper_eq1(out.data_ptr(), t_words.data_ptr(), int(n), int(m), _stream_ptr(stream))
+    return out
+
+
 class Hasher:
-    """One pa_handle: fixed (n, m, seed); hash any number of n-bit keys."""
+    """One pa_handle: fixed (n, m, seed); hash any number of n-bit keys.
+
+    workspace: optional CUDA tensor (>= workspace_size(n, m, ...) bytes, 256-byte
+    aligned) that holds all of the handle's device memory (pa_create_ws); the
+    Hasher keeps a reference to it.  max_transform_len forces the Eq. (4)
+    column split, batch_keys the keys per launch (include/pa.h pa_options)."""
 
     def __init__(self, n: int, m: int, seed: torch.Tensor, route: str = "auto",
-                 seed_bit_offset: int = 0, stream=None, allow_wide: bool = False):
+                 seed_bit_offset: int = 0, stream=None, allow_wide: bool = False, batch_keys: int = 0,
+                 max_transform_len: int = 0, workspace: torch.Tensor | None = None):
         _need_cuda(seed, "seed", seed_bit_offset + n + m - 1)
         self.n, self.m = int(n), int(m)
+        self.seed_bit_offset = int(seed_bit_offset)
         self.device = seed.device
-        opt = pa_options_init()
-        opt.route = ROUTES[route]
-        opt.seed_bit_offset = int(seed_bit_offset)
-        opt.allow_wide = 1 if allow_wide else 0
+        opt = make_options(route, seed_bit_offset, allow_wide, batch_keys, max_transform_len)
+        self._ws = workspace
         with torch.cuda.device(self.device):
-            self._h = pa_create_ex(self.n, self.m, seed.data_ptr(), opt, _stream_ptr(stream))
+            if workspace is None:
+                self._h = pa_create_ex(self.n, self.m, seed.data_ptr(), opt, _stream_ptr(stream))
+            else:
+                if not workspace.is_cuda or not workspace.is_contiguous():
+                    raise ValueError("workspace must be a contiguous CUDA tensor")
+                self._h = pa_create_ws(self.n, self.m, seed.data_ptr(), opt, workspace.data_ptr(),
+                                       workspace.numel() * workspace.element_size(), _stream_ptr(stream))
         self.info = pa_get_info(self._h)
 
     @property
@@ -117,9 +158,27 @@ class Hasher:
             pa_hash_host(self._h, key_host.data_ptr(), out_host.data_ptr(), _stream_ptr(stream))
         return out_host
 
+    def hash_fresh_batch(self, seeds: torch.Tensor, keys: torch.Tensor, outs: torch.Tensor | None = None,
+                         stream=None) -> torch.Tensor:
+        """Key k hashed with its own seed k (pa_hash_fresh_batch): seeds (count, words),
+        keys (count, words).  The handle keeps the last seed."""
+        if keys.dim() != 2 or seeds.dim() != 2 or seeds.shape[0] != keys.shape[0]:
+            raise ValueError("seeds and keys must be 2-D with one row per key")
+        count = keys.shape[0]
+        if outs is None:
+            outs = self.new_out(count)
+        _need_cuda(keys, "keys", self.n * count)
+        _need_cuda(seeds, "seeds", (self.seed_bit_offset + self.n + self.m - 1) * count)
+        _need_cuda(outs, "outs", self.m * count)
+        st = [t.stride(0) * t.element_size() // 4 for t in (seeds, keys, outs)]
+        with torch.cuda.device(self.device):
+            pa_hash_fresh_batch(self._h, seeds.data_ptr(), st[0], keys.data_ptr(), st[1], outs.data_ptr(), st[2],
+                                count, _stream_ptr(stream))
+        return outs
+
     def set_seed(self, seed: torch.Tensor, stream=None) -> None:
         """Fresh seed for the next hashes (pa_set_seed; same n, m, seed_bit_offset)."""
-        _need_cuda(seed, "seed", self.n + self.m - 1)
+        _need_cuda(seed, "seed", self.seed_bit_offset + self.n + self.m - 1)
         with torch.cuda.device(self.device):
             pa_set_seed(self._h, seed.data_ptr(), _stream_ptr(stream))
 

@@ -32,7 +32,8 @@ PA_RESIDUAL_LIMIT = 0.25
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
-            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked"]
+            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked",
+            "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1"]
 
 
 class PaError(RuntimeError):
@@ -44,14 +45,16 @@ class PaError(RuntimeError):
 class pa_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("route", ctypes.c_int32),
                 ("seed_bit_offset", ctypes.c_uint64), ("allow_wide", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 7)]
+                ("batch_keys", ctypes.c_uint32), ("max_transform_len", ctypes.c_uint64),
+                ("reserved", ctypes.c_uint32 * 3)]
 
 
 class pa_info(ctypes.Structure):
     _fields_ = [("n", ctypes.c_uint64), ("m", ctypes.c_uint64), ("route", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("transform_len", ctypes.c_uint64),
                 ("n1", ctypes.c_uint64), ("n2", ctypes.c_uint64), ("cols_per_cta", ctypes.c_uint64),
-                ("workspace_bytes", ctypes.c_uint64), ("kernels_per_hash", ctypes.c_uint64)]
+                ("workspace_bytes", ctypes.c_uint64), ("kernels_per_hash", ctypes.c_uint64),
+                ("column_blocks", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -88,6 +91,10 @@ _sig = {
     "pa_profile_enable": (_st, [_H, ctypes.c_int]),
     "pa_plan": (_st, [_u64, _u64, ctypes.POINTER(pa_info)]),
     "pa_set_seed": (_st, [_H, _p, _p]),
+    "pa_workspace_size": (_st, [_u64, _u64, ctypes.POINTER(pa_options), ctypes.POINTER(_u64)]),
+    "pa_create_ws": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, ctypes.POINTER(pa_options), _p, _u64, _p]),
+    "pa_hash_fresh_batch": (_st, [_H, _p, _u64, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
+    "pa_seed_from_paper_eq1": (_st, [_p, _p, _u64, _u64, _p]),
     "pa_xor_fold": (_st, [_p, _p, _u64, ctypes.c_uint32, _u64, _p]),
     "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
                               ctypes.POINTER(ctypes.c_uint32)]),
@@ -208,3 +215,28 @@ def pa_xor_fold(dst_ptr: int, src_ptr: int, words: int, count: int, src_stride_w
 def pa_hash_blocked(n: int, m: int, seed_ptr: int, key_ptr: int, out_ptr: int, max_block_bits: int = 0,
                     stream: int = 0) -> None:
     _check(_lib.pa_hash_blocked(n, m, seed_ptr, key_ptr, out_ptr, max_block_bits, stream))
+
+
+def pa_workspace_size(n: int, m: int, opt: pa_options | None = None) -> int:
+    """Host-only: exact device bytes pa_create_ws needs for (n, m, opt)."""
+    b = _u64()
+    _check(_lib.pa_workspace_size(n, m, ctypes.byref(opt) if opt is not None else None, ctypes.byref(b)))
+    return int(b.value)
+
+
+def pa_create_ws(n: int, m: int, seed_ptr: int, opt: pa_options | None, workspace_ptr: int,
+                 workspace_bytes: int, stream: int = 0) -> int:
+    h = _H()
+    _check(_lib.pa_create_ws(ctypes.byref(h), n, m, seed_ptr, ctypes.byref(opt) if opt is not None else None,
+                             workspace_ptr, workspace_bytes, stream))
+    return h.value
+
+
+def pa_hash_fresh_batch(h: int, seeds_ptr: int, seed_stride_words: int, keys_ptr: int, key_stride_words: int,
+                        outs_ptr: int, out_stride_words: int, count: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash_fresh_batch(h, seeds_ptr, seed_stride_words, keys_ptr, key_stride_words, outs_ptr,
+                                    out_stride_words, count, stream))
+
+
+def pa_seed_from_paper_eq1(s_ptr: int, t_ptr: int, n: int, m: int, stream: int = 0) -> None:
+    _check(_lib.pa_seed_from_paper_eq1(s_ptr, t_ptr, n, m, stream))

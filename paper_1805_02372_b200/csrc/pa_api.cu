@@ -7,6 +7,7 @@
 
 #include <new>
 #include <string>
+#include <vector>
 
 #include "pa_internal.h"
 
@@ -69,6 +70,39 @@ static pa_status check_dev_ptr(const void *p, const char *name, int device)
     return PA_OK;
 }
 
+pa_status dev_alloc(pa_ctx *h, void **p, size_t bytes, const char *what)
+{
+    *p = nullptr;
+    bytes = al256(bytes);
+    if (h->arena) {
+        Arena &A = *h->arena;
+        if (A.used + bytes > A.size) {
+            set_error("%s: workspace too small (%llu bytes used + %llu needed > %llu; see "
+                      "pa_workspace_size)", what, (unsigned long long)A.used, (unsigned long long)bytes,
+                      (unsigned long long)A.size);
+            return PA_ERR_NOMEM;
+        }
+        *p = A.base + A.used;
+        A.used += bytes;
+    } else {
+        cudaError_t e = cudaMalloc(p, bytes);
+        if (e != cudaSuccess) {
+            *p = nullptr;
+            cudaGetLastError();
+            set_error("%s: cudaMalloc of %llu bytes failed: %s", what, (unsigned long long)bytes,
+                      cudaGetErrorString(e));
+            return PA_ERR_NOMEM;
+        }
+    }
+    h->ws_bytes += bytes;
+    return PA_OK;
+}
+
+void dev_free(pa_ctx *h, void *p)
+{
+    if (p && !h->arena) cudaFree(p);
+}
+
 static cudaEvent_t prof_event(Profiler &P)
 {
     if (P.npool > 0) return P.pool[--P.npool];
@@ -77,9 +111,10 @@ static cudaEvent_t prof_event(Profiler &P)
     return e;
 }
 
+// column-block sub-handles report into their parent's profiler
 void prof_begin(pa_ctx *h, int k, cudaStream_t s)
 {
-    Profiler &P = h->prof;
+    Profiler &P = (h->parent ? h->parent : h)->prof;
     if (!P.on) return;
     if (P.npend == P.cap) {
         int nc = P.cap ? 2 * P.cap : 64;
@@ -97,7 +132,7 @@ void prof_begin(pa_ctx *h, int k, cudaStream_t s)
 
 void prof_end(pa_ctx *h, cudaStream_t s)
 {
-    Profiler &P = h->prof;
+    Profiler &P = (h->parent ? h->parent : h)->prof;
     if (!P.on || P.npend == 0 || P.pend[P.npend - 1].e1) return;
     Profiler::Pending &q = P.pend[P.npend - 1];
     q.e1 = prof_event(P);
@@ -169,24 +204,147 @@ pa_status pa_options_init(pa_options *opt)
     return PA_OK;
 }
 
+static void destroy_ctx(pa_ctx *h)
+{
+    for (uint32_t g = 0; g < h->nsub; ++g)
+        if (h->sub[g]) destroy_ctx(h->sub[g]);
+    delete[] h->sub;
+    delete[] h->sub_c0;
+    prof_free(h->prof);
+    drop_host_graph(h);
+    ra_destroy(h);
+    rb_destroy(h);
+    dev_free(h, h->stage_blk);
+    if (h->own_arena) delete h->arena;
+    delete h;
+}
+
 void pa_destroy(pa_handle h)
 {
     if (!h) return;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(h->device);
-    prof_free(h->prof);
-    drop_host_graph(h);
-    ra_destroy(h);
-    rb_destroy(h);
-    if (h->stage_key) cudaFree(h->stage_key);
-    if (h->stage_out) cudaFree(h->stage_out);
+    destroy_ctx(h);
     cudaSetDevice(prev);
-    delete h;
 }
 
-pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *seed_bits,
-                       const pa_options *opt, void *stream)
+// Validate and complete the caller's options.
+static pa_status parse_options(const pa_options *opt, uint64_t n, uint64_t m, pa_options *o)
+{
+    pa_options_init(o);
+    if (opt) {
+        if (opt->struct_size != sizeof(pa_options)) {
+            set_error("opt->struct_size = %u, expected %u (call pa_options_init)", opt->struct_size,
+                      (unsigned)sizeof(pa_options));
+            return PA_ERR_INVALID_ARG;
+        }
+        *o = *opt;
+    }
+    if (n == 0 || m == 0 || (m > n && !o->allow_wide)) {
+        set_error("need 1 <= m <= n (or opt->allow_wide), got n = %llu, m = %llu", (unsigned long long)n,
+                  (unsigned long long)m);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (n > (1ull << 40) || m > (1ull << 40)) {
+        set_error("n = %llu, m = %llu: lengths beyond 2^40 bits are unsupported", (unsigned long long)n,
+                  (unsigned long long)m);
+        return PA_ERR_UNSUPPORTED;
+    }
+    if (o->route < PA_ROUTE_AUTO || o->route > PA_ROUTE_BITPACKED) {
+        set_error("opt->route = %d is not a pa_route", o->route);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (o->allow_wide > 1) {
+        set_error("opt->allow_wide = %u must be 0 or 1", o->allow_wide);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (o->batch_keys > 4096) {
+        set_error("opt->batch_keys = %u exceeds 4096", o->batch_keys);
+        return PA_ERR_INVALID_ARG;
+    }
+    for (int i = 0; i < 3; ++i)
+        if (o->reserved[i]) {
+            set_error("opt->reserved[%d] = %u must be 0", i, o->reserved[i]);
+            return PA_ERR_INVALID_ARG;
+        }
+    if (o->route == PA_ROUTE_AUTO) o->route = choose_route(n, m);
+    return PA_OK;
+}
+
+static bool plan_fits(uint64_t n, uint64_t m, uint64_t maxlen)  // route (a) can plan within the cap
+{
+    Geometry g;
+    char err[256];
+    return ra_plan(n, m, &g, err, sizeof err, maxlen) == PA_OK;
+}
+
+// Eq. (4) column blocks for a transform-length cap: equal blocks of nb key
+// bits (a multiple of 128, so every block's key pointer stays 16-byte aligned) and a
+// shorter last one.  c0 receives the block starts; one entry = no split.
+static pa_status split_plan(uint64_t n, uint64_t m, uint64_t maxlen, std::vector<uint64_t> *c0)
+{
+    c0->assign(1, 0);
+    if (!maxlen || plan_fits(n, m, maxlen)) return PA_OK;
+    if (maxlen + 1 < m + 128) {
+        set_error("max_transform_len = %llu cannot hold even a 128-bit key block with m = %llu "
+                  "(needs >= %llu)", (unsigned long long)maxlen, (unsigned long long)m,
+                  (unsigned long long)(m + 127));
+        return PA_ERR_UNSUPPORTED;
+    }
+    uint64_t nb = (maxlen + 1 - m) / 128 * 128;  // nb + m - 1 <= maxlen
+    if (nb >= n) nb = (n - 1) / 128 * 128;       // the whole key did not fit: split it anyway
+    while (nb >= 128) {
+        const uint64_t last = n - (n - 1) / nb * nb;
+        if (plan_fits(nb, m, maxlen) && plan_fits(last, m, maxlen)) break;
+        uint64_t step = (nb / 64 + 127) / 128 * 128;
+        nb = nb > step ? nb - step : 0;
+    }
+    if (nb < 128) {
+        set_error("max_transform_len = %llu: no 128-bit-aligned key block plan fits (m = %llu)",
+                  (unsigned long long)maxlen, (unsigned long long)m);
+        return PA_ERR_UNSUPPORTED;
+    }
+    const uint64_t G = (n + nb - 1) / nb;
+    if (G > 65536) {
+        set_error("max_transform_len = %llu would cut the key into %llu blocks (> 65536)",
+                  (unsigned long long)maxlen, (unsigned long long)G);
+        return PA_ERR_UNSUPPORTED;
+    }
+    c0->clear();
+    for (uint64_t g = 0; g < G; ++g) c0->push_back(g * nb);
+    return PA_OK;
+}
+
+static size_t stage_bytes(uint64_t n, uint64_t m) { return al256((n + 31) / 32 * 4) + al256((m + 31) / 32 * 4); }
+
+// Exact device bytes a handle takes for (n, m, o) -- the sum of its dev_alloc calls.
+static pa_status handle_bytes(uint64_t n, uint64_t m, const pa_options &o, bool arena, size_t *bytes)
+{
+    *bytes = arena ? stage_bytes(n, m) : 0;  // without a workspace staging is allocated lazily
+    if (o.route == PA_ROUTE_BITPACKED) {
+        *bytes += rb_bytes(n, m);
+        return PA_OK;
+    }
+    std::vector<uint64_t> c0;
+    pa_status st = split_plan(n, m, o.max_transform_len, &c0);
+    if (st != PA_OK) return st;
+    const uint32_t cap = arena && o.batch_keys ? o.batch_keys : 1;
+    for (size_t g = 0; g < c0.size(); ++g) {
+        const uint64_t ng = (g + 1 < c0.size() ? c0[g + 1] : n) - c0[g];
+        Geometry geo;
+        char err[256];
+        if ((st = ra_plan(ng, m, &geo, err, sizeof err, o.max_transform_len)) != PA_OK) {
+            set_error("%s", err);
+            return st;
+        }
+        *bytes += ra_persist_bytes(geo) + ra_work_bytes(geo, cap);
+    }
+    return PA_OK;
+}
+
+static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *seed_bits,
+                             const pa_options *opt, void *workspace, uint64_t workspace_bytes, void *stream)
 {
     if (!out) {
         set_error("h (output handle pointer) is NULL");
@@ -194,43 +352,21 @@ pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *s
     }
     *out = nullptr;
     pa_options o;
-    pa_options_init(&o);
-    if (opt) {
-        if (opt->struct_size != sizeof(pa_options)) {
-            set_error("opt->struct_size = %u, expected %u (call pa_options_init)",
-                      opt->struct_size, (unsigned)sizeof(pa_options));
-            return PA_ERR_INVALID_ARG;
-        }
-        o = *opt;
-    }
-    if (n == 0 || m == 0 || (m > n && !o.allow_wide)) {
-        set_error("need 1 <= m <= n (or opt->allow_wide), got n = %llu, m = %llu",
-                  (unsigned long long)n, (unsigned long long)m);
-        return PA_ERR_INVALID_ARG;
-    }
-    if (n > (1ull << 40) || m > (1ull << 40)) {
-        set_error("n = %llu, m = %llu: lengths beyond 2^40 bits are unsupported",
-                  (unsigned long long)n, (unsigned long long)m);
-        return PA_ERR_UNSUPPORTED;
-    }
-    if (o.route < PA_ROUTE_AUTO || o.route > PA_ROUTE_BITPACKED) {
-        set_error("opt->route = %d is not a pa_route", o.route);
-        return PA_ERR_INVALID_ARG;
-    }
-    if (o.allow_wide > 1) {
-        set_error("opt->allow_wide = %u must be 0 or 1", o.allow_wide);
-        return PA_ERR_INVALID_ARG;
-    }
-    for (int i = 0; i < 7; ++i)
-        if (o.reserved[i]) {
-            set_error("opt->reserved[%d] = %u must be 0", i, o.reserved[i]);
-            return PA_ERR_INVALID_ARG;
-        }
+    pa_status st = parse_options(opt, n, m, &o);
+    if (st != PA_OK) return st;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    pa_status st = check_dev_ptr(seed_bits, "seed_bits", dev);
-    if (st != PA_OK) return st;
+    if ((st = check_dev_ptr(seed_bits, "seed_bits", dev)) != PA_OK) return st;
+    if (workspace) {
+        if ((st = check_dev_ptr(workspace, "workspace", dev)) != PA_OK) return st;
+        if ((uintptr_t)workspace & 255) {
+            set_error("workspace = %p is not 256-byte aligned", workspace);
+            return PA_ERR_INVALID_ARG;
+        }
+    }
+    std::vector<uint64_t> c0;
+    if (o.route == PA_ROUTE_TRANSFORM && (st = split_plan(n, m, o.max_transform_len, &c0)) != PA_OK) return st;
 
     pa_ctx *h = new (std::nothrow) pa_ctx();
     if (!h) {
@@ -242,9 +378,61 @@ pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *s
     h->m = m;
     h->L = n + m - 1;
     h->off = o.seed_bit_offset;
-    h->route = o.route == PA_ROUTE_AUTO ? choose_route(n, m) : o.route;
+    h->route = o.route;
+    h->batch_opt = o.batch_keys;
+    h->max_len = o.route == PA_ROUTE_TRANSFORM ? o.max_transform_len : 0;
+    if (workspace) {
+        h->arena = new (std::nothrow) Arena();
+        if (!h->arena) {
+            delete h;
+            set_error("host allocation of the handle failed");
+            return PA_ERR_NOMEM;
+        }
+        h->own_arena = true;
+        h->arena->base = (char *)workspace;
+        h->arena->size = workspace_bytes;
+        // staging for pa_hash_host comes out of the workspace up front
+        if ((st = dev_alloc(h, (void **)&h->stage_blk, stage_bytes(n, m), "pa_hash_host staging")) == PA_OK) {
+            h->stage_key = (uint32_t *)h->stage_blk;
+            h->stage_out = (uint32_t *)(h->stage_blk + al256((n + 31) / 32 * 4));
+        }
+    }
     cudaStream_t s = (cudaStream_t)stream;
-    st = h->route == PA_ROUTE_TRANSFORM ? ra_create(h, seed_bits, s) : rb_create(h, seed_bits, s);
+    if (st == PA_OK && c0.size() > 1) {
+        // Eq. (4) split: block g = key bits [c0, c0 + ng), seed window offset n - ng - c0
+        h->nsub = (uint32_t)c0.size();
+        h->sub = new (std::nothrow) pa_ctx *[h->nsub]();
+        h->sub_c0 = new (std::nothrow) uint64_t[h->nsub];
+        if (!h->sub || !h->sub_c0) {
+            set_error("host allocation of %u block handles failed", h->nsub);
+            st = PA_ERR_NOMEM;
+        }
+        for (uint32_t g = 0; st == PA_OK && g < h->nsub; ++g) {
+            const uint64_t ng = (g + 1 < h->nsub ? c0[g + 1] : n) - c0[g];
+            pa_ctx *b = new (std::nothrow) pa_ctx();
+            if (!b) {
+                set_error("host allocation of block handle %u failed", g);
+                st = PA_ERR_NOMEM;
+                break;
+            }
+            h->sub[g] = b;
+            h->sub_c0[g] = c0[g];
+            b->parent = h;
+            b->arena = h->arena;
+            b->device = dev;
+            b->n = ng;
+            b->m = m;
+            b->L = ng + m - 1;
+            b->off = h->off + (n - ng - c0[g]);
+            b->route = PA_ROUTE_TRANSFORM;
+            b->batch_opt = h->batch_opt;
+            b->max_len = h->max_len;
+            st = ra_create(b, seed_bits, s);
+            h->kernels_per_hash += b->kernels_per_hash;
+        }
+    } else if (st == PA_OK) {
+        st = h->route == PA_ROUTE_TRANSFORM ? ra_create(h, seed_bits, s) : rb_create(h, seed_bits, s);
+    }
     if (st != PA_OK) {
         std::string keep = g_err;
         pa_destroy(h);
@@ -253,6 +441,39 @@ pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *s
     }
     *out = h;
     return PA_OK;
+}
+
+pa_status pa_create_ex(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *seed_bits,
+                       const pa_options *opt, void *stream)
+{
+    return create_impl(out, n, m, seed_bits, opt, nullptr, 0, stream);
+}
+
+pa_status pa_workspace_size(uint64_t n, uint64_t m, const pa_options *opt, uint64_t *bytes)
+{
+    if (!bytes) {
+        set_error("pa_workspace_size: bytes is NULL");
+        return PA_ERR_INVALID_ARG;
+    }
+    *bytes = 0;
+    pa_options o;
+    pa_status st = parse_options(opt, n, m, &o);
+    if (st != PA_OK) return st;
+    size_t b = 0;
+    if ((st = handle_bytes(n, m, o, true, &b)) != PA_OK) return st;
+    *bytes = b;
+    return PA_OK;
+}
+
+pa_status pa_create_ws(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits, const pa_options *opt,
+                       void *workspace, uint64_t workspace_bytes, void *stream)
+{
+    if (!workspace) {
+        if (h) *h = nullptr;
+        set_error("pa_create_ws: workspace is NULL (use pa_create_ex for library-owned memory)");
+        return PA_ERR_INVALID_ARG;
+    }
+    return create_impl(h, n, m, seed_bits, opt, workspace, workspace_bytes, stream);
 }
 
 pa_status pa_create(pa_handle *h, uint64_t n, uint64_t m, const uint32_t *seed_bits, void *stream)
@@ -266,6 +487,18 @@ pa_status pa_create_u64(pa_handle *h, uint64_t n, uint64_t m, const uint64_t *se
     return pa_create_ex(h, n, m, (const uint32_t *)seed_bits, nullptr, stream);
 }
 
+static pa_status seed_impl(pa_ctx *h, const uint32_t *seed_bits, cudaStream_t s)
+{
+    if (h->nsub) {
+        for (uint32_t g = 0; g < h->nsub; ++g) {
+            pa_status st = ra_seed(h->sub[g], seed_bits, s);
+            if (st != PA_OK) return st;
+        }
+        return PA_OK;
+    }
+    return h->route == PA_ROUTE_TRANSFORM ? ra_seed(h, seed_bits, s) : rb_seed(h, seed_bits, s);
+}
+
 pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream)
 {
     if (!h) {
@@ -274,8 +507,51 @@ pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream)
     }
     pa_status st = check_dev_ptr(seed_bits, "seed_bits", h->device);
     if (st != PA_OK) return st;
-    return h->route == PA_ROUTE_TRANSFORM ? ra_seed(h, seed_bits, (cudaStream_t)stream)
-                                          : rb_seed(h, seed_bits, (cudaStream_t)stream);
+    return seed_impl(h, seed_bits, (cudaStream_t)stream);
+}
+
+// Keys [0, count) of a batch; the column blocks of a split handle XOR into the
+// outputs the first block zeroed (Eq. (7)).
+static pa_status batch_impl(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
+                            uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s)
+{
+    if (h->nsub) {
+        for (uint32_t g = 0; g < h->nsub; ++g) {
+            pa_status st = batch_impl(h->sub[g], keys + h->sub_c0[g] / 32, key_stride, outs, out_stride, count,
+                                      g ? 0 : zero_words, s);
+            if (st != PA_OK) return st;
+        }
+        return PA_OK;
+    }
+    if (h->route != PA_ROUTE_TRANSFORM) {
+        for (uint32_t k = 0; k < count; ++k) {
+            pa_status st = rb_hash(h, keys + k * key_stride, outs + k * out_stride, zero_words, s);
+            if (st != PA_OK) return st;
+        }
+        return PA_OK;
+    }
+    // keys in chunks: all kernels take the key index from the grid
+    const uint32_t chunk = ra_batch_keys(h);
+    for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
+        const uint32_t c = count - k0 < chunk ? count - k0 : chunk;
+        pa_status st = ra_hash_batch(h, keys + k0 * key_stride, key_stride, outs + k0 * out_stride, out_stride, c,
+                                     zero_words, s);
+        if (st != PA_OK) return st;
+    }
+    return PA_OK;
+}
+
+// would a batch of `count` keys grow (reallocate) some work buffer?
+static bool batch_grows(const pa_ctx *h, uint32_t count)
+{
+    if (h->nsub) {
+        for (uint32_t g = 0; g < h->nsub; ++g)
+            if (batch_grows(h->sub[g], count)) return true;
+        return false;
+    }
+    if (h->route != PA_ROUTE_TRANSFORM || h->arena) return false;
+    const uint32_t chunk = ra_batch_keys(h);
+    return h->a.cap < (count < chunk ? count : chunk);
 }
 
 static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
@@ -296,6 +572,7 @@ static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint
             h->ok_out = out;
         }
     }
+    if (h->nsub) return batch_impl(h, key, 0, out, 0, 1, zero_words, s);
     return h->route == PA_ROUTE_TRANSFORM ? ra_hash(h, key, out, zero_words, s)
                                           : rb_hash(h, key, out, zero_words, s);
 }
@@ -319,6 +596,21 @@ pa_status pa_hash_u64(pa_handle h, const uint64_t *key_bits, uint64_t *out_bits,
                      (cudaStream_t)stream, true);
 }
 
+static pa_status check_strides(pa_handle h, uint64_t key_stride_words, uint64_t out_stride_words)
+{
+    if (key_stride_words < (h->n + 31) / 32 || out_stride_words < (h->m + 31) / 32) {
+        set_error("key_stride_words = %llu (need >= %llu), out_stride_words = %llu (need >= %llu)",
+                  (unsigned long long)key_stride_words, (unsigned long long)((h->n + 31) / 32),
+                  (unsigned long long)out_stride_words, (unsigned long long)((h->m + 31) / 32));
+        return PA_ERR_INVALID_ARG;
+    }
+    if ((key_stride_words & 3) || (out_stride_words & 3)) {
+        set_error("strides must keep every key/output 16-byte aligned (multiples of 4 words)");
+        return PA_ERR_INVALID_ARG;
+    }
+    return PA_OK;
+}
+
 pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_words,
                         uint32_t *outs, uint64_t out_stride_words, uint32_t count, void *stream)
 {
@@ -326,37 +618,42 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
         set_error("handle is NULL");
         return PA_ERR_INVALID_ARG;
     }
-    if (key_stride_words < (h->n + 31) / 32 || out_stride_words < (h->m + 31) / 32) {
-        set_error("key_stride_words = %llu (need >= %llu), out_stride_words = %llu (need >= %llu)",
-                  (unsigned long long)key_stride_words, (unsigned long long)((h->n + 31) / 32),
-                  (unsigned long long)out_stride_words, (unsigned long long)((h->m + 31) / 32));
-        return PA_ERR_INVALID_ARG;
-    }
+    pa_status st;
+    if ((st = check_strides(h, key_stride_words, out_stride_words)) != PA_OK) return st;
     if (count == 0) return PA_OK;
-    if ((key_stride_words & 3) || (out_stride_words & 3)) {
-        set_error("strides must keep every key/output 16-byte aligned (multiples of 4 words)");
+    if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
+    if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
+    // growing the work buffers reallocates them: a captured pa_hash_host graph must go
+    if (count > 1 && batch_grows(h, count)) drop_host_graph(h);
+    return batch_impl(h, keys, key_stride_words, outs, out_stride_words, count, (h->m + 31) / 32,
+                      (cudaStream_t)stream);
+}
+
+pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_stride_words,
+                              const uint32_t *keys, uint64_t key_stride_words, uint32_t *outs,
+                              uint64_t out_stride_words, uint32_t count, void *stream)
+{
+    if (!h) {
+        set_error("handle is NULL");
         return PA_ERR_INVALID_ARG;
     }
     pa_status st;
+    if ((st = check_strides(h, key_stride_words, out_stride_words)) != PA_OK) return st;
+    if (seed_stride_words < (h->off + h->L + 31) / 32 || (seed_stride_words & 3)) {
+        set_error("seed_stride_words = %llu: need >= %llu and a multiple of 4", (unsigned long long)seed_stride_words,
+                  (unsigned long long)((h->off + h->L + 31) / 32));
+        return PA_ERR_INVALID_ARG;
+    }
+    if (count == 0) return PA_OK;
+    if ((st = check_dev_ptr(seeds, "seeds", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
-    if (h->route == PA_ROUTE_TRANSFORM) {
-        // keys in chunks: all kernels take the key index from the grid.  Growing the
-        // work buffers reallocates them: a captured pa_hash_host graph must go.
-        if (count > 1 && h->a.cap < (count < ra_batch_keys(h) ? count : ra_batch_keys(h))) drop_host_graph(h);
-        const uint32_t chunk = ra_batch_keys(h);
-        for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
-            const uint32_t c = count - k0 < chunk ? count - k0 : chunk;
-            st = ra_hash_batch(h, keys + k0 * key_stride_words, key_stride_words, outs + k0 * out_stride_words,
-                               out_stride_words, c, (h->m + 31) / 32, (cudaStream_t)stream);
-            if (st != PA_OK) return st;
-        }
-        return PA_OK;
-    }
+    cudaStream_t s = (cudaStream_t)stream;
     for (uint32_t k = 0; k < count; ++k) {
-        st = hash_impl(h, keys + k * key_stride_words, outs + k * out_stride_words,
-                       (h->m + 31) / 32, (cudaStream_t)stream, false);
-        if (st != PA_OK) return st;
+        if ((st = seed_impl(h, seeds + k * seed_stride_words, s)) != PA_OK) return st;
+        if ((st = hash_impl(h, keys + k * key_stride_words, outs + k * out_stride_words, (h->m + 31) / 32, s,
+                            false)) != PA_OK)
+            return st;
     }
     return PA_OK;
 }
@@ -436,16 +733,11 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
     cudaStream_t s = (cudaStream_t)stream;
     size_t kb = ((h->n + 31) / 32) * 4, ob = ((h->m + 31) / 32) * 4;
     cudaError_t e;
-    if (!h->stage_key) {
-        if ((e = cudaMalloc(&h->stage_key, kb)) != cudaSuccess) {
-            h->stage_key = nullptr;
-            return cuda_fail(e, "pa_hash_host staging alloc");
-        }
-        if ((e = cudaMalloc(&h->stage_out, ob)) != cudaSuccess) {
-            h->stage_out = nullptr;
-            return cuda_fail(e, "pa_hash_host staging alloc");
-        }
-        h->ws_bytes += kb + ob;
+    if (!h->stage_blk) {  // library-owned memory: staging on first use
+        pa_status st = dev_alloc(h, (void **)&h->stage_blk, stage_bytes(h->n, h->m), "pa_hash_host staging");
+        if (st != PA_OK) return st;
+        h->stage_key = (uint32_t *)h->stage_blk;
+        h->stage_out = (uint32_t *)(h->stage_blk + al256(kb));
     }
     if (h->prof.on) {  // per-launch profiling events need the plain launches
         if ((e = cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -496,14 +788,20 @@ pa_status pa_residual(pa_handle h, double *max_residual, void *stream)
     *max_residual = 0.0;
     if (h->route != PA_ROUTE_TRANSFORM) return PA_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    unsigned long long bits = 0;
-    cudaError_t e;
-    if ((e = cudaMemcpyAsync(&bits, h->a.resid, sizeof bits, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-        (e = cudaStreamSynchronize(s)) != cudaSuccess ||
-        (e = cudaMemsetAsync(h->a.resid, 0, sizeof bits, s)) != cudaSuccess)
-        return cuda_fail(e, "pa_residual");
-    double r;
-    memcpy(&r, &bits, sizeof r);
+    double r = 0.0;
+    const uint32_t nb = h->nsub ? h->nsub : 1;
+    for (uint32_t g = 0; g < nb; ++g) {  // max over the column blocks of a split handle
+        pa_ctx *b = h->nsub ? h->sub[g] : h;
+        unsigned long long bits = 0;
+        cudaError_t e;
+        if ((e = cudaMemcpyAsync(&bits, b->a.resid, sizeof bits, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(s)) != cudaSuccess ||
+            (e = cudaMemsetAsync(b->a.resid, 0, sizeof bits, s)) != cudaSuccess)
+            return cuda_fail(e, "pa_residual");
+        double rb;
+        memcpy(&rb, &bits, sizeof rb);
+        if (rb > r) r = rb;
+    }
     *max_residual = r;
     if (r > PA_RESIDUAL_LIMIT) {
         set_error("FP64 residual %.3e exceeds PA_RESIDUAL_LIMIT %.2f", r, PA_RESIDUAL_LIMIT);
@@ -573,8 +871,9 @@ pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
     info->route = choose_route(n, m);
     info->device = -1;
     if (info->route == PA_ROUTE_BITPACKED) {
-        info->workspace_bytes = 4 * ((m + 31) / 32 + (n + 31) / 32 + 4);
+        info->workspace_bytes = rb_bytes(n, m);
         info->kernels_per_hash = 1;
+        info->column_blocks = 1;
         return PA_OK;
     }
     Geometry g;
@@ -588,8 +887,9 @@ pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
     info->n1 = g.N1;
     info->n2 = g.N2;
     info->cols_per_cta = g.C;
-    info->workspace_bytes = 32 * g.M + (uint64_t)(g.N1 / g.C) * g.kbw * 4;
+    info->workspace_bytes = ra_persist_bytes(g) + ra_work_bytes(g, 1);
     info->kernels_per_hash = 4;
+    info->column_blocks = 1;
     return PA_OK;
 }
 
@@ -604,13 +904,17 @@ pa_status pa_get_info(pa_handle h, pa_info *info)
     info->m = h->m;
     info->route = h->route;
     info->device = h->device;
-    if (h->route == PA_ROUTE_TRANSFORM) {
-        info->transform_len = 2 * h->a.g.M;
-        info->n1 = h->a.g.N1;
-        info->n2 = h->a.g.N2;
-        info->cols_per_cta = h->a.g.C;
-    }
+    info->column_blocks = h->nsub ? h->nsub : 1;
     info->workspace_bytes = h->ws_bytes;
+    for (uint32_t g = 0; g < h->nsub; ++g) info->workspace_bytes += h->sub[g]->ws_bytes;
+    // geometry: the handle's own, or its first (largest) column block's
+    const pa_ctx *b = h->nsub ? h->sub[0] : h;
+    if (h->route == PA_ROUTE_TRANSFORM) {
+        info->transform_len = 2 * b->a.g.M;
+        info->n1 = b->a.g.N1;
+        info->n2 = b->a.g.N2;
+        info->cols_per_cta = b->a.g.C;
+    }
     info->kernels_per_hash = h->kernels_per_hash;
     return PA_OK;
 }

@@ -33,6 +33,8 @@ struct RouteTables {
 
 struct RouteA {
     Geometry g;
+    char *pblk = nullptr;      // persistent block: spec, tables, rev2, resid
+    char *wblk = nullptr;      // work block: buf, kb for `cap` keys
     double2 *buf = nullptr;    // [N2][N1] working array (also the seed's scratch)
     double2 *spec = nullptr;   // [N2][N1] seed spectrum / M, in K2's position order
     double2 *tables = nullptr; // backing store of T's double2 tables
@@ -51,6 +53,14 @@ struct RouteB {
 }  // namespace pa
 
 namespace pa {
+// Caller-owned device memory (pa_create_ws): a bump allocator shared by a handle
+// and its column-block sub-handles.  Without one, libpa cudaMallocs.
+struct Arena {
+    char *base = nullptr;
+    size_t size = 0, used = 0;
+};
+inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
 // launch-bracketing CUDA events for pa_profile_* (kernel k = index into names)
 struct Profiler {
     bool on = false;
@@ -78,8 +88,19 @@ struct pa_ctx {
     // pointer-validation cache (pa_hash called repeatedly with the same buffers)
     const void *ok_key = nullptr, *ok_out = nullptr;
     pa::Profiler prof;
-    // staging for pa_hash_host
+    // staging for pa_hash_host (one block: key words, then output words)
+    char *stage_blk = nullptr;
     uint32_t *stage_key = nullptr, *stage_out = nullptr;
+    // device memory: the caller's workspace (nullptr: cudaMalloc)
+    pa::Arena *arena = nullptr;
+    bool own_arena = false;
+    uint32_t batch_opt = 0;  // pa_options.batch_keys
+    // Eq. (4) column split (pa_options.max_transform_len): one sub-handle per key block
+    pa_ctx *parent = nullptr;
+    pa_ctx **sub = nullptr;
+    uint64_t *sub_c0 = nullptr;  // first key bit of each block (multiple of 128)
+    uint32_t nsub = 0;
+    uint64_t max_len = 0;        // pa_options.max_transform_len (route (a) planning cap)
     // pa_hash_host as one CUDA graph (H2D, kernels, D2H); host pointers patched per call
     cudaGraph_t host_graph = nullptr;
     cudaGraphExec_t host_exec = nullptr;
@@ -91,7 +112,8 @@ struct pa_ctx {
 namespace pa {
 
 // route (a)
-pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen);
+// max_len: cap on the real transform length 2 M (0 = none), pa_options.max_transform_len
+pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len = 0);
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
@@ -107,6 +129,14 @@ pa_status rb_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                   cudaStream_t s);
 void rb_destroy(pa_ctx *h);
+
+size_t ra_persist_bytes(const Geometry &g);
+size_t ra_work_bytes(const Geometry &g, uint32_t cap);
+size_t rb_bytes(uint64_t n, uint64_t m);
+
+// device memory from the handle's arena or cudaMalloc (dev_free is a no-op for arena memory)
+pa_status dev_alloc(pa_ctx *h, void **p, size_t bytes, const char *what);
+void dev_free(pa_ctx *h, void *p);
 
 void set_error(const char *fmt, ...);
 // bracket one kernel launch with profiling events (no-ops unless enabled)

@@ -253,7 +253,7 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     grid_dep_wait();  // K0's bit streams
-    if (zero_out) {  // K3 ORs this hash's output bits in
+    if (zero_out) {  // K3 XORs this hash's output bits in (zero_words = 0: accumulate)
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
              i += (uint64_t)gridDim.x * blockDim.x)
             zero_out[i] = 0u;
@@ -490,8 +490,10 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
                 }
                 const uint64_t wd = (uint64_t)i0 >> 5;
                 const int sh = (int)(i0 & 31);
-                atomicOr(out + wd, run << sh);
-                if (sh && (run >> (32 - sh))) atomicOr(out + wd + 1, run >> (32 - sh));
+                // XOR: each output bit is produced once per hash, so on the zeroed output this
+                // equals OR; column blocks of the Eq. (4) split accumulate Eq. (7) in place
+                atomicXor(out + wd, run << sh);
+                if (sh && (run >> (32 - sh))) atomicXor(out + wd + 1, run >> (32 - sh));
             }
         }
     }
@@ -568,7 +570,7 @@ static uint32_t smem_k13(uint32_t N2, uint32_t C, uint32_t nhi2)
 }
 static uint32_t smem_k2(uint32_t N1, uint32_t nhi1) { return tile_bytes(N1) + 2 * (64 + nhi1) * 16; }
 
-pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
+pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len)
 {
     const uint64_t L = n + m - 1;
     const uint64_t Mmin = (L + 1) / 2;
@@ -591,6 +593,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
         auto it0 = std::lower_bound(sm.begin(), sm.end(), (uint32_t)need);
         for (auto it = it0; it != sm.end() && *it <= need * 1.12 + 16; ++it) {
         const uint32_t N2 = *it;
+        if (max_len && 2ull * N1 * N2 > max_len) continue;
         FftPlan p1, p2;
         if (!make_plan(N1, &p1) || !make_plan(N2, &p2)) continue;
         for (uint32_t C = 16; C >= 1; C >>= 1) {
@@ -638,8 +641,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
     if (!found) {
         snprintf(err, errlen,
                  "route (a): n+m-1 = %llu needs a complex transform of length >= %llu, beyond the "
-                 "two-pass plan's limit",
-                 (unsigned long long)L, (unsigned long long)Mmin);
+                 "two-pass plan's limit%s",
+                 (unsigned long long)L, (unsigned long long)Mmin,
+                 max_len ? " or pa_options.max_transform_len" : "");
         return PA_ERR_UNSUPPORTED;
     }
     uint32_t logC = 0;
@@ -660,38 +664,52 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen)
     return PA_OK;
 }
 
-static pa_status alloc(void **p, size_t bytes, pa_ctx *h, const char *what)
+static size_t ntables(const Geometry &g) { return 64 + g.f1.nhi + 2 * (64 + g.f2.nhi); }
+static size_t kb_bytes(const Geometry &g) { return (size_t)(g.N1 / g.C) * g.kbw * 4; }
+
+// Persistent block: spec [M] | tables | rev2 [N2] | resid.  Work block: buf [cap][M] |
+// kb [cap][...].  Both 256-byte carved, so pa_workspace_size can add them up exactly.
+size_t ra_persist_bytes(const Geometry &g)
 {
-    cudaError_t e = cudaMalloc(p, bytes);
-    if (e != cudaSuccess) {
-        *p = nullptr;
-        set_error("route (a): cudaMalloc(%s, %llu bytes) failed: %s", what,
-                  (unsigned long long)bytes, cudaGetErrorString(e));
-        return PA_ERR_NOMEM;
-    }
-    h->ws_bytes += bytes;
-    return PA_OK;
+    return al256(g.M * sizeof(double2)) + al256(ntables(g) * sizeof(double2)) + al256(g.N2 * 4u) + al256(8);
+}
+size_t ra_work_bytes(const Geometry &g, uint32_t cap)
+{
+    return al256((size_t)cap * g.M * sizeof(double2)) + al256((size_t)cap * kb_bytes(g));
+}
+
+static void carve_work(RouteA &a, char *blk, uint32_t cap)
+{
+    a.wblk = blk;
+    a.buf = reinterpret_cast<double2 *>(blk);
+    a.kb = reinterpret_cast<uint32_t *>(blk + al256((size_t)cap * a.g.M * sizeof(double2)));
+    a.cap = cap;
 }
 
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 {
     char err[256];
     Geometry &g = h->a.g;
-    pa_status st = ra_plan(h->n, h->m, &g, err, sizeof err);
+    pa_status st = ra_plan(h->n, h->m, &g, err, sizeof err, h->max_len);
     if (st != PA_OK) {
         set_error("%s", err);
         return st;
     }
     RouteA &a = h->a;
     RouteTables &T = a.T;
-    if ((st = alloc((void **)&a.buf, g.M * sizeof(double2), h, "buf"))) return st;
-    if ((st = alloc((void **)&a.spec, g.M * sizeof(double2), h, "spec"))) return st;
-    size_t ntab = 64 + g.f1.nhi + 2 * (64 + g.f2.nhi);
-    if ((st = alloc((void **)&a.tables, ntab * sizeof(double2), h, "tables"))) return st;
-    if ((st = alloc((void **)&T.rev2, g.N2 * sizeof(uint32_t), h, "rev2"))) return st;
-    if ((st = alloc((void **)&a.resid, sizeof(unsigned long long), h, "resid"))) return st;
-    if ((st = alloc((void **)&a.kb, (size_t)(g.N1 / g.C) * g.kbw * 4, h, "kb"))) return st;
-    a.cap = 1;
+    char *pb = nullptr, *wb = nullptr;
+    const uint32_t cap = h->arena && h->batch_opt ? h->batch_opt : 1;
+    if ((st = dev_alloc(h, (void **)&pb, ra_persist_bytes(g), "route (a) spectrum + tables"))) return st;
+    a.pblk = pb;
+    if ((st = dev_alloc(h, (void **)&wb, ra_work_bytes(g, cap), "route (a) work buffers"))) return st;
+    carve_work(a, wb, cap);
+    a.spec = reinterpret_cast<double2 *>(pb);
+    pb += al256(g.M * sizeof(double2));
+    a.tables = reinterpret_cast<double2 *>(pb);
+    pb += al256(ntables(g) * sizeof(double2));
+    T.rev2 = reinterpret_cast<uint32_t *>(pb);
+    pb += al256(g.N2 * 4u);
+    a.resid = reinterpret_cast<unsigned long long *>(pb);
     double2 *p = a.tables;
     T.W1lo = p; p += 64;
     T.W1hi = p; p += g.f1.nhi;
@@ -751,37 +769,37 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 // Work buffers for `count` keys in flight (grown on demand, kept for the next call).
+// A caller workspace is never grown: pa_hash_batch chunks by its capacity.
 static pa_status ra_reserve(pa_ctx *h, uint32_t count)
 {
     RouteA &a = h->a;
     if (count <= a.cap) return PA_OK;
-    const Geometry &g = a.g;
-    const size_t kbk = (size_t)(g.N1 / g.C) * g.kbw * 4;
-    double2 *nb = nullptr;
-    uint32_t *nk = nullptr;
-    cudaError_t e = cudaMalloc(&nb, (size_t)count * g.M * sizeof(double2));
-    if (e == cudaSuccess) e = cudaMalloc(&nk, (size_t)count * kbk);
-    if (e != cudaSuccess) {
-        if (nb) cudaFree(nb);
-        cudaGetLastError();
-        set_error("route (a): cannot allocate work buffers for %u keys (%llu bytes): %s", count,
-                  (unsigned long long)((size_t)count * (g.M * sizeof(double2) + kbk)), cudaGetErrorString(e));
+    if (h->arena) {
+        set_error("route (a): %u keys in flight exceed the workspace's %u (pa_options.batch_keys)", count,
+                  a.cap);
         return PA_ERR_NOMEM;
     }
-    // the handle's own single-key buffers are freed when replaced (stream-ordered via sync)
-    cudaStreamSynchronize(0);
+    char *nb = nullptr;
+    const size_t bytes = ra_work_bytes(a.g, count);
+    cudaError_t e = cudaMalloc(&nb, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("route (a): cannot allocate work buffers for %u keys (%llu bytes): %s", count,
+                  (unsigned long long)bytes, cudaGetErrorString(e));
+        return PA_ERR_NOMEM;
+    }
+    // the old buffers may still be in use by enqueued work
     cudaDeviceSynchronize();
-    h->ws_bytes += (size_t)(count - a.cap) * (g.M * sizeof(double2) + kbk);
-    cudaFree(a.buf);
-    cudaFree(a.kb);
-    a.buf = nb;
-    a.kb = nk;
-    a.cap = count;
+    h->ws_bytes += bytes - ra_work_bytes(a.g, a.cap);
+    cudaFree(a.wblk);
+    carve_work(a, nb, count);
     return PA_OK;
 }
 
 uint32_t ra_batch_keys(const pa_ctx *h)
 {
+    if (h->arena) return h->a.cap;        // the workspace was sized for this many
+    if (h->batch_opt) return h->batch_opt;
     // keys per launch: enough CTAs to fill the GPU for small transforms, within 4 GiB
     const Geometry &g = h->a.g;
     const double per_key = (double)g.M * 16.0 + (double)(g.N1 / g.C) * g.kbw * 4;
@@ -836,9 +854,8 @@ extern "C" int pa_debug_trace(unsigned long long *out)
 void ra_destroy(pa_ctx *h)
 {
     RouteA &a = h->a;
-    void *ptrs[] = {a.buf, a.spec, a.tables, a.T.rev2, a.resid, a.kb};
-    for (void *p : ptrs)
-        if (p) cudaFree(p);
+    dev_free(h, a.pblk);
+    dev_free(h, a.wblk);
     a = RouteA{};
 }
 

@@ -83,18 +83,14 @@ k_toeplitz_bitpacked(const uint32_t *__restrict__ key, uint64_t n, uint64_t m,
 
 }  // namespace
 
+size_t rb_bytes(uint64_t n, uint64_t m) { return al256(((m + 31) / 32 + (n + 31) / 32 + 4) * 4); }
+
 pa_status rb_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 {
     uint64_t Q = (h->m + 31) / 32, KW = (h->n + 31) / 32;
     h->b.srw = Q + KW + 4;
-    cudaError_t e = cudaMalloc(&h->b.sr, h->b.srw * sizeof(uint32_t));
-    if (e != cudaSuccess) {
-        h->b.sr = nullptr;
-        set_error("route (b): cudaMalloc of %llu bytes failed: %s",
-                  (unsigned long long)(h->b.srw * 4), cudaGetErrorString(e));
-        return PA_ERR_NOMEM;
-    }
-    h->ws_bytes += h->b.srw * sizeof(uint32_t);
+    pa_status st = dev_alloc(h, (void **)&h->b.sr, rb_bytes(h->n, h->m), "route (b) reversed seed");
+    if (st != PA_OK) return st;
     h->kernels_per_hash = 1;
     return rb_seed(h, seed, s);
 }
@@ -137,7 +133,7 @@ pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
 
 void rb_destroy(pa_ctx *h)
 {
-    if (h->b.sr) cudaFree(h->b.sr);
+    dev_free(h, h->b.sr);
     h->b.sr = nullptr;
 }
 

@@ -4,6 +4,7 @@ work are exercised here."""
 import ctypes
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -54,12 +55,29 @@ def test_version_and_status_strings():
     assert pa.pa_status_string(5) == "PA_ERR_PRECISION"
 
 
-def test_struct_layouts_match_header():
+def _c_layout(tmp_path, struct, fields):
+    """sizeof / offsetof as the C compiler sees include/pa.h."""
+    src = tmp_path / f"{struct}.c"
+    body = "".join(f'    printf("%zu\\n", offsetof({struct}, {f}));\n' for f in fields)
+    src.write_text(f'#include <stddef.h>\n#include <stdio.h>\n#include "pa.h"\nint main(void) {{\n'
+                   f'    printf("%zu\\n", sizeof({struct}));\n{body}    return 0;\n}}\n')
+    exe = tmp_path / f"{struct}.out"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    return int(out[0]), [int(v) for v in out[1:]]
+
+
+@pytest.mark.parametrize("struct", ["pa_options", "pa_info", "pa_kernel_time"])
+def test_struct_layouts_match_header(tmp_path, struct):
     import paper_1805_02372_b200._lib as L
-    assert ctypes.sizeof(L.pa_options) == 4 + 4 + 8 + 4 + 28
-    assert ctypes.sizeof(L.pa_info) == 8 * 2 + 4 * 2 + 8 * 6
-    o = L.pa_options_init()
-    assert o.struct_size == ctypes.sizeof(L.pa_options) and o.route == 0
+    cls = getattr(L, struct)
+    names = [f for f, _ in cls._fields_]
+    size, offs = _c_layout(tmp_path, struct, names)
+    assert ctypes.sizeof(cls) == size
+    assert [getattr(cls, f).offset for f in names] == offs
+    if struct == "pa_options":
+        o = L.pa_options_init()
+        assert o.struct_size == size and o.route == 0 and o.batch_keys == 0 and o.max_transform_len == 0
 
 
 def test_invalid_lengths_rejected_before_device_work():
@@ -118,3 +136,50 @@ def test_planner_host_only():
             continue
         if p["route"] == pa.PA_ROUTE_TRANSFORM:
             assert p["transform_len"] >= n + m - 1
+
+
+def test_workspace_size_is_host_only_and_adds_up():
+    """pa_workspace_size needs no device: route (b) = reversed seed + staging; route (a) grows
+    with batch_keys by whole per-key work buffers; the Eq. (4) split sums its blocks."""
+    import paper_1805_02372_b200 as pa
+    al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    n, m = 4096, 1024
+    stage = al((n + 31) // 32 * 4) + al((m + 31) // 32 * 4)
+    assert pa.workspace_size(n, m, route="bitpacked") == al(((m + 31) // 32 + (n + 31) // 32 + 4) * 4) + stage
+    n, m = 1_000_003, 250_000
+    one = pa.workspace_size(n, m, route="transform")
+    four = pa.workspace_size(n, m, route="transform", batch_keys=4)
+    info = pa.pa_plan(n, m)
+    assert one >= 32 * (info["transform_len"] // 2)
+    assert four - one >= 3 * 16 * (info["transform_len"] // 2)
+    split = pa.workspace_size(n, m, route="transform", max_transform_len=600_000)
+    assert split > one  # two or more blocks, each with its own spectrum
+    # an unsplit handle whose default plan already fits is unchanged by the cap
+    assert pa.workspace_size(n, m, route="transform", max_transform_len=10**9) == one
+
+
+def test_option_and_pointer_errors_before_device_work():
+    import paper_1805_02372_b200 as pa
+    with pytest.raises(pa.PaError) as e:
+        pa.workspace_size(10_000, 5_000, route="transform", max_transform_len=5_000)
+    assert e.value.status == pa.PA_ERR_UNSUPPORTED and "max_transform_len" in pa.pa_last_error()
+    with pytest.raises(pa.PaError) as e:
+        pa.workspace_size(100, 10, batch_keys=5000)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "batch_keys" in pa.pa_last_error()
+    o = pa.make_options()
+    o.reserved[1] = 7
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_workspace_size(100, 10, o)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "reserved[1]" in pa.pa_last_error()
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_create_ws(100, 10, 0, None, 0, 1 << 20, 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "workspace" in pa.pa_last_error()
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_seed_from_paper_eq1(0, 0, 10, 5, 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG
+    with pytest.raises(pa.PaError) as e:  # overlap is rejected from the pointer values alone
+        pa.pa_seed_from_paper_eq1(1 << 20, (1 << 20) + 16, 1000, 100, 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "overlap" in pa.pa_last_error()
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_hash_fresh_batch(0, 0, 4, 0, 4, 0, 4, 1, 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG

@@ -236,3 +236,39 @@ def test_splitmix64_reference_values():
     assert [int(v) for v in w] == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
     b = syn.random_bits(123, 100)
     assert b.size == 2 and int(b[1]) >> 36 == 0
+
+
+# ---------------------------------------------------------------- Eq. (1) form (reading R2)
+def test_eq1_matrix_is_the_printed_figure():
+    """Eq. (1) as printed, square n x n with symbolic entries t_k = k: first row
+    t_0, t_n, t_{n+1}, .., t_{2n-2}; first column t_0 .. t_{n-1}; last row t_{n-1} .. t_1, t_0;
+    constant diagonals."""
+    n = 6
+    T = oracle.eq1_matrix(np.arange(2 * n - 1) % 256, n, n)
+    assert list(T[0]) == [0] + list(range(n, 2 * n - 1))
+    assert list(T[:, 0]) == list(range(n))
+    assert list(T[n - 1]) == list(range(n - 1, -1, -1))
+    assert list(T[1, :3]) == [1, 0, n]          # second printed row: t_1 t_0 t_n
+    for d in range(-(n - 1), n):
+        assert len(set(np.diagonal(T, offset=d))) == 1
+
+
+def test_eq1_hash_equals_diagonal_layout_after_conversion():
+    """The paper's r = u T with Eq. (1) equals this library's y = T x on
+    the converted seed, for random t, u and non-square shapes (n x l, l <= n)."""
+    rng = np.random.default_rng(1805)
+    for n, m in [(1, 1), (2, 1), (3, 2), (5, 5), (8, 3), (17, 9), (40, 13), (64, 64)]:
+        for _ in range(5):
+            t = rng.integers(0, 2, n + m - 1, dtype=np.uint8)
+            u = rng.integers(0, 2, n, dtype=np.uint8)
+            r = oracle.eq1_hash(t, u, n, m)
+            y = oracle.toeplitz_bits(n, m, oracle.seed_from_eq1(t, n, m), u)
+            assert np.array_equal(r, y), (n, m)
+
+
+def test_seed_from_eq1_is_an_involution_on_the_first_n_bits():
+    rng = np.random.default_rng(7)
+    t = rng.integers(0, 2, 30, dtype=np.uint8)
+    s = oracle.seed_from_eq1(t, 20, 11)
+    assert np.array_equal(oracle.seed_from_eq1(s, 20, 11), t)
+    assert np.array_equal(s[20:], t[20:])

@@ -377,3 +377,147 @@ def test_worst_case_rounding_all_ones(name):
         res = h.residual()
     assert np.all(got == (n & 1))
     assert res < 1e-3, res
+
+
+# ---------------------------------------------------------------- caller-owned workspace
+@pytest.mark.parametrize("route,n,m,split", [("bitpacked", 4096, 1024, 0), ("transform", 300_007, 60_001, 0),
+                                             ("transform", 300_007, 60_001, 200_000)])
+def test_workspace_owned_by_caller(route, n, m, split):
+    """pa_create_ws: the handle's device memory is the caller's tensor -- nothing else is
+    allocated (device free memory unchanged), the bytes match pa_workspace_size and the
+    result matches the oracle, for single keys, batches (chunked at batch_keys) and the
+    host path."""
+    sw = syn.random_bits(syn.seed_stream(61), n + m - 1)
+    keys = [syn.random_bits(syn.key_stream(61, k), n) for k in range(7)]
+    opts = dict(route=route, batch_keys=3, max_transform_len=split)
+    need = pa.workspace_size(n, m, **opts)
+    # every torch buffer first, so the free-memory check below sees libpa alone
+    seed_t = to_dev(sw)
+    ws = torch.empty(need, dtype=torch.uint8, device=DEV)
+    kt = torch.stack([to_dev(k) for k in keys])
+    w4 = ((m + 31) // 32 + 3) // 4 * 4
+    outs = torch.empty((len(keys), w4), dtype=torch.int32, device=DEV)
+    one = torch.empty(w4, dtype=torch.int32, device=DEV)
+    kh = kt[1].cpu().pin_memory()
+    oh = torch.zeros(w4, dtype=torch.int32).pin_memory()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    with pa.Hasher(n, m, seed_t, workspace=ws, **opts) as h:
+        h.hash_batch(kt, outs)
+        h.hash(kt[0], one)
+        h.hash_host(kh, oh)
+        torch.cuda.synchronize()
+        free1 = torch.cuda.mem_get_info()[0]
+        assert h.info["workspace_bytes"] == need
+        assert (h.info["column_blocks"] > 1) == bool(split)
+        assert h.residual() < 1e-3
+    assert abs(free0 - free1) <= (2 << 20), (free0, free1)  # no hidden cudaMalloc
+    for k, kw in enumerate(keys):
+        want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+        assert np.array_equal(from_dev(outs[k], m), want), k
+    assert np.array_equal(from_dev(one, m), oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[0]), m))
+    assert np.array_equal(oracle.unpack(oh.numpy().view(np.uint32), m),
+                          oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[1]), m))
+
+
+def test_workspace_too_small_is_nomem():
+    n, m = 100_000, 10_000
+    seed_t = to_dev(syn.random_bits(syn.seed_stream(62), n + m - 1))
+    need = pa.workspace_size(n, m, route="transform")
+    ws = torch.empty(need - 4096, dtype=torch.uint8, device=DEV)
+    with pytest.raises(pa.PaError) as e:
+        pa.Hasher(n, m, seed_t, route="transform", workspace=ws)
+    assert e.value.status == pa.PA_ERR_NOMEM and "workspace" in pa.pa_last_error()
+
+
+# ---------------------------------------------------------------- Eq. (4) split in a handle
+@pytest.mark.parametrize("n,m,maxlen", [(300_007, 60_001, 200_000), (500_009, 100_000, 350_000),
+                                        (65_537, 60_000, 61_000), (4_099, 4_000, 4_300)])
+def test_max_transform_len_split_matches_unsplit_and_oracle(n, m, maxlen):
+    """Plan invariance: the column-split handle (Eq. (4) blocks on seed windows
+    n - n_g - c0, partial outputs XOR-merged in place, Eq. (7)) reproduces y exactly, through
+    pa_hash, pa_hash_batch, pa_hash_u64 and pa_set_seed."""
+    sw = syn.random_bits(syn.seed_stream(63), n + m - 1)
+    sw2 = syn.random_bits(syn.seed_stream(64), n + m - 1)
+    keys = [syn.random_bits(syn.key_stream(63, k), n) for k in range(3)]
+    with pa.Hasher(n, m, to_dev(sw), route="transform", max_transform_len=maxlen) as h:
+        info = h.info
+        assert info["column_blocks"] > 1 and info["transform_len"] <= maxlen, info
+        y = [h.hash(to_dev(k)) for k in keys]
+        kt = torch.stack([to_dev(k) for k in keys])
+        yb = h.hash_batch(kt)
+        k64 = to_dev(keys[0])
+        o64 = torch.full((2 * ((m + 63) // 64) + 4,), -1, dtype=torch.int32, device=DEV)
+        pa.pa_hash_u64(h.handle, k64.data_ptr(), o64.data_ptr(), 0)
+        h.set_seed(to_dev(sw2))
+        y2 = h.hash(to_dev(keys[0]))
+        torch.cuda.synchronize()
+        assert h.residual() < 1e-3
+    for k, kw in enumerate(keys):
+        want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+        assert np.array_equal(from_dev(y[k], m), want), ("hash", k)
+        assert np.array_equal(from_dev(yb[k], m), want), ("batch", k)
+    w64 = o64.cpu().numpy().view(np.uint32)
+    assert np.array_equal(oracle.unpack(w64, m), oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[0]), m))
+    assert not oracle.unpack(w64[: 2 * ((m + 63) // 64)], 64 * ((m + 63) // 64))[m:].any()
+    assert np.array_equal(from_dev(y2, m), oracle.unpack(oracle.toeplitz_words(n, m, sw2, keys[0]), m))
+
+
+def test_max_transform_len_too_small_is_unsupported():
+    n, m = 10_000, 5_000
+    seed_t = to_dev(syn.random_bits(syn.seed_stream(65), n + m - 1))
+    with pytest.raises(pa.PaError) as e:
+        pa.Hasher(n, m, seed_t, route="transform", max_transform_len=m + 100)
+    assert e.value.status == pa.PA_ERR_UNSUPPORTED
+
+
+# ---------------------------------------------------------------- fresh seed per key
+@pytest.mark.parametrize("route,maxlen", [("bitpacked", 0), ("transform", 0), ("transform", 150_000)])
+def test_hash_fresh_batch_per_key_seeds(route, maxlen):
+    """NEXT-2: key k hashed with its own seed k, three transforms per key."""
+    n, m = (3_001, 1_000) if route == "bitpacked" else (120_001, 30_000)
+    count = 5
+    seeds = [syn.random_bits(syn.seed_stream(70 + k), n + m - 1) for k in range(count)]
+    keys = [syn.random_bits(syn.key_stream(70, k), n) for k in range(count)]
+    st, kt = torch.stack([to_dev(s) for s in seeds]), torch.stack([to_dev(k) for k in keys])
+    with pa.Hasher(n, m, st[0], route=route, max_transform_len=maxlen) as h:
+        outs = h.hash_fresh_batch(st, kt)
+        torch.cuda.synchronize()
+    for k in range(count):
+        want = oracle.unpack(oracle.toeplitz_words(n, m, seeds[k], keys[k]), m)
+        assert np.array_equal(from_dev(outs[k], m), want), k
+
+
+# ---------------------------------------------------------------- Eq. (1) seed converter
+@pytest.mark.parametrize("n,m", [(1, 1), (3, 2), (31, 2), (32, 32), (33, 7), (100, 61), (4096, 1024),
+                                 (100_003, 9_999)])
+def test_seed_from_paper_eq1_matches_oracle(n, m):
+    """pa_seed_from_paper_eq1 == the oracle's reading-R2 conversion bit for bit (garbage
+    past n+m-1 in the source is not copied), and hashing the converted seed equals the
+    paper's literal r = u T with Eq. (1) on small shapes."""
+    L = n + m - 1
+    rng = np.random.default_rng(n * 7 + m)
+    t01 = rng.integers(0, 2, L, dtype=np.uint8)
+    tw = oracle.pack(t01, 32)
+    tw = np.concatenate([tw, np.full(4, 0xFFFFFFFF, np.uint32)])  # garbage tail words
+    if L % 32:
+        tw[L // 32] |= np.uint32((0xFFFFFFFF << (L % 32)) & 0xFFFFFFFF)  # garbage bits past L
+    t_dev = torch.from_numpy(tw.view(np.int32).copy()).to(DEV)
+    s_dev = pa.seed_from_paper_eq1(t_dev, n, m)
+    torch.cuda.synchronize()
+    got = s_dev.cpu().numpy().view(np.uint32)
+    want = oracle.seed_from_eq1(t01, n, m)
+    assert np.array_equal(oracle.unpack(got, L), want)
+    assert not oracle.unpack(got[: (L + 31) // 32], 32 * ((L + 31) // 32))[L:].any()
+    if n * m <= 1 << 14:
+        u01 = rng.integers(0, 2, n, dtype=np.uint8)
+        with pa.Hasher(n, m, s_dev) as h:
+            y = from_dev(h.hash(to_dev(oracle.pack(u01))), m)
+        assert np.array_equal(y, oracle.eq1_hash(t01, u01, n, m))
+
+
+def test_seed_from_paper_eq1_rejects_overlap():
+    buf = torch.zeros(64, dtype=torch.int32, device=DEV)
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_seed_from_paper_eq1(buf.data_ptr(), buf[4:].data_ptr(), 500, 100, 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG
