@@ -344,6 +344,33 @@ def sweep(torch, pa, dev, steps=10):
         res[name + "_batched"] = {"n": n, "m": m, "keys": count, "ms_per_key": t,
                                   "gbit_s": n / (t * 1e-3) / 1e9, "transform_len": h.info["transform_len"]}
         h.close()
+    # C1 throughput: 2^16 keys against one seed, route (b) batched on the grid
+    n, m, sw, kw = syn.config_inputs("C1")
+    count = 1 << 16
+    h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+    kw32 = (n + 31) // 32
+    keys = dev_words(torch, kw, dev)[:kw32].repeat(count, 1).contiguous()
+    outs = h.new_out(count)
+    h.hash_batch(keys, outs)
+    ms = time_steps(torch, lambda: h.hash_batch(keys, outs), 3, flush)
+    t = float(np.mean(ms)) / count
+    res["C1_batched"] = {"n": n, "m": m, "keys": count, "route": h.route, "us_per_key": t * 1e3,
+                         "gbit_s": n / (t * 1e-3) / 1e9}
+    h.close()
+    # fresh seed per key (NEXT-2): seed transform + hash per key, C2 shape
+    n, m, sw, kw = syn.config_inputs("C2")
+    count = 8
+    seeds = torch.stack([dev_words(torch, syn.random_bits(syn.seed_stream(900 + k), n + m - 1), dev)
+                         for k in range(count)])
+    keys = torch.stack([dev_words(torch, kw, dev)] * count)
+    h = pa.Hasher(n, m, seeds[0])
+    outs = h.new_out(count)
+    h.hash_fresh_batch(seeds, keys, outs)
+    ms = time_steps(torch, lambda: h.hash_fresh_batch(seeds, keys, outs), 3, flush)
+    t = float(np.mean(ms)) / count
+    res["C2_fresh_seed"] = {"n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
+                            "note": "pa_hash_fresh_batch: new seed transform + hash per key"}
+    h.close()
     return res
 
 

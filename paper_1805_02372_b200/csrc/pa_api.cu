@@ -523,13 +523,7 @@ static pa_status batch_impl(pa_ctx *h, const uint32_t *keys, uint64_t key_stride
         }
         return PA_OK;
     }
-    if (h->route != PA_ROUTE_TRANSFORM) {
-        for (uint32_t k = 0; k < count; ++k) {
-            pa_status st = rb_hash(h, keys + k * key_stride, outs + k * out_stride, zero_words, s);
-            if (st != PA_OK) return st;
-        }
-        return PA_OK;
-    }
+    if (h->route != PA_ROUTE_TRANSFORM) return rb_hash_batch(h, keys, key_stride, outs, out_stride, count, zero_words, s);
     // keys in chunks: all kernels take the key index from the grid
     const uint32_t chunk = ra_batch_keys(h);
     for (uint32_t k0 = 0; k0 < count; k0 += chunk) {

@@ -128,6 +128,8 @@ pa_status rb_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status rb_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                   cudaStream_t s);
+pa_status rb_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs, uint64_t out_stride,
+                        uint32_t count, uint64_t zero_words, cudaStream_t s);
 void rb_destroy(pa_ctx *h);
 
 size_t ra_persist_bytes(const Geometry &g);

@@ -12,6 +12,8 @@
 // CTA take consecutive q (coalesced seed loads), the key word is a warp-uniform
 // broadcast load, and CTAs along y take disjoint key-word chunks whose partial
 // parities are merged with atomicXor (order-independent, hence deterministic).
+#include <algorithm>
+
 #include "bits.cuh"
 #include "pa_internal.h"
 
@@ -38,13 +40,19 @@ __global__ void k_reverse_seed(const uint32_t *__restrict__ seed, uint64_t off, 
 
 constexpr int kThreadsB = 128;
 
+// Threads of a CTA: qb consecutive offsets q (qb = 32, 64 or 128: all of them when
+// m is small) times 128/qb key-word chunks.  blockIdx.z = key of the batch.
 __global__ void __launch_bounds__(kThreadsB)
 k_toeplitz_bitpacked(const uint32_t *__restrict__ key, uint64_t n, uint64_t m,
                      const uint32_t *__restrict__ sr, uint32_t *__restrict__ out,
-                     uint64_t Q, uint64_t KW, uint64_t KC)
+                     uint64_t Q, uint64_t KW, uint64_t KC, uint32_t qb, uint64_t key_stride,
+                     uint64_t out_stride)
 {
-    uint64_t q = blockIdx.x * (uint64_t)kThreadsB + threadIdx.x;
-    uint64_t k0 = blockIdx.y * KC;
+    key += blockIdx.z * key_stride;
+    out += blockIdx.z * out_stride;
+    const uint32_t cb = kThreadsB / qb;
+    uint64_t q = blockIdx.x * (uint64_t)qb + threadIdx.x % qb;
+    uint64_t k0 = (blockIdx.y * (uint64_t)cb + threadIdx.x / qb) * KC;
     uint64_t k1 = min(KW, k0 + KC);
     if (q >= Q || k0 >= k1) return;
     uint32_t acc[32];
@@ -105,30 +113,44 @@ pa_status rb_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     return PA_OK;
 }
 
-pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
-                  cudaStream_t s)
+pa_status rb_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs, uint64_t out_stride,
+                        uint32_t count, uint64_t zero_words, cudaStream_t s)
 {
     uint64_t Q = (h->m + 31) / 32, KW = (h->n + 31) / 32;
-    cudaError_t e = cudaMemsetAsync(out, 0, zero_words * sizeof(uint32_t), s);
+    cudaError_t e = cudaSuccess;
+    if (zero_words)
+        e = count == 1 ? cudaMemsetAsync(outs, 0, zero_words * 4, s)
+                       : cudaMemset2DAsync(outs, out_stride * 4, 0, zero_words * 4, count, s);
     if (e != cudaSuccess) return cuda_fail(e, "route (b) output memset");
-    // key-word chunk so that ~8 CTAs per SM worth of (q, chunk) items exist
-    uint64_t gx = (Q + kThreadsB - 1) / kThreadsB;
-    uint64_t want_y = (148ull * 8 + gx - 1) / gx;
+    const uint32_t qb = Q <= 32 ? 32 : Q <= 64 ? 64 : kThreadsB;
+    const uint32_t cb = kThreadsB / qb;
+    // key-word chunk so that ~8 CTAs per SM worth of (q, chunk) items exist (over the batch)
+    uint64_t gx = (Q + qb - 1) / qb;
+    uint64_t want_y = std::max<uint64_t>(1, (148ull * 8 * cb + gx * count - 1) / (gx * count));
     uint64_t KC = (KW + want_y - 1) / want_y;
     if (KC < 16) KC = 16;
-    uint64_t gy = (KW + KC - 1) / KC;
+    uint64_t gy = ((KW + KC - 1) / KC + cb - 1) / cb;
     if (gy > 65535) {
-        gy = 65535;
-        KC = (KW + gy - 1) / gy;
-        gy = (KW + KC - 1) / KC;
+        KC = (KW + 65535 * cb - 1) / (65535 * cb);
+        gy = ((KW + KC - 1) / KC + cb - 1) / cb;
     }
-    dim3 grid((unsigned)gx, (unsigned)gy);
     prof_begin(h, 3, s);
-    k_toeplitz_bitpacked<<<grid, kThreadsB, 0, s>>>(key, h->n, h->m, h->b.sr, out, Q, KW, KC);
+    for (uint32_t k0 = 0; k0 < count; k0 += 65535) {
+        const uint32_t c = count - k0 < 65535 ? count - k0 : 65535;
+        dim3 grid((unsigned)gx, (unsigned)gy, c);
+        k_toeplitz_bitpacked<<<grid, kThreadsB, 0, s>>>(keys + k0 * key_stride, h->n, h->m, h->b.sr,
+                                                        outs + k0 * out_stride, Q, KW, KC, qb, key_stride,
+                                                        out_stride);
+    }
     prof_end(h, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (b) kernel launch");
     return PA_OK;
+}
+
+pa_status rb_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words, cudaStream_t s)
+{
+    return rb_hash_batch(h, key, 0, out, 0, 1, zero_words, s);
 }
 
 void rb_destroy(pa_ctx *h)

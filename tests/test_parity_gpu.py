@@ -521,3 +521,28 @@ def test_seed_from_paper_eq1_rejects_overlap():
     with pytest.raises(pa.PaError) as e:
         pa.pa_seed_from_paper_eq1(buf.data_ptr(), buf[4:].data_ptr(), 500, 100, 0)
     assert e.value.status == pa.PA_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("n,m,count", [(4096, 1024, 300), (33, 7, 70_000), (20_000, 3_000, 9), (5_000, 5_000, 3)])
+def test_bitpacked_batch_native(n, m, count):
+    """Route (b) batches on grid.z (chunks of 65535 keys) with strided zeroing; every key vs
+    the oracle (sampled keys for the 70k batch)."""
+    kw32 = (n + 31) // 32
+    stride = (kw32 + 3) // 4 * 4
+    sw = syn.random_bits(syn.seed_stream(81), n + m - 1)
+    rng = np.random.default_rng(81)
+    keys = rng.integers(0, 2**32, (count, stride), dtype=np.uint64).astype(np.uint32)
+    with pa.Hasher(n, m, to_dev(sw), route="bitpacked") as h:
+        kt = torch.from_numpy(keys.view(np.int32)).to(DEV)
+        outs = h.new_out(count)
+        outs.fill_(-1)
+        h.hash_batch(kt, outs)
+        torch.cuda.synchronize()
+        got = outs.cpu().numpy().view(np.uint32)
+    check_k = range(count) if count <= 300 else np.unique(np.r_[0, 65534, 65535, count - 1,
+                                                                 rng.integers(0, count, 50)])
+    for k in check_k:
+        kk = keys[k].copy()
+        want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kk), m)
+        assert np.array_equal(oracle.unpack(got[k], m), want), k
+        assert not oracle.unpack(got[k][: (m + 31) // 32], 32 * ((m + 31) // 32))[m:].any()
