@@ -546,3 +546,49 @@ def test_bitpacked_batch_native(n, m, count):
         want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kk), m)
         assert np.array_equal(oracle.unpack(got[k], m), want), k
         assert not oracle.unpack(got[k][: (m + 31) // 32], 32 * ((m + 31) // 32))[m:].any()
+
+
+# ---------------------------------------------------------------- full outputs at scale (P11)
+@pytest.mark.parametrize("name", ["C3", "C5c", "C4"])
+def test_full_output_vs_fft_reference(name):
+    """Every output bit at the BASELINE sizes, in the bench's launch configuration, against
+    the FP64 pocketfft reference (tests/fft_ref.py, pinned to the direct oracle in
+    tests/test_fft_ref.py; its own rounding certificate must be < 0.25)."""
+    from fft_ref import fft_window
+    n, m, sw, kw = syn.config_inputs(name)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        out = h.hash(to_dev(kw))
+        torch.cuda.synchronize()
+        got = from_dev(out, m)
+        res = h.residual()
+    want, cert = fft_window(n, m, sw, kw)
+    assert cert < 0.25, cert
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, f"{name}: {bad.size} wrong bits, first {bad[:8]}"
+    assert res < 1e-3
+
+
+# ---------------------------------------------------------------- confirmation digest (NEXT-4)
+def test_confirmation_digest():
+    """a second, independently seeded Toeplitz hash to 64 bits; equal keys
+    confirm, every one of 100 single-bit flips is detected, digest == oracle."""
+    from paper_1805_02372_b200.confirm import confirmation_digest, digests_match
+    l, tag = 250_000, 64
+    key = syn.random_bits(syn.key_stream(95, 0), l)
+    tseed = syn.random_bits(syn.seed_stream(95), l + tag - 1)
+    ts = to_dev(tseed)
+    da = confirmation_digest(to_dev(key), l, ts, tag)
+    db = confirmation_digest(to_dev(key.copy()), l, ts, tag)
+    assert digests_match(da, db, tag)
+    assert np.array_equal(from_dev(da, tag), oracle.unpack(oracle.toeplitz_words(l, tag, tseed, key), tag))
+    rng = np.random.default_rng(95)
+    kb = key.view(np.uint32).copy()
+    missed = 0
+    for j in rng.choice(l, 100, replace=False):
+        flipped = kb.copy()
+        flipped[j // 32] ^= np.uint32(1 << (j % 32))
+        if digests_match(da, confirmation_digest(to_dev(flipped.view(np.uint64)), l, ts, tag), tag):
+            missed += 1
+    assert missed == 0
+    with pytest.raises(ValueError):
+        confirmation_digest(to_dev(key), l, ts, 32)
