@@ -29,6 +29,7 @@ struct RouteTables {
     double2 *W2lo, *W2hi;   // omega_N2^e
     double2 *thlo, *thhi;   // theta_b = exp(i pi b / (2 N2)) = zeta^{N1 b}, two-level
     uint32_t *rev2;         // K1 DIF output position p -> frequency index k_b
+    double2 *rho;           // [N2][64 + N1/64]: row p's two-level table of rho = e^{2 pi i (1-4k_b)/4M}
 };
 
 struct RouteA {

@@ -167,6 +167,16 @@ __global__ void k_tables(Geometry g, RouteTables T)
     }
 }
 
+// Per-row twist tables for K2 (create time): row p holds rho^e, rho = e^{2 pi i (1-4k)/4M},
+// k = rev2[p], as rlo[e & 63] * rhi[e >> 6] -- computing them in K2's prologue costs a
+// chain of 64-bit remainders, an FP64 division and sincospi per thread on every hash.
+__global__ void k_rho_tables(Geometry g, RouteTables T)
+{
+    const uint32_t w = 64 + g.f1.nhi;
+    double2 *r = T.rho + (size_t)blockIdx.x * w;
+    rho_tables(r, r + 64, g.f1.nhi, g.M, T.rev2[blockIdx.x]);
+}
+
 // ------------------------------------------------------------------ K0
 // Bit transpose of the zero-padded input into one bit stream per K1 column
 // group: group g (columns [gC, gC+C)) holds, for each row b < N2, the 2C bits
@@ -189,6 +199,7 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
     kb += (uint64_t)blockIdx.z * (g.N1 / g.C) * g.kbw;
     TRACE_BEGIN(0);
     __shared__ uint32_t tre[kK0Rows][kK0Cols / 32 + 1], tim[kK0Rows][kK0Cols / 32 + 1];
+    grid_dep_wait();    // launched with PDL itself: whatever wrote the key precedes us
     grid_dep_launch();  // K1 may start its prologue (K0 is a single short wave)
     const uint32_t C = g.C, twoC = 2 * C, epw = 32 / twoC;
     const uint32_t RB = k0_rows(g), CB = k0_cols(g), CW = CB / 32;
@@ -351,7 +362,10 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *sp = spec + (uint64_t)row * N1;
     load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi);
-    rho_tables(rlo, rhi, g.f1.nhi, g.M, __ldg(T.rev2 + row));
+    {
+        const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
+        load_tables(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
+    }
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
     if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
@@ -516,7 +530,7 @@ std::vector<uint32_t> smooth_numbers(uint32_t limit)
     return v;
 }
 
-bool make_plan(uint32_t Lt, FftPlan *P)
+bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16)
 {
     uint32_t L = Lt;
     int e2 = 0, e3 = 0, e5 = 0, e7 = 0;
@@ -534,10 +548,16 @@ bool make_plan(uint32_t Lt, FftPlan *P)
     for (int i = 0; i < e7; ++i) push(7);
     for (int i = 0; i < e5; ++i) push(5);
     for (int i = 0; i < e3; ++i) push(3);
-    if (e2 % 4 == 1) push(2);
-    if (e2 % 4 == 2) push(4);
-    if (e2 % 4 == 3) push(8);
-    for (int i = 0; i < e2 / 4; ++i) push(16);
+    if (rmax >= 16) {
+        if (e2 % 4 == 1) push(2);
+        if (e2 % 4 == 2) push(4);
+        if (e2 % 4 == 3) push(8);
+        for (int i = 0; i < e2 / 4; ++i) push(16);
+    } else {  // radix <= 8: more, lighter stages (one butterfly per thread at 512 threads)
+        if (e2 % 3 == 1) push(2);
+        if (e2 % 3 == 2) push(4);
+        for (int i = 0; i < e2 / 3; ++i) push(8);
+    }
     P->S = S;
     P->Lt = Lt;
     P->nhi = (Lt + 63) / 64;
@@ -649,7 +669,8 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     uint32_t logC = 0;
     while ((1u << logC) < g->C) ++logC;
     g->logC = logC;
-    make_plan(g->N1, &g->f1);
+    const char *r1 = getenv("PA_FORCE_RMAX1");  // developer override: row-plan radix cap
+    make_plan(g->N1, &g->f1, r1 ? (uint32_t)atoi(r1) : 16);
     make_plan(g->N2, &g->f2);
     g->tile1 = tile_bytes((uint64_t)g->N2 * g->C) / 16;
     g->tile2 = tile_bytes(g->N1) / 16;
@@ -664,7 +685,10 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     return PA_OK;
 }
 
-static size_t ntables(const Geometry &g) { return 64 + g.f1.nhi + 2 * (64 + g.f2.nhi); }
+static size_t ntables(const Geometry &g)
+{
+    return 64 + g.f1.nhi + 2 * (64 + g.f2.nhi) + (size_t)g.N2 * (64 + g.f1.nhi);
+}
 static size_t kb_bytes(const Geometry &g) { return (size_t)(g.N1 / g.C) * g.kbw * 4; }
 
 // Persistent block: spec [M] | tables | rev2 [N2] | resid.  Work block: buf [cap][M] |
@@ -717,12 +741,14 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     T.W2hi = p; p += g.f2.nhi;
     T.thlo = p; p += 64;
     T.thhi = p; p += g.f2.nhi;
+    T.rho = p; p += (size_t)g.N2 * (64 + g.f1.nhi);
 
     cudaError_t e;
     if ((e = cudaMemsetAsync(a.resid, 0, sizeof(unsigned long long), s)) != cudaSuccess)
         return cuda_fail(e, "route (a) residual reset");
     uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
     k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
+    k_rho_tables<<<g.N2, 128, 0, s>>>(g, T);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) table launch");
     h->kernels_per_hash = 4;
     return ra_seed(h, seed, s);
@@ -817,7 +843,7 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
     const Geometry &g = a.g;
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), count);
     prof_begin(h, 4, s);
-    k0_bits_transpose<<<g0, 256, 0, s>>>(keys, 0, h->n, a.kb, g, key_stride);
+    launch_pdl(k0_bits_transpose, g0, dim3(256), 0, s, keys, (uint64_t)0, h->n, a.kb, g, key_stride);
     prof_end(h, s);
     prof_begin(h, 0, s);
     launch_pdl(k1_fwd_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
