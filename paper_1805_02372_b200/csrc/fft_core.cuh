@@ -13,6 +13,7 @@ constexpr int kMaxStages = 24;
 // G = Lt / L (omega_L^{jk} = omega_Lt^{jkG}), nb = Lt / R butterflies per sequence.
 struct StageDesc {
     uint32_t R, L, Ls, G, nb;
+    uint32_t toff;   // G > 1: this stage's own table of omega_L^j at whi + toff (see butterfly)
     uint64_t magic;  // ceil(2^40 / Ls): t / Ls == (t * magic) >> 40 for t < 2^24
 };
 
@@ -20,6 +21,7 @@ struct FftPlan {
     int S;              // number of stages (0 when Lt == 1)
     uint32_t Lt;        // transform length
     uint32_t nhi;       // two-level twiddle table: omega_Lt^e = hi[e >> 6] * lo[e & 63]
+    uint32_t ntw;       // entries of the per-stage tables that follow hi[] (stages with G > 1)
     StageDesc st[kMaxStages];
 };
 
@@ -235,12 +237,25 @@ __device__ __forceinline__ void apply_twiddles(double2 *v, double2 w1)
     }
 }
 
+// omega_L^j of a stage.  G = 1: the plan's two-level table at e = j (consecutive lanes,
+// consecutive entries).  G > 1: reading the plan's table at e = jG would stride the
+// 64-entry low table by G (bank conflicts: up to 8-way for G = 40), so such a stage has
+// its own table indexed by j: lo[j & 63] (* hi[j >> 6] when Ls > 64), both exact
+// roundings of exp(-2 pi i e / Lt) computed at create time.
+__device__ __forceinline__ double2 stage_twiddle(const StageDesc &sd, uint32_t j, const double2 *wlo,
+                                                 const double2 *whi)
+{
+    if (sd.G == 1) return twiddle(wlo, whi, j);
+    const double2 *t = whi + sd.toff;
+    return sd.Ls > 64 ? cmul(t[64 + (j >> 6)], t[j & 63]) : t[j];
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void butterfly(double2 *v, uint32_t j, const StageDesc &sd, const double2 *wlo,
                                           const double2 *whi)
 {
     if (!INV) Dft<R, false>::run(v);
-    if (j) apply_twiddles<R, INV>(v, twiddle(wlo, whi, j * sd.G));
+    if (j) apply_twiddles<R, INV>(v, stage_twiddle(sd, j, wlo, whi));
     if (INV) Dft<R, true>::run(v);
 }
 

@@ -167,6 +167,24 @@ __global__ void k_tables(Geometry g, RouteTables T)
     }
 }
 
+// Per-stage twiddle tables (create time; see stage_twiddle in fft_core.cuh): stage s of plan
+// P holds omega_Lt^{jG} for j < min(64, Ls) at hi + toff and, when Ls > 64, omega_Lt^{64 j' G}
+// for j' < Ls/64 at hi + toff + 64.  `hi` is the plan's global hi[] table.
+__global__ void k_stage_tables(FftPlan P, double2 *hi)
+{
+    for (int s = 0; s < P.S; ++s) {
+        const StageDesc &d = P.st[s];
+        if (d.G == 1 || d.Ls <= 1) continue;
+        const uint32_t nlo = d.Ls > 64 ? 64 : d.Ls, nh = d.Ls > 64 ? (d.Ls + 63) / 64 : 0;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nlo + nh; i += gridDim.x * blockDim.x) {
+            const uint64_t e = i < nlo ? (uint64_t)i * d.G : 64ull * (i - nlo) * d.G;
+            double sn, cs;
+            sincospi(2.0 * (double)e / (double)P.Lt, &sn, &cs);
+            hi[d.toff + (i < nlo ? i : 64 + (i - nlo))] = make_double2(cs, -sn);
+        }
+    }
+}
+
 // Per-row twist tables for K2 (create time): row p holds rho^e, rho = e^{2 pi i (1-4k)/4M},
 // k = rev2[p], as rlo[e & 63] * rhi[e >> 6] -- computing them in K2's prologue costs a
 // chain of 64-bit remainders, an FP64 division and sincospi per thread on every hash.
@@ -255,13 +273,13 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     if (zero_out) zero_out += blockIdx.y * out_stride;
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
-    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
     uint32_t *rowbits = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
     TRACE_BEGIN(1);
     TSTAMPK(0, 0);
-    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     grid_dep_wait();  // K0's bit streams
     if (zero_out) {  // K3 XORs this hash's output bits in (zero_words = 0: accumulate)
@@ -352,7 +370,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
 {
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
-    double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi, *rhi = rlo + 64;
+    double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi + g.f1.ntw, *rhi = rlo + 64;
     // grid (keys, rows): the CTAs of one spectrum row run back to back, so the row is
     // read from HBM once per batch and served from L2 to the other keys
     const uint32_t row = blockIdx.y;
@@ -361,7 +379,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *sp = spec + (uint64_t)row * N1;
-    load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi);
+    load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
@@ -431,12 +449,12 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     out += blockIdx.y * out_stride;
     extern __shared__ double2 sm[];
     const uint32_t logC = g.logC, C = 1u << logC;
-    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi, *thhi = thlo + 64;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
     TRACE_BEGIN(3);
     TSTAMPK(2, 0);
-    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi);
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
     load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     grid_dep_wait();  // K2's rows
     // first inverse stage reads the columns straight from global when the per-row chunk is
@@ -561,7 +579,7 @@ bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16)
     P->S = S;
     P->Lt = Lt;
     P->nhi = (Lt + 63) / 64;
-    uint32_t span = Lt;
+    uint32_t span = Lt, off = P->nhi;  // per-stage tables follow the plan's hi[] table
     for (int i = 0; i < S; ++i) {
         StageDesc &d = P->st[i];
         d.R = (uint32_t)R[i];
@@ -570,8 +588,14 @@ bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16)
         d.G = Lt / span;
         d.nb = Lt / d.R;
         d.magic = ((1ull << 40) + d.Ls - 1) / d.Ls;
+        d.toff = 0;
+        if (d.G > 1 && d.Ls > 1) {  // Ls = 1: j = 0 only, no twiddles
+            d.toff = off;
+            off += d.Ls > 64 ? 64 + (d.Ls + 63) / 64 : d.Ls;
+        }
         span = d.Ls;
     }
+    P->ntw = off - P->nhi;
     return S < kMaxStages;
 }
 
@@ -584,11 +608,12 @@ static uint32_t kb_words(uint32_t N2, uint32_t C)  // K0 stream words per group 
     const uint32_t epw = 16 / C;
     return ((N2 + epw - 1) / epw + 3) / 4 * 4;
 }
-static uint32_t smem_k13(uint32_t N2, uint32_t C, uint32_t nhi2)
+// tile | twiddle tables (lo, hi, per-stage) | theta (K1/K3) or rho (K2) tables | K1 bit stream
+static uint32_t smem_k13(uint32_t N2, uint32_t C, const FftPlan &p2)
 {
-    return tile_bytes((uint64_t)N2 * C) + 2 * (64 + nhi2) * 16 + kb_words(N2, C) * 4;
+    return tile_bytes((uint64_t)N2 * C) + (2 * (64 + p2.nhi) + p2.ntw) * 16 + kb_words(N2, C) * 4;
 }
-static uint32_t smem_k2(uint32_t N1, uint32_t nhi1) { return tile_bytes(N1) + 2 * (64 + nhi1) * 16; }
+static uint32_t smem_k2(uint32_t N1, const FftPlan &p1) { return tile_bytes(N1) + (2 * (64 + p1.nhi) + p1.ntw) * 16; }
 
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len)
 {
@@ -605,7 +630,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     //  - a CTA needs >= ~1.6 us per stage pass whatever its size (latency floor).
     const double sm_rate = 148.0 * 1.9e9;
     for (uint32_t N1 : sm) {
-        if (smem_k2(N1, (N1 + 63) / 64) > kSmemLimit) break;
+        if (tile_bytes(N1) > kSmemLimit) break;
+        FftPlan p1;
+        if (!make_plan(N1, &p1) || smem_k2(N1, p1) > kSmemLimit) continue;
         uint64_t need = (Mmin + N1 - 1) / N1;
         if (need > 32768) continue;
         // every smooth N2 within +12% of the minimum: a longer but radix-16-friendly
@@ -614,11 +641,11 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         for (auto it = it0; it != sm.end() && *it <= need * 1.12 + 16; ++it) {
         const uint32_t N2 = *it;
         if (max_len && 2ull * N1 * N2 > max_len) continue;
-        FftPlan p1, p2;
-        if (!make_plan(N1, &p1) || !make_plan(N2, &p2)) continue;
+        FftPlan p2;
+        if (!make_plan(N2, &p2)) continue;
         for (uint32_t C = 16; C >= 1; C >>= 1) {
             if (N1 % C) continue;
-            uint32_t s13 = smem_k13(N2, C, (N2 + 63) / 64);
+            uint32_t s13 = smem_k13(N2, C, p2);
             if (s13 > kSmemLimit) continue;
             // measured: every FFT stage pass (and the load / store / twiddle passes around
             // them) costs ~0.62 cycles per element per SM, largely independent of the radix
@@ -626,7 +653,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             const double pass13 = p2.S + 2.0, pass2 = 2.0 * p1.S + 1.0;
             const double cfac = C == 1 ? 1.5 : C == 2 ? 1.0 : 0.95;  // short HBM runs (K1/K3)
             const uint32_t occ13 = std::min<uint32_t>(2, kSmemLimit / s13);
-            const uint32_t occ2 = std::min<uint32_t>(2, kSmemLimit / smem_k2(N1, (N1 + 63) / 64));
+            const uint32_t occ2 = std::min<uint32_t>(2, kSmemLimit / smem_k2(N1, p1));
             auto ktime = [&](double passes, double fac, uint32_t occ, double ctas) {
                 double thr = M * passes * 0.62 * fac / sm_rate;
                 double waves = std::ceil(ctas / (148.0 * occ));
@@ -647,10 +674,10 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // developer override for plan experiments: PA_FORCE_PLAN="N1,N2,C"
     if (const char *fp = getenv("PA_FORCE_PLAN")) {
         unsigned f1 = 0, f2 = 0, fc = 0;
-        FftPlan tmp;
+        FftPlan q1, q2;
         if (sscanf(fp, "%u,%u,%u", &f1, &f2, &fc) == 3 && (uint64_t)f1 * f2 >= Mmin && fc >= 1 &&
-            fc <= 16 && (fc & (fc - 1)) == 0 && f1 % fc == 0 && make_plan(f1, &tmp) && make_plan(f2, &tmp) &&
-            smem_k2(f1, (f1 + 63) / 64) <= kSmemLimit && smem_k13(f2, fc, (f2 + 63) / 64) <= kSmemLimit) {
+            fc <= 16 && (fc & (fc - 1)) == 0 && f1 % fc == 0 && make_plan(f1, &q1) && make_plan(f2, &q2) &&
+            smem_k2(f1, q1) <= kSmemLimit && smem_k13(f2, fc, q2) <= kSmemLimit) {
             g->N1 = f1;
             g->N2 = f2;
             g->C = fc;
@@ -674,9 +701,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     make_plan(g->N2, &g->f2);
     g->tile1 = tile_bytes((uint64_t)g->N2 * g->C) / 16;
     g->tile2 = tile_bytes(g->N1) / 16;
-    g->smem1 = smem_k13(g->N2, g->C, g->f2.nhi);
+    g->smem1 = smem_k13(g->N2, g->C, g->f2);
     g->kbw = kb_words(g->N2, g->C);
-    g->smem2 = smem_k2(g->N1, g->f1.nhi);
+    g->smem2 = smem_k2(g->N1, g->f1);
     // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
     g->t1 = 2 * g->smem1 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
     g->t2 = 2 * g->smem2 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
@@ -687,7 +714,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
 
 static size_t ntables(const Geometry &g)
 {
-    return 64 + g.f1.nhi + 2 * (64 + g.f2.nhi) + (size_t)g.N2 * (64 + g.f1.nhi);
+    return 64 + g.f1.nhi + g.f1.ntw + 64 + g.f2.nhi + g.f2.ntw + 64 + g.f2.nhi + (size_t)g.N2 * (64 + g.f1.nhi);
 }
 static size_t kb_bytes(const Geometry &g) { return (size_t)(g.N1 / g.C) * g.kbw * 4; }
 
@@ -736,9 +763,9 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     a.resid = reinterpret_cast<unsigned long long *>(pb);
     double2 *p = a.tables;
     T.W1lo = p; p += 64;
-    T.W1hi = p; p += g.f1.nhi;
+    T.W1hi = p; p += g.f1.nhi + g.f1.ntw;  // stage tables follow hi[] (one contiguous copy)
     T.W2lo = p; p += 64;
-    T.W2hi = p; p += g.f2.nhi;
+    T.W2hi = p; p += g.f2.nhi + g.f2.ntw;
     T.thlo = p; p += 64;
     T.thhi = p; p += g.f2.nhi;
     T.rho = p; p += (size_t)g.N2 * (64 + g.f1.nhi);
@@ -749,6 +776,8 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
     k_tables<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 4096), 256, 0, s>>>(g, T);
     k_rho_tables<<<g.N2, 128, 0, s>>>(g, T);
+    k_stage_tables<<<4, 256, 0, s>>>(g.f1, T.W1hi);
+    k_stage_tables<<<4, 256, 0, s>>>(g.f2, T.W2hi);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) table launch");
     h->kernels_per_hash = 4;
     return ra_seed(h, seed, s);
