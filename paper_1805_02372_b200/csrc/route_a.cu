@@ -266,7 +266,8 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
 // Column DIF of C adjacent columns; input = this group's bit stream from K0.
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
-               uint32_t *__restrict__ zero_out, uint64_t zero_words, uint64_t out_stride)
+               uint32_t *__restrict__ zero_out, uint64_t zero_words, uint64_t out_stride,
+               const uint32_t *__restrict__ xkey, uint64_t xstride, uint64_t xbits)
 {
     kb += (uint64_t)blockIdx.y * (g.N1 / g.C) * g.kbw;        // batch: key blockIdx.y
     buf += (uint64_t)blockIdx.y * g.M;
@@ -287,8 +288,26 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
              i += (uint64_t)gridDim.x * blockDim.x)
             zero_out[i] = 0u;
     }
-    const uint32_t *src = kb + (uint64_t)blockIdx.x * g.kbw;
-    for (uint32_t i = threadIdx.x; i < g.kbw; i += blockDim.x) rowbits[i] = __ldg(src + i);
+    if (xkey) {
+        // wide column groups (C >= 8: runs of >= 1 byte per row) gather their bit stream
+        // from the key directly instead of through K0 -- the same entries K0 would write:
+        // row b holds x[a0 + N1 b + c] (c < C) then x[M + a0 + N1 b + c], zero past n
+        const uint32_t *kx = xkey + blockIdx.y * xstride;
+        const uint32_t twoC = 2 * C, epw = 32 / twoC, mask = (1u << C) - 1u;
+        for (uint32_t i = threadIdx.x; i < g.kbw; i += blockDim.x) rowbits[i] = 0u;
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < g.N2; b += blockDim.x) {
+            const int64_t u = (int64_t)a0 + (int64_t)g.N1 * b;
+            const uint32_t re = bits32(kx, u, 0, (int64_t)xbits) & mask;
+            const uint32_t im = bits32(kx, u + (int64_t)g.M, 0, (int64_t)xbits) & mask;
+            const uint32_t ent = re | (im << C);
+            if (epw == 1) rowbits[b] = ent;
+            else if (ent) atomicOr(rowbits + b / epw, ent << ((b % epw) * twoC));
+        }
+    } else {
+        const uint32_t *src = kb + (uint64_t)blockIdx.x * g.kbw;
+        for (uint32_t i = threadIdx.x; i < g.kbw; i += blockDim.x) rowbits[i] = __ldg(src + i);
+    }
     TSTAMPK(0, 1);
     __syncthreads();
     TSTAMPK(0, 2);
@@ -737,6 +756,17 @@ static void carve_work(RouteA &a, char *blk, uint32_t cap)
     a.cap = cap;
 }
 
+// K1 reads the key itself (no K0) when its column groups are at least `min C` wide:
+// C = 16 (2-byte runs) saves K0 on the small transforms (C2 38.9 -> 37.9 us cold)
+static bool k1_direct(const Geometry &g)
+{
+    static const uint32_t cmin = [] {
+        const char *e = getenv("PA_K1_DIRECT_MINC");  // developer override (0 = never)
+        return e ? (uint32_t)atoi(e) : 16u;  // C = 8 measured slower (C3 K1 66 -> 80 us)
+    }();
+    return cmin && g.C >= cmin;
+}
+
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 {
     char err[256];
@@ -779,7 +809,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     k_stage_tables<<<4, 256, 0, s>>>(g.f1, T.W1hi);
     k_stage_tables<<<4, 256, 0, s>>>(g.f2, T.W2hi);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) table launch");
-    h->kernels_per_hash = 4;
+    h->kernels_per_hash = k1_direct(g) ? 3 : 4;
     return ra_seed(h, seed, s);
 }
 
@@ -800,7 +830,7 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0);
+    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
     k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) seed transform launches");
     return PA_OK;
@@ -871,12 +901,15 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
     RouteA &a = h->a;
     const Geometry &g = a.g;
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), count);
-    prof_begin(h, 4, s);
-    launch_pdl(k0_bits_transpose, g0, dim3(256), 0, s, keys, (uint64_t)0, h->n, a.kb, g, key_stride);
-    prof_end(h, s);
+    const bool direct = k1_direct(g);
+    if (!direct) {
+        prof_begin(h, 4, s);
+        launch_pdl(k0_bits_transpose, g0, dim3(256), 0, s, keys, (uint64_t)0, h->n, a.kb, g, key_stride);
+        prof_end(h, s);
+    }
     prof_begin(h, 0, s);
     launch_pdl(k1_fwd_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
-               out_stride);
+               out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
     prof_end(h, s);
     prof_begin(h, 1, s);
     launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.spec, g, a.T, 0, 1.0);
