@@ -206,7 +206,7 @@ pa_status pa_options_init(pa_options *opt)
 
 static void destroy_ctx(pa_ctx *h)
 {
-    for (uint32_t g = 0; g < h->nsub; ++g)
+    for (uint32_t g = 0; h->sub && g < h->nsub; ++g)
         if (h->sub[g]) destroy_ctx(h->sub[g]);
     delete[] h->sub;
     delete[] h->sub_c0;
@@ -400,12 +400,14 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
     cudaStream_t s = (cudaStream_t)stream;
     if (st == PA_OK && c0.size() > 1) {
         // Eq. (4) split: block g = key bits [c0, c0 + ng), seed window offset n - ng - c0
-        h->nsub = (uint32_t)c0.size();
-        h->sub = new (std::nothrow) pa_ctx *[h->nsub]();
-        h->sub_c0 = new (std::nothrow) uint64_t[h->nsub];
+        const uint32_t nb = (uint32_t)c0.size();
+        h->sub = new (std::nothrow) pa_ctx *[nb]();
+        h->sub_c0 = new (std::nothrow) uint64_t[nb];
         if (!h->sub || !h->sub_c0) {
-            set_error("host allocation of %u block handles failed", h->nsub);
+            set_error("host allocation of %u block handles failed", nb);
             st = PA_ERR_NOMEM;
+        } else {
+            h->nsub = nb;  // only now: destroy_ctx walks sub[0 .. nsub)
         }
         for (uint32_t g = 0; st == PA_OK && g < h->nsub; ++g) {
             const uint64_t ng = (g + 1 < h->nsub ? c0[g + 1] : n) - c0[g];
