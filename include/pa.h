@@ -78,8 +78,8 @@ typedef struct pa_options {
     uint32_t allow_wide;      /* 1 = accept m > n (column shards of the Eq. (4) split,
                                  P:107-110, have n_g < m); default 0 keeps 1 <= m <= n */
     uint32_t batch_keys;      /* keys per launch in pa_hash_batch (0 = library choice).  With
-                                 a caller workspace (pa_create_ws) it sizes the per-key work
-                                 buffers: 0 means 1 */
+                                 a caller workspace (pa_create_ws), and for the column blocks of
+                                 a split handle, it fixes the per-key work buffers: 0 means 1 */
     uint64_t max_transform_len; /* route (a): 0 = no limit.  Otherwise the key is cut into
                                  column blocks (Eq. (4)) so that no block's real
                                  transform length exceeds this; each block is hashed on its
@@ -87,7 +87,8 @@ typedef struct pa_options {
                                  are XOR-merged in place (Eq. (7)).  Blocks start at
                                  multiples of 128 key bits.  PA_ERR_UNSUPPORTED if even a
                                  128-bit block's transform (>= 128 + m - 1) exceeds it.  Ignored
-                                 by route (b) */
+                                 by route (b).  With 0, pa_create splits by itself when n + m is
+                                 beyond one transform (~3.3e8 bits; pa_plan reports the blocks) */
     uint32_t reserved[3];     /* must be zero */
 } pa_options;
 

@@ -272,6 +272,11 @@ static pa_status parse_options(const pa_options *opt, uint64_t n, uint64_t m, pa
     return PA_OK;
 }
 
+// (an upper bound on) the longest real transform one route-(a) plan reaches: a K2 row (N1
+// points) and a K1/K3 column (N2 points) must each fit one CTA's 227 KB of shared memory at
+// 17 bytes per padded complex point, so N1, N2 <~ 13.3 k; two reals per complex point
+static const uint64_t kMaxPlanLen = 2ull * 13312 * 13312;
+
 static bool plan_fits(uint64_t n, uint64_t m, uint64_t maxlen)  // route (a) can plan within the cap
 {
     Geometry g;
@@ -285,7 +290,14 @@ static bool plan_fits(uint64_t n, uint64_t m, uint64_t maxlen)  // route (a) can
 static pa_status split_plan(uint64_t n, uint64_t m, uint64_t maxlen, std::vector<uint64_t> *c0)
 {
     c0->assign(1, 0);
-    if (!maxlen || plan_fits(n, m, maxlen)) return PA_OK;
+    if (!maxlen) {
+        // no cap requested: split only when no single transform can be planned (n + m beyond
+        // ~3.5e8 bits -- the paper's length-compatible regime), with the blocks as
+        // long as one plan allows
+        if (plan_fits(n, m, 0)) return PA_OK;
+        maxlen = kMaxPlanLen;
+    }
+    if (plan_fits(n, m, maxlen)) return PA_OK;
     if (maxlen + 1 < m + 128) {
         set_error("max_transform_len = %llu cannot hold even a 128-bit key block with m = %llu "
                   "(needs >= %llu)", (unsigned long long)maxlen, (unsigned long long)m,
@@ -329,16 +341,21 @@ static pa_status handle_bytes(uint64_t n, uint64_t m, const pa_options &o, bool 
     std::vector<uint64_t> c0;
     pa_status st = split_plan(n, m, o.max_transform_len, &c0);
     if (st != PA_OK) return st;
-    const uint32_t cap = arena && o.batch_keys ? o.batch_keys : 1;
+    const uint32_t cap = (arena || c0.size() > 1) && o.batch_keys ? o.batch_keys : 1;
+    const uint64_t cap_len = c0.size() > 1 && !o.max_transform_len ? kMaxPlanLen : o.max_transform_len;
+    size_t w0 = 0;
     for (size_t g = 0; g < c0.size(); ++g) {
         const uint64_t ng = (g + 1 < c0.size() ? c0[g + 1] : n) - c0[g];
         Geometry geo;
         char err[256];
-        if ((st = ra_plan(ng, m, &geo, err, sizeof err, o.max_transform_len)) != PA_OK) {
+        if ((st = ra_plan(ng, m, &geo, err, sizeof err, cap_len)) != PA_OK) {
             set_error("%s", err);
             return st;
         }
-        *bytes += ra_persist_bytes(geo) + ra_work_bytes(geo, cap);
+        const size_t w = ra_work_bytes(geo, cap);
+        *bytes += ra_persist_bytes(geo);
+        if (g == 0) w0 = w;
+        if (g == 0 || w > w0) *bytes += w;  // later blocks borrow block 0's work buffers (create_impl)
     }
     return PA_OK;
 }
@@ -381,6 +398,7 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
     h->route = o.route;
     h->batch_opt = o.batch_keys;
     h->max_len = o.route == PA_ROUTE_TRANSFORM ? o.max_transform_len : 0;
+    if (o.route == PA_ROUTE_TRANSFORM && c0.size() > 1 && !h->max_len) h->max_len = kMaxPlanLen;  // auto split
     if (workspace) {
         h->arena = new (std::nothrow) Arena();
         if (!h->arena) {
@@ -429,6 +447,10 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
             b->route = PA_ROUTE_TRANSFORM;
             b->batch_opt = h->batch_opt;
             b->max_len = h->max_len;
+            if (g > 0) {
+                b->share_w = h->sub[0]->a.wblk;
+                b->share_w_bytes = ra_work_bytes(h->sub[0]->a.g, h->sub[0]->a.cap);
+            }
             st = ra_create(b, seed_bits, s);
             h->kernels_per_hash += b->kernels_per_hash;
         }
@@ -545,7 +567,7 @@ static bool batch_grows(const pa_ctx *h, uint32_t count)
             if (batch_grows(h->sub[g], count)) return true;
         return false;
     }
-    if (h->route != PA_ROUTE_TRANSFORM || h->arena) return false;
+    if (h->route != PA_ROUTE_TRANSFORM || h->arena || h->parent) return false;
     const uint32_t chunk = ra_batch_keys(h);
     return h->a.cap < (count < chunk ? count : chunk);
 }
@@ -872,10 +894,14 @@ pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
         info->column_blocks = 1;
         return PA_OK;
     }
+    // the column split pa_create falls back to when no single transform can be planned
+    std::vector<uint64_t> c0;
+    pa_status st = split_plan(n, m, 0, &c0);
+    if (st != PA_OK) return st;
     Geometry g;
     char err[256];
-    pa_status st = ra_plan(n, m, &g, err, sizeof err);
-    if (st != PA_OK) {
+    const uint64_t n0 = c0.size() > 1 ? c0[1] : n;
+    if ((st = ra_plan(n0, m, &g, err, sizeof err, c0.size() > 1 ? kMaxPlanLen : 0)) != PA_OK) {
         set_error("%s", err);
         return st;
     }
@@ -883,9 +909,14 @@ pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
     info->n1 = g.N1;
     info->n2 = g.N2;
     info->cols_per_cta = g.C;
-    info->workspace_bytes = ra_persist_bytes(g) + ra_work_bytes(g, 1);
-    info->kernels_per_hash = 4;
-    info->column_blocks = 1;
+    pa_options o;
+    pa_options_init(&o);
+    o.route = PA_ROUTE_TRANSFORM;
+    size_t b = 0;
+    if ((st = handle_bytes(n, m, o, false, &b)) != PA_OK) return st;
+    info->workspace_bytes = b;
+    info->kernels_per_hash = (uint64_t)c0.size() * (g.C >= 16 ? 3 : 4);
+    info->column_blocks = c0.size();
     return PA_OK;
 }
 

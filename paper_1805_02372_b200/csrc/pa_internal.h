@@ -43,6 +43,7 @@ struct RouteA {
     unsigned long long *resid = nullptr; // max |v - rint v| (as double bits)
     uint32_t *kb = nullptr;    // K0 output: per-column-group bit streams of the input
     uint32_t cap = 0;          // keys the work buffers (buf, kb) hold
+    bool shared_w = false;     // work block borrowed from the first column block (not owned)
 };
 
 // ---------------------------------------------------------------- route (b)
@@ -102,6 +103,8 @@ struct pa_ctx {
     uint64_t *sub_c0 = nullptr;  // first key bit of each block (multiple of 128)
     uint32_t nsub = 0;
     uint64_t max_len = 0;        // pa_options.max_transform_len (route (a) planning cap)
+    char *share_w = nullptr;     // column blocks 1..: the first block's work block, if large enough
+    size_t share_w_bytes = 0;
     // pa_hash_host as one CUDA graph (H2D, kernels, D2H); host pointers patched per call
     cudaGraph_t host_graph = nullptr;
     cudaGraphExec_t host_exec = nullptr;

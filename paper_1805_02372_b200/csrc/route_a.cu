@@ -779,11 +779,20 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     RouteA &a = h->a;
     RouteTables &T = a.T;
     char *pb = nullptr, *wb = nullptr;
-    const uint32_t cap = h->arena && h->batch_opt ? h->batch_opt : 1;
+    // fixed work-buffer capacity for workspace handles and for the column blocks of a split
+    // handle (they share block 0's buffers, which therefore must never be reallocated)
+    const uint32_t cap = (h->arena || h->parent) && h->batch_opt ? h->batch_opt : 1;
     if ((st = dev_alloc(h, (void **)&pb, ra_persist_bytes(g), "route (a) spectrum + tables"))) return st;
     a.pblk = pb;
-    if ((st = dev_alloc(h, (void **)&wb, ra_work_bytes(g, cap), "route (a) work buffers"))) return st;
-    carve_work(a, wb, cap);
+    if (h->share_w && ra_work_bytes(g, cap) <= h->share_w_bytes) {
+        // a later column block of a split handle: blocks run one after another in stream
+        // order, so they share the first block's work buffers
+        carve_work(a, h->share_w, cap);
+        a.shared_w = true;
+    } else {
+        if ((st = dev_alloc(h, (void **)&wb, ra_work_bytes(g, cap), "route (a) work buffers"))) return st;
+        carve_work(a, wb, cap);
+    }
     a.spec = reinterpret_cast<double2 *>(pb);
     pb += al256(g.M * sizeof(double2));
     a.tables = reinterpret_cast<double2 *>(pb);
@@ -859,7 +868,7 @@ static pa_status ra_reserve(pa_ctx *h, uint32_t count)
 {
     RouteA &a = h->a;
     if (count <= a.cap) return PA_OK;
-    if (h->arena) {
+    if (h->arena || h->parent) {
         set_error("route (a): %u keys in flight exceed the workspace's %u (pa_options.batch_keys)", count,
                   a.cap);
         return PA_ERR_NOMEM;
@@ -883,7 +892,7 @@ static pa_status ra_reserve(pa_ctx *h, uint32_t count)
 
 uint32_t ra_batch_keys(const pa_ctx *h)
 {
-    if (h->arena) return h->a.cap;        // the workspace was sized for this many
+    if (h->arena || h->parent) return h->a.cap;  // fixed-size (workspace or shared) buffers
     if (h->batch_opt) return h->batch_opt;
     // keys per launch: enough CTAs to fill the GPU for small transforms, within 4 GiB
     const Geometry &g = h->a.g;
@@ -943,7 +952,7 @@ void ra_destroy(pa_ctx *h)
 {
     RouteA &a = h->a;
     dev_free(h, a.pblk);
-    dev_free(h, a.wblk);
+    if (!a.shared_w) dev_free(h, a.wblk);
     a = RouteA{};
 }
 

@@ -135,7 +135,9 @@ def test_planner_host_only():
             assert e.status == pa.PA_ERR_UNSUPPORTED
             continue
         if p["route"] == pa.PA_ROUTE_TRANSFORM:
-            assert p["transform_len"] >= n + m - 1
+            # a column-split plan covers its longest block (<= ceil(n / blocks) + 127 bits) plus m
+            nb = -(-n // p["column_blocks"]) if p["column_blocks"] > 1 else n
+            assert p["transform_len"] >= min(n, nb) + m - 1
 
 
 def test_workspace_size_is_host_only_and_adds_up():
@@ -153,7 +155,7 @@ def test_workspace_size_is_host_only_and_adds_up():
     assert one >= 32 * (info["transform_len"] // 2)
     assert four - one >= 3 * 16 * (info["transform_len"] // 2)
     split = pa.workspace_size(n, m, route="transform", max_transform_len=600_000)
-    assert split > one  # two or more blocks, each with its own spectrum
+    assert split >= 16 * (info["transform_len"] // 2)  # one spectrum per block, 16 B per complex point
     # an unsplit handle whose default plan already fits is unchanged by the cap
     assert pa.workspace_size(n, m, route="transform", max_transform_len=10**9) == one
 
@@ -183,3 +185,14 @@ def test_option_and_pointer_errors_before_device_work():
     with pytest.raises(pa.PaError) as e:
         pa.pa_hash_fresh_batch(0, 0, 4, 0, 4, 0, 4, 1, 0)
     assert e.value.status == pa.PA_ERR_INVALID_ARG
+
+
+def test_plan_splits_keys_beyond_one_transform():
+    """pa_plan (host-only) reports the Eq. (4) column split pa_create falls back to when n + m
+    exceeds what one transform plans, and no split below that."""
+    import paper_1805_02372_b200 as pa
+    assert pa.pa_plan(10**8, 2 * 10**7)["column_blocks"] == 1
+    p = pa.pa_plan(10**9, 10**8)
+    assert p["column_blocks"] > 1 and p["transform_len"] < 10**9 + 10**8
+    p = pa.pa_plan(10**10, 10**7)
+    assert p["column_blocks"] >= 28 and p["workspace_bytes"] < 180 * 2**30

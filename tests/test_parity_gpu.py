@@ -592,3 +592,30 @@ def test_confirmation_digest():
     assert missed == 0
     with pytest.raises(ValueError):
         confirmation_digest(to_dev(key), l, ts, 32)
+
+
+# ---------------------------------------------------------------- keys beyond one transform
+def test_auto_split_gigabit_key():
+    """n ~ 10^9 (the paper's 50-100 km regime): no single transform plans, so
+    pa_create splits the key into Eq. (4) column blocks by itself (plain pa_create, default
+    options).  Sampled rows vs the oracle for a random key; every output bit vs the all-ones
+    closed form y[i] = P[i+n] xor P[i] (P = prefix XOR of the seed)."""
+    n, m = 1_000_000_007, 100_000_003
+    sw = syn.random_bits(syn.seed_stream(97), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(97, 0), n)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        assert h.info["column_blocks"] > 1 and h.route == "transform", h.info
+        out = h.hash(to_dev(kw))
+        ones = h.hash(to_dev(syn.ones_bits(n)))
+        torch.cuda.synchronize()
+        assert h.residual() < 1e-3
+        got = from_dev(out, m)
+        got_ones = from_dev(ones, m)
+    rows = sample_rows(m, 97, k=512)
+    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+    s01 = oracle.unpack(sw, n + m - 1)
+    P = np.zeros(n + m, dtype=np.uint8)
+    np.bitwise_xor.accumulate(s01, out=P[1:])
+    want = P[n:n + m] ^ P[:m]
+    bad = np.flatnonzero(got_ones != want)
+    assert bad.size == 0, f"{bad.size} wrong bits, first {bad[:8]}"
