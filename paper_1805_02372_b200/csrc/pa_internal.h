@@ -22,6 +22,7 @@ struct Geometry {
     uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)
     uint32_t smem1, smem2;  // dynamic shared bytes: K1/K3, K2
     uint32_t kbw;           // K0 bit-stream words per column group
+    uint32_t pf2;           // K2: L2 prefetch distance in rows (0 = off)
 };
 
 struct RouteTables {

@@ -442,6 +442,18 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
         return;
     }
     TSTAMP(2);
+    if (g.pf2 && mode == 0 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
+        // the CTA one wave ahead will load row + pf2: start pulling it into L2 now, under this
+        // row's compute (multi-wave grids only, see ra_plan; C4 K2 1219 -> 1129 us.  Prefetching
+        // the spectrum row as well, or K3's next column group, measured slower)
+        const uint32_t q = threadIdx.x;
+        const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
+        const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
+        if (q * chunk < bytes) {
+            const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)q * chunk), "r"(sz) : "memory");
+        }
+    }
     dif_stages(sm, P, dif_from, P.S - 1, 0, wlo, whi);
     TSTAMP(3);
     fused_mid_any(P.st[P.S - 1], sm, sp);
@@ -726,6 +738,13 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
     g->t1 = 2 * g->smem1 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
     g->t2 = 2 * g->smem2 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
+    // K2: L2 prefetch of the row one wave ahead when one CTA per SM runs > 2 waves (C4); it
+    // measured slower at two CTAs per SM.  Developer override PA_PF=0 turns it off
+    {
+        const char *e = getenv("PA_PF");
+        const bool pf = !e || atoi(e) != 0;
+        g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
+    }
     if (const char *e = getenv("PA_FORCE_T1")) g->t1 = (uint32_t)atoi(e);  // developer overrides
     if (const char *e = getenv("PA_FORCE_T2")) g->t2 = (uint32_t)atoi(e);
     return PA_OK;
