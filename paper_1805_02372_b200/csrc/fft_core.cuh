@@ -272,6 +272,7 @@ struct StageCtx {
     double2 *gout = nullptr;                         // K2 row in global memory
     const double2 *gin = nullptr;                    // MODE_TAU_IN / MODE_GCOL: global input
     uint32_t ld = 0;                                 // MODE_GCOL(_OUT): row pitch in elements
+    uint32_t nth = 0;                                // threads sharing the stage (0 = blockDim.x)
 };
 
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
@@ -287,7 +288,8 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
     const uint32_t nb = sd.nb << logC;
     const uint32_t cm = (1u << logC) - 1;
     const uint32_t stride = sd.Ls << logC;
-    for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
+    const uint32_t nth = x.nth ? x.nth : blockDim.x;
+    for (uint32_t q = threadIdx.x; q < nb; q += nth) {
         const uint32_t c = q & cm, t = q >> logC;
         const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
         const uint32_t j = t - g * sd.Ls;

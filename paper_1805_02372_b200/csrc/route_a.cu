@@ -472,32 +472,10 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
 }
 
 // ------------------------------------------------------------------ K3
-__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
-k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
-               uint32_t *__restrict__ out, unsigned long long *__restrict__ resid, uint64_t out_stride)
+// Rows b of column group a0 that hold output-window bits: [b_lo, b_hi).
+__device__ __forceinline__ void k3_window_rows(const Geometry &g, uint32_t a0, uint32_t C, uint64_t n, uint64_t m,
+                                               int64_t *blo, int64_t *bhi)
 {
-    buf += (uint64_t)blockIdx.y * g.M;                        // batch: key blockIdx.y
-    out += blockIdx.y * out_stride;
-    extern __shared__ double2 sm[];
-    const uint32_t logC = g.logC, C = 1u << logC;
-    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
-    const uint32_t a0 = blockIdx.x * C;
-    const uint32_t tot = g.N2 << logC;
-    TRACE_BEGIN(3);
-    TSTAMPK(2, 0);
-    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
-    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
-    grid_dep_wait();  // K2's rows
-    // first inverse stage reads the columns straight from global when the per-row chunk is
-    // >= 64 B (C >= 4); with 32 B chunks (C = 2) the staged cp.async copy is faster (round 1:
-    // C4 K3 731 vs 986 us; C5c at C = 4 117 -> 111 us, C3 at C = 8 68 -> 64.5 us)
-    const bool direct = g.f2.S > 1 && C >= 4;
-    if (!direct) {
-        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-            cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
-        cp_async_wait_all();
-    }
-    __syncthreads();
     const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;  // output window [t0, t1)
     // only rows b holding some t in the window: u = a0 + c + N1 b (Re) or u + M (Im)
     auto row_lo = [&](int64_t tmin) -> int64_t {  // first b with a0 + C - 1 + N1 b >= tmin
@@ -510,27 +488,25 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     };
     const int64_t rb0 = row_lo(t0), rb1 = row_hi(t1);
     const int64_t ib0 = row_lo(t0 - (int64_t)g.M), ib1 = row_hi(t1 - (int64_t)g.M);
-    const int64_t b_lo = std::min(rb1 > rb0 ? rb0 : (int64_t)g.N2, ib1 > ib0 ? ib0 : (int64_t)g.N2);
-    const int64_t b_hi = std::max(rb1 > rb0 ? rb1 : 0, ib1 > ib0 ? ib1 : 0);
-    TSTAMPK(2, 1);
-    if (direct) {
-        StageCtx gx;
-        gx.gin = buf + a0;
-        gx.ld = g.N1;
-        stage_any<true, MODE_GCOL>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
-        __syncthreads();
-        dit_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
-    } else {
-        dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
-    }
-    TSTAMPK(2, 2);
-    // epilogue: element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M]
-    const uint32_t lane = threadIdx.x & 31;
+    *blo = std::min(rb1 > rb0 ? rb0 : (int64_t)g.N2, ib1 > ib0 ? ib0 : (int64_t)g.N2);
+    *bhi = std::max(rb1 > rb0 ? rb1 : 0, ib1 > ib0 ? ib1 : 0);
+}
+
+// Window + parity + packing of one column group (threads tid, tid + nth, ...; nth a multiple
+// of 32 and of C).  Element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M].
+// Returns this thread's largest |v - rint v| over window values.
+__device__ __forceinline__ double k3_epilogue(const double2 *sm, const Geometry &g, uint32_t a0, uint32_t logC,
+                                              uint64_t n, uint64_t m, const double2 *thlo, const double2 *thhi,
+                                              uint32_t *out, uint32_t b_lo, uint32_t b_hi, uint32_t tid, uint32_t nth)
+{
+    const uint32_t C = 1u << logC;
+    const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;
+    const uint32_t lane = tid & 31;
     const uint32_t runmask = (C == 32) ? 0xFFFFFFFFu : ((1u << C) - 1u);
     double rmax = 0.0;
-    const uint32_t e_lo = b_hi > b_lo ? (uint32_t)(b_lo << logC) : 0;
-    const uint32_t e_hi = b_hi > b_lo ? (uint32_t)(b_hi << logC) : 0;
-    for (uint32_t e = e_lo + threadIdx.x; e < e_hi; e += blockDim.x) {
+    const uint32_t e_lo = b_hi > b_lo ? (b_lo << logC) : 0;
+    const uint32_t e_hi = b_hi > b_lo ? (b_hi << logC) : 0;
+    for (uint32_t e = e_lo + tid; e < e_hi; e += nth) {
         const uint32_t b = e >> logC, c = e & (C - 1);
         const double2 wv = cmulc(sm[pidx(e)], twiddle(thlo, thhi, b));
         const int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
@@ -560,11 +536,215 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
             }
         }
     }
-    TSTAMPK(2, 3);
+    return rmax;
+}
+
+__device__ __forceinline__ void k3_residual(double rmax, unsigned long long *resid)
+{
 #pragma unroll
     for (int d = 16; d; d >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xFFFFFFFFu, rmax, d));
-    if (lane == 0 && rmax > 0.0) atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
+    if ((threadIdx.x & 31) == 0 && rmax > 0.0) atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
+}
+
+__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
+k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
+               uint32_t *__restrict__ out, unsigned long long *__restrict__ resid, uint64_t out_stride)
+{
+    buf += (uint64_t)blockIdx.y * g.M;                        // batch: key blockIdx.y
+    out += blockIdx.y * out_stride;
+    extern __shared__ double2 sm[];
+    const uint32_t logC = g.logC, C = 1u << logC;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
+    const uint32_t a0 = blockIdx.x * C;
+    const uint32_t tot = g.N2 << logC;
+    TRACE_BEGIN(3);
+    TSTAMPK(2, 0);
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
+    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    grid_dep_wait();  // K2's rows
+    // first inverse stage reads the columns straight from global when the per-row chunk is
+    // >= 64 B (C >= 4); with 32 B chunks (C = 2) the staged cp.async copy is faster (round 1:
+    // C4 K3 731 vs 986 us; C5c at C = 4 117 -> 111 us, C3 at C = 8 68 -> 64.5 us)
+    const bool direct = g.f2.S > 1 && C >= 4;
+    if (!direct) {
+        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
+            cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    int64_t b_lo, b_hi;
+    k3_window_rows(g, a0, C, n, m, &b_lo, &b_hi);
+    TSTAMPK(2, 1);
+    if (direct) {
+        StageCtx gx;
+        gx.gin = buf + a0;
+        gx.ld = g.N1;
+        stage_any<true, MODE_GCOL>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
+        __syncthreads();
+        dit_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+    } else {
+        dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+    }
+    TSTAMPK(2, 2);
+    const double rmax = k3_epilogue(sm, g, a0, logC, n, m, thlo, thhi, out, (uint32_t)b_lo, (uint32_t)b_hi,
+                                    threadIdx.x, blockDim.x);
+    TSTAMPK(2, 3);
+    k3_residual(rmax, resid);
     TRACE_END(3);
+}
+
+// ------------------------------------------------------------------ K3T (TMEM-staged K3)
+// K3 for 32-byte column groups (C = 2) when its grid runs many waves of one CTA per SM (C4,
+// C5d).  There the tile load -- N2 scattered 32-byte row pieces -- is a third of K3's time and
+// nothing overlaps it: shared memory holds one tile.  Tensor memory (256 KB per SM, otherwise
+// idle in this library) holds the next one.  Persistent CTAs (one per SM); warps 0..11 run the
+// inverse stages and the window epilogue of tile t from shared memory while warps 12..15, one
+// per TMEM lane quarter, load tile t + gridDim.x from HBM into TMEM (ld.global -> tcgen05.st);
+// at the switch the compute warps copy TMEM -> shared memory (tcgen05.ld, ~3 k cycles instead
+// of a ~13 k-cycle HBM load).  TMEM layout: lane p holds rows b = p + 128 i, columns
+// [8 i, 8 i + 8) = the row's two complex values (4 words each).
+constexpr uint32_t kK3tCompute = 384;  // compute threads (12 warps); 4 loader warps follow
+
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void cta_sync_tmem()  // barrier ordering tcgen05 traffic across warps
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// loader warps: tile t of the batch into TMEM (8 rows = 16 x 16 B loads in flight per batch)
+__device__ __forceinline__ void k3t_load_tile(const double2 *__restrict__ buf, const Geometry &g, uint32_t t,
+                                              uint32_t ngroups, uint32_t tm)
+{
+    const uint32_t key = t / ngroups, grp = t % ngroups;
+    const double2 *src = buf + (size_t)key * g.M + (size_t)grp * 2;
+    const uint32_t q = (threadIdx.x >> 5) & 3, p = 32 * q + (threadIdx.x & 31);
+    const uint32_t rpl = (g.N2 + 127) / 128;  // rows per lane (planner: <= 64)
+    // registers bound the loads in flight (8 rows per thread, ~32 KB per SM): first pull every
+    // row piece of this lane into L2 (no registers), so the batches below hit L2
+    for (uint32_t i = 0; i < rpl; ++i) {
+        const uint32_t b = p + 128 * i;
+        if (b < g.N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)b * g.N1) : "memory");
+    }
+    for (uint32_t i0 = 0; i0 < rpl; i0 += 8) {
+        double2 v[16];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t b = p + 128 * (i0 + k);
+            if (i0 + k < rpl && b < g.N2) {
+                v[2 * k] = __ldg(src + (size_t)b * g.N1);
+                v[2 * k + 1] = __ldg(src + (size_t)b * g.N1 + 1);
+            } else {
+                v[2 * k] = v[2 * k + 1] = make_double2(0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            if (i0 + 4 * s < rpl) {  // warp-uniform
+                uint32_t r[32];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double2 d = v[8 * s + k];
+                    r[4 * k] = __double2loint(d.x);
+                    r[4 * k + 1] = __double2hiint(d.x);
+                    r[4 * k + 2] = __double2loint(d.y);
+                    r[4 * k + 3] = __double2hiint(d.y);
+                }
+                tm_st32(tm + ((32 * q) << 16) + 8 * (i0 + 4 * s), r);
+            }
+        }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(PA_TMAX, 1)
+k3t_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
+                uint32_t *__restrict__ out, unsigned long long *__restrict__ resid, uint64_t out_stride,
+                uint32_t count)
+{
+    extern __shared__ double2 sm[];
+    __shared__ uint32_t tm_base;
+    constexpr uint32_t C = 2, logC = 1;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t ngroups = g.N1 / C, ntiles = ngroups * count;
+    const bool loader = threadIdx.x >= kK3tCompute;
+    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
+    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tm_base)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    cta_sync_tmem();
+    const uint32_t tm = tm_base;
+    grid_dep_wait();  // K2's rows
+    uint32_t t = blockIdx.x;
+    if (loader && t < ntiles) k3t_load_tile(buf, g, t, ngroups, tm);
+    double rmax = 0.0;
+    const uint32_t rpl = (g.N2 + 127) / 128, nchunk = (rpl + 3) / 4;
+    for (; t < ntiles; t += gridDim.x) {
+        cta_sync_tmem();  // TMEM holds tile t; the shared tile is free
+        if (!loader) {
+            // TMEM -> shared memory: warp w reads lane quarter w & 3, column chunks w >> 2, +3, ..
+            const uint32_t q = warp & 3, p = 32 * q + lane;
+            for (uint32_t ch = warp >> 2; ch < nchunk; ch += 3) {
+                uint32_t r[32];
+                tm_ld32(tm + ((32 * q) << 16) + 32 * ch, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t b = p + 128 * (4 * ch + k);
+                    if (b < g.N2) {
+                        sm[pidx(2 * b)] = make_double2(__hiloint2double(r[8 * k + 1], r[8 * k]),
+                                                       __hiloint2double(r[8 * k + 3], r[8 * k + 2]));
+                        sm[pidx(2 * b + 1)] = make_double2(__hiloint2double(r[8 * k + 5], r[8 * k + 4]),
+                                                           __hiloint2double(r[8 * k + 7], r[8 * k + 6]));
+                    }
+                }
+            }
+        }
+        cta_sync_tmem();  // TMEM consumed, tile t in shared memory
+        if (loader) {
+            if (t + gridDim.x < ntiles) k3t_load_tile(buf, g, t + gridDim.x, ngroups, tm);
+            continue;
+        }
+        const uint32_t key = t / ngroups, a0 = (t % ngroups) * C;
+        StageCtx cx;
+        cx.nth = kK3tCompute;
+        for (int i = g.f2.S - 1; i >= 0; --i) {
+            stage_any<true>(sm, g.f2.st[i], logC, wlo, whi, cx);
+            asm volatile("bar.sync 1, %0;" ::"r"(kK3tCompute) : "memory");
+        }
+        int64_t b_lo, b_hi;
+        k3_window_rows(g, a0, C, n, m, &b_lo, &b_hi);
+        rmax = fmax(rmax, k3_epilogue(sm, g, a0, logC, n, m, thlo, thhi, out + key * out_stride, (uint32_t)b_lo,
+                                      (uint32_t)b_hi, threadIdx.x, kK3tCompute));
+    }
+    if (!loader) k3_residual(rmax, resid);
+    cta_sync_tmem();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
 // ------------------------------------------------------------------ host plan
@@ -745,6 +925,14 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const bool pf = !e || atoi(e) != 0;
         g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
     }
+    // K3T (TMEM-staged K3): opt-in, PA_K3T=1.  Bit-exact, but measured slower than K3 (C4 K3
+    // 723 -> 1019 us): its loader warps keep ~2 k row pieces in flight against K3's 12 k
+    // cp.async (registers bound them; shared memory has no room for staging), see DESIGN.md
+    {
+        const char *e = getenv("PA_K3T");
+        g->k3t = e && atoi(e) == 1 && g->C == 2 && g->t1 == PA_TMAX && g->N2 <= 8192 &&
+                 g->N1 / g->C > 2 * 148u && g->smem1 + 1024 <= kSmemLimit;
+    }
     if (const char *e = getenv("PA_FORCE_T1")) g->t1 = (uint32_t)atoi(e);  // developer overrides
     if (const char *e = getenv("PA_FORCE_T2")) g->t2 = (uint32_t)atoi(e);
     return PA_OK;
@@ -854,7 +1042,9 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         (e = cudaFuncSetAttribute(k2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k3_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess)
+                                  (int)kSmemLimit)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k3t_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
@@ -943,8 +1133,14 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
     launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.spec, g, a.T, 0, 1.0);
     prof_end(h, s);
     prof_begin(h, 2, s);
-    launch_pdl(k3_inv_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf, g, a.T, h->n, h->m, outs,
-               a.resid, out_stride);
+    if (g.k3t) {
+        const uint32_t tiles = (g.N1 / g.C) * count;
+        launch_pdl(k3t_inv_columns, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1, s, a.buf, g, a.T,
+                   h->n, h->m, outs, a.resid, out_stride, count);
+    } else {
+        launch_pdl(k3_inv_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf, g, a.T, h->n, h->m, outs,
+                   a.resid, out_stride);
+    }
     prof_end(h, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "route (a) hash launches");

@@ -619,3 +619,22 @@ def test_auto_split_gigabit_key():
     want = P[n:n + m] ^ P[:m]
     bad = np.flatnonzero(got_ones != want)
     assert bad.size == 0, f"{bad.size} wrong bits, first {bad[:8]}"
+
+
+@pytest.mark.parametrize("name", ["C4", "C5d"])
+def test_tmem_staged_k3_opt_in(name, monkeypatch):
+    """The opt-in TMEM-staged K3 (PA_K3T=1: persistent CTAs, loader warps ld.global ->
+    tcgen05.st, compute warps tcgen05.ld -> shared memory) is bit-exact at the sizes it serves:
+    sampled rows vs the oracle plus the full unit-key closed form."""
+    monkeypatch.setenv("PA_K3T", "1")
+    n, m, sw, kw = syn.config_inputs(name)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        got = from_dev(h.hash(to_dev(kw)), m)
+        j = n // 3
+        unit = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
+        torch.cuda.synchronize()
+        assert h.residual() < 1e-3
+    rows = sample_rows(m, 5)
+    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+    s01 = oracle.unpack(sw, n + m - 1)
+    assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m])
