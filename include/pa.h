@@ -160,7 +160,8 @@ pa_status pa_seed_from_paper_eq1(uint32_t *s_bits, const uint32_t *t_bits, uint6
                                  void *stream);
 
 /* y = T x.  key_bits: device, ceil(n/32) uint32 words; bits >= n are ignored.
- * out_bits: device, ceil(m/32) uint32 words; every bit >= m is written 0.
+ * out_bits: device, ceil(m/32) uint32 words; every bit >= m is written 0.  key_bits and
+ * out_bits must not overlap (PA_ERR_INVALID_ARG): the output is zeroed while the key is read.
  * Deterministic, bit-exact, stream-ordered, asynchronous. */
 pa_status pa_hash(pa_handle h, const uint32_t *key_bits, uint32_t *out_bits, void *stream);
 

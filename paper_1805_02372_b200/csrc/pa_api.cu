@@ -572,6 +572,13 @@ static bool batch_grows(const pa_ctx *h, uint32_t count)
     return h->a.cap < (count < chunk ? count : chunk);
 }
 
+// [a, a + na) and [b, b + nb) bytes overlap?
+static bool overlaps(const void *a, uint64_t na, const void *b, uint64_t nb)
+{
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
 static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                            cudaStream_t s, bool validate)
 {
@@ -581,6 +588,12 @@ static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint
     }
     if (validate) {
         pa_status st;
+        // the output is zeroed before (or while) the key is read: they must not share memory
+        if (overlaps(key, (h->n + 31) / 32 * 4, out, zero_words * 4)) {
+            set_error("key_bits (%p, %llu words) and out_bits (%p, %llu words) overlap", (const void *)key,
+                      (unsigned long long)((h->n + 31) / 32), (void *)out, (unsigned long long)zero_words);
+            return PA_ERR_INVALID_ARG;
+        }
         if (key != h->ok_key) {
             if ((st = check_dev_ptr(key, "key_bits", h->device)) != PA_OK) return st;
             h->ok_key = key;
@@ -641,6 +654,11 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
     if (count == 0) return PA_OK;
     if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
+    if (overlaps(keys, ((uint64_t)(count - 1) * key_stride_words + (h->n + 31) / 32) * 4, outs,
+                 ((uint64_t)(count - 1) * out_stride_words + (h->m + 31) / 32) * 4)) {
+        set_error("keys and outs overlap");
+        return PA_ERR_INVALID_ARG;
+    }
     // growing the work buffers reallocates them: a captured pa_hash_host graph must go
     if (count > 1 && batch_grows(h, count)) drop_host_graph(h);
     return batch_impl(h, keys, key_stride_words, outs, out_stride_words, count, (h->m + 31) / 32,

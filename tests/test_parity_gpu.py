@@ -638,3 +638,39 @@ def test_tmem_staged_k3_opt_in(name, monkeypatch):
     assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
     s01 = oracle.unpack(sw, n + m - 1)
     assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m])
+
+
+def test_key_and_output_must_not_overlap():
+    n, m = 1_000_003, 250_000
+    with pa.Hasher(n, m, to_dev(syn.random_bits(syn.seed_stream(99), n + m - 1))) as h:
+        buf = torch.zeros(pa.words32(n) + 64, dtype=torch.int32, device=DEV)
+        with pytest.raises(pa.PaError) as e:
+            pa.pa_hash(h.handle, buf.data_ptr(), buf[16:].data_ptr(), 0)
+        assert e.value.status == pa.PA_ERR_INVALID_ARG and "overlap" in pa.pa_last_error()
+        keys = torch.zeros((4, (pa.words32(n) + 3) // 4 * 4), dtype=torch.int32, device=DEV)
+        with pytest.raises(pa.PaError):
+            pa.pa_hash_batch(h.handle, keys.data_ptr(), keys.shape[1], keys[1].data_ptr(), keys.shape[1], 2, 0)
+
+
+
+def _fuzz_shapes(count=48, seed=1805):
+    rng = np.random.default_rng(seed)
+    shapes = []
+    for _ in range(count):
+        n = int(np.exp(rng.uniform(0, np.log(3e6))))
+        m = int(rng.integers(1, n + 1)) if rng.random() < 0.8 else max(1, n // int(rng.integers(100, 5000)))
+        shapes.append((n, m))
+    return shapes
+
+
+@pytest.mark.parametrize("n,m", _fuzz_shapes())
+def test_random_shapes_fuzz(n, m):
+    """Seeded random (n, m) across every planner regime (route choice, smooth lengths, N1 x N2
+    splits, column-group widths, direct K1 gather), both routes where route (b) is affordable;
+    full outputs or sampled rows vs the oracle."""
+    sw = syn.random_bits(syn.seed_stream(n % 1000 + 7), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(m % 1000 + 7, 0), n)
+    got, info = check(n, m, sw, kw, "transform")
+    if n * m <= 2e9:
+        got_b, _ = check(n, m, sw, kw, "bitpacked", full=False)
+        assert np.array_equal(got, got_b)
