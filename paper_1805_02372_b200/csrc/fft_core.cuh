@@ -271,9 +271,22 @@ struct StageCtx {
     const double2 *rlo = nullptr, *rhi = nullptr;    // rho^e two-level tables (K2 row)
     double2 *gout = nullptr;                         // K2 row in global memory
     const double2 *gin = nullptr;                    // MODE_TAU_IN / MODE_GCOL: global input
-    uint32_t ld = 0;                                 // MODE_GCOL(_OUT): row pitch in elements
+    uint32_t ld = 0;                                 // MODE_GCOL(_OUT): row(-block) pitch in elements
     uint32_t nth = 0;                                // threads sharing the stage (0 = blockDim.x)
+    // work-array layout (route_a.cu widx): rows in blocks of 2^lr, column groups of 2^lc
+    uint32_t lr = 0, lc = 0;
 };
+
+// MODE_GCOL(_OUT): element (row, c) of a column group at gin/gout + gcol_off
+__device__ __forceinline__ uint64_t gcol_off(const StageCtx &x, uint32_t row, uint32_t c)
+{
+    return (uint64_t)(row >> x.lr) * x.ld + ((row & ((1u << x.lr) - 1)) << x.lc) + c;
+}
+// MODE_TAU_IN / MODE_TAU_OUT: element a of a work-array row at gin/gout + grow_off
+__device__ __forceinline__ uint32_t grow_off(const StageCtx &x, uint32_t a)
+{
+    return ((a >> x.lc) << (x.lc + x.lr)) + (a & ((1u << x.lc) - 1));
+}
 
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
 // in padded shared memory (element idx of sequence c at pidx((idx << logC) + c)).
@@ -298,8 +311,8 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            if (MODE == MODE_TAU_IN && x.gin) v[r] = x.gin[idx0 + r * sd.Ls];
-            else if (MODE == MODE_GCOL) v[r] = x.gin[(uint64_t)(idx0 + r * sd.Ls) * x.ld + c];
+            if (MODE == MODE_TAU_IN && x.gin) v[r] = x.gin[grow_off(x, idx0 + r * sd.Ls)];
+            else if (MODE == MODE_GCOL) v[r] = x.gin[gcol_off(x, idx0 + r * sd.Ls, c)];
             else v[r] = sm[pidx(base + r * stride)];
             if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
         }
@@ -308,9 +321,9 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
         for (int r = 0; r < R; ++r) {
             if (MODE == MODE_TAU_OUT) {
                 const uint32_t idx = idx0 + r * sd.Ls;
-                x.gout[idx] = cmulc(v[r], twiddle(x.rlo, x.rhi, idx));
+                x.gout[grow_off(x, idx)] = cmulc(v[r], twiddle(x.rlo, x.rhi, idx));
             } else if (MODE == MODE_GCOL_OUT) {
-                x.gout[(uint64_t)(idx0 + r * sd.Ls) * x.ld + c] = v[r];
+                x.gout[gcol_off(x, idx0 + r * sd.Ls, c)] = v[r];
             } else {
                 sm[pidx(base + r * stride)] = v[r];
             }

@@ -23,6 +23,7 @@ struct Geometry {
     uint32_t smem1, smem2;  // dynamic shared bytes: K1/K3, K2
     uint32_t kbw;           // K0 bit-stream words per column group
     uint32_t pf2;           // K2: L2 prefetch distance in rows (0 = off)
+    uint32_t lr;            // work array: rows in blocks of 2^lr (route_a.cu wrow / wcol)
     bool k3t;               // K3 as the persistent TMEM-staged k3t_inv_columns (opt-in)
 };
 

@@ -85,6 +85,21 @@ __device__ __forceinline__ unsigned smid()
 // Programmatic dependent launch: the prologue (tables, per-row constants) of a
 // kernel overlaps the tail of the previous one; grid_dep_wait() blocks until the
 // previous grid has completed and its memory is visible.
+// Work-array layout.  Element (row b, column a) of the [N2][N1] array: rows are grouped in
+// blocks of R = 2^lr and columns in groups of C, and an R x C block of a column group is
+// contiguous -- so K1's stores and K3's loads of a C-column group move runs of 16 C R bytes
+// (128 B for C = 2, R = 4) instead of 16 C, while K2's row reads become C-element pieces at a
+// 16 C R-byte stride that the R concurrent CTAs of a row block complete in L2.  lr = 0 is the
+// plain row-major layout.
+__device__ __forceinline__ uint64_t wrow(const Geometry &g, uint32_t b)
+{
+    return (((uint64_t)(b >> g.lr) * g.N1) << g.lr) + ((uint64_t)(b & ((1u << g.lr) - 1)) << g.logC);
+}
+__device__ __forceinline__ uint32_t wcol(const Geometry &g, uint32_t a)
+{
+    return ((a >> g.logC) << (g.logC + g.lr)) + (a & (g.C - 1));
+}
+
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -330,8 +345,10 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
         dif_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
         StageCtx gx;
-        gx.gout = buf + a0;
-        gx.ld = g.N1;
+        gx.gout = buf + ((uint64_t)a0 << g.lr);
+        gx.ld = g.N1 << g.lr;
+        gx.lr = g.lr;
+        gx.lc = logC;
         stage_any<false, MODE_GCOL_OUT>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
         TSTAMPK(0, 4);
     } else {
@@ -339,7 +356,7 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
         grid_dep_launch();  // K2 may start its prologue
         TSTAMPK(0, 4);
         for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-            buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
+            buf[wrow(g, e >> logC) + ((uint64_t)a0 << g.lr) + (e & (C - 1))] = sm[pidx(e)];
     }
     TSTAMPK(0, 5);
     TRACE_END(1);
@@ -396,7 +413,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     buf += (uint64_t)blockIdx.x * g.M;
     TRACE_BEGIN(2);
     TSTAMP(0);
-    double2 *rp = buf + (uint64_t)row * N1;
+    double2 *rp = buf + wrow(g, row);  // element a of the row at rp[wcol(g, a)]
     double2 *sp = spec + (uint64_t)row * N1;
     load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
@@ -406,7 +423,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
     if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + wcol(g, e));
         cp_async_wait_all();
     }
     __syncthreads();
@@ -416,6 +433,8 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     rt.rlo = rlo;
     rt.rhi = rhi;
     rt.gout = rp;
+    rt.lr = g.lr;
+    rt.lc = g.logC;
     if (P.S <= 1) {  // N1 <= 16: tau elementwise, then the single stage below runs plain
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
         __syncthreads();
@@ -447,7 +466,10 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
         // row's compute (multi-wave grids only, see ra_plan; C4 K2 1219 -> 1129 us.  Prefetching
         // the spectrum row as well, or K3's next column group, measured slower)
         const uint32_t q = threadIdx.x;
-        const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
+        // row + pf2 lives in a block of R rows: this CTA takes the block's share of one row
+        const uint32_t nr = row + g.pf2;
+        const char *src = reinterpret_cast<const char *>(
+            buf + (((uint64_t)(nr >> g.lr) * N1) << g.lr) + (uint64_t)(nr & ((1u << g.lr) - 1)) * N1);
         const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
         if (q * chunk < bytes) {
             const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
@@ -460,7 +482,8 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     TSTAMP(4);
     __syncthreads();
     if (P.S == 1) {
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) rp[e] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x)
+            rp[wcol(g, e)] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
         return;
     }
     dit_stages(sm, P, 1, P.S - 1, 0, wlo, whi);
@@ -568,7 +591,7 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     const bool direct = g.f2.S > 1 && C >= 4;
     if (!direct) {
         for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-            cp_async16(sm + pidx(e), buf + (uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1)));
+            cp_async16(sm + pidx(e), buf + wrow(g, e >> logC) + ((uint64_t)a0 << g.lr) + (e & (C - 1)));
         cp_async_wait_all();
     }
     __syncthreads();
@@ -577,8 +600,10 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     TSTAMPK(2, 1);
     if (direct) {
         StageCtx gx;
-        gx.gin = buf + a0;
-        gx.ld = g.N1;
+        gx.gin = buf + ((uint64_t)a0 << g.lr);
+        gx.ld = g.N1 << g.lr;
+        gx.lr = g.lr;
+        gx.lc = logC;
         stage_any<true, MODE_GCOL>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
         __syncthreads();
         dit_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
@@ -638,14 +663,14 @@ __device__ __forceinline__ void k3t_load_tile(const double2 *__restrict__ buf, c
                                               uint32_t ngroups, uint32_t tm)
 {
     const uint32_t key = t / ngroups, grp = t % ngroups;
-    const double2 *src = buf + (size_t)key * g.M + (size_t)grp * 2;
+    const double2 *src = buf + (size_t)key * g.M + ((size_t)grp * 2 << g.lr);
     const uint32_t q = (threadIdx.x >> 5) & 3, p = 32 * q + (threadIdx.x & 31);
     const uint32_t rpl = (g.N2 + 127) / 128;  // rows per lane (planner: <= 64)
     // registers bound the loads in flight (8 rows per thread, ~32 KB per SM): first pull every
     // row piece of this lane into L2 (no registers), so the batches below hit L2
     for (uint32_t i = 0; i < rpl; ++i) {
         const uint32_t b = p + 128 * i;
-        if (b < g.N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)b * g.N1) : "memory");
+        if (b < g.N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + wrow(g, b)) : "memory");
     }
     for (uint32_t i0 = 0; i0 < rpl; i0 += 8) {
         double2 v[16];
@@ -653,8 +678,8 @@ __device__ __forceinline__ void k3t_load_tile(const double2 *__restrict__ buf, c
         for (int k = 0; k < 8; ++k) {
             const uint32_t b = p + 128 * (i0 + k);
             if (i0 + k < rpl && b < g.N2) {
-                v[2 * k] = __ldg(src + (size_t)b * g.N1);
-                v[2 * k + 1] = __ldg(src + (size_t)b * g.N1 + 1);
+                v[2 * k] = __ldg(src + wrow(g, b));
+                v[2 * k + 1] = __ldg(src + wrow(g, b) + 1);
             } else {
                 v[2 * k] = v[2 * k + 1] = make_double2(0.0, 0.0);
             }
@@ -924,6 +949,14 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const char *e = getenv("PA_PF");
         const bool pf = !e || atoi(e) != 0;
         g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
+    }
+    // row blocks (opt-in PA_LR=1): 128-byte runs for 2- and 4-column groups.  Bit-exact, but
+    // K2's rows become 32-byte pieces shared by R CTAs: C4 K1 795 -> 691, K3 732 -> 628, K2
+    // 1130 -> 1295 us (net 0), C5d -2.4%, so row-major stays the default
+    {
+        const char *e = getenv("PA_LR");
+        const uint32_t lr = g->C == 2 ? 2u : g->C == 4 ? 1u : 0u;
+        g->lr = e && atoi(e) == 1 && g->N2 % (1u << lr) == 0 ? lr : 0u;
     }
     // K3T (TMEM-staged K3): opt-in, PA_K3T=1.  Bit-exact, but measured slower than K3 (C4 K3
     // 723 -> 1019 us): its loader warps keep ~2 k row pieces in flight against K3's 12 k

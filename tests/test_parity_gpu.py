@@ -674,3 +674,25 @@ def test_random_shapes_fuzz(n, m):
     if n * m <= 2e9:
         got_b, _ = check(n, m, sw, kw, "bitpacked", full=False)
         assert np.array_equal(got, got_b)
+
+
+@pytest.mark.parametrize("n,m", [(100_000_000, 20_000_000), (16_777_233, 1_677_723), (300_007, 60_001)])
+def test_row_block_layout_opt_in(n, m, monkeypatch):
+    """Opt-in blocked work-array layout (PA_LR=1: R x C blocks of a column group contiguous)
+    through K1/K2/K3 (and the seed path): bit-exact vs the oracle on sampled rows and the
+    full unit-key closed form, with and without the TMEM-staged K3."""
+    monkeypatch.setenv("PA_LR", "1")
+    sw = syn.random_bits(syn.seed_stream(101), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(101, 0), n)
+    s01 = oracle.unpack(sw, n + m - 1)
+    rows = sample_rows(m, 9)
+    for k3t in ("0", "1"):
+        monkeypatch.setenv("PA_K3T", k3t)
+        with pa.Hasher(n, m, to_dev(sw), route="transform") as h:
+            got = from_dev(h.hash(to_dev(kw)), m)
+            j = (2 * n) // 3
+            unit = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
+            torch.cuda.synchronize()
+            assert h.residual() < 1e-3
+        assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows)), k3t
+        assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m]), k3t
