@@ -696,3 +696,52 @@ def test_row_block_layout_opt_in(n, m, monkeypatch):
             assert h.residual() < 1e-3
         assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows)), k3t
         assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m]), k3t
+
+
+def test_no_device_memory_leak_across_handles():
+    """200 create / hash / destroy cycles over both routes, split, workspace-backed and host-path
+    handles return device memory to its starting level (libpa cudaMallocs are all freed)."""
+    shapes = [(4096, 1024, {}), (1_000_003, 250_000, {}), (300_007, 60_001, {"max_transform_len": 200_000}),
+              (65_537, 6_553, {"route": "bitpacked"})]
+    inputs = [(to_dev(syn.random_bits(syn.seed_stream(110 + i), n + m - 1)),
+               to_dev(syn.random_bits(syn.key_stream(110, i), n))) for i, (n, m, _) in enumerate(shapes)]
+    kh = torch.zeros(pa.words32(1_000_003), dtype=torch.int32).pin_memory()
+    oh = torch.zeros(pa.words32(250_000), dtype=torch.int32).pin_memory()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for it in range(50):
+        for i, (n, m, opts) in enumerate(shapes):
+            with pa.Hasher(n, m, inputs[i][0], **opts) as h:
+                h.hash(inputs[i][1])
+                if n == 1_000_003:
+                    h.hash_host(kh, oh)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 <= (4 << 20), (free0, free1)
+
+
+def test_concurrent_handles_on_streams():
+    """Independent handles on separate streams, interleaved, each bit-exact (one hash in flight
+    per handle, several handles in flight at once)."""
+    cases = [(1_000_003, 250_000), (300_007, 30_001), (4096, 1024), (2_000_001, 200_000)]
+    hs, keys, outs, streams, wants = [], [], [], [], []
+    for i, (n, m) in enumerate(cases):
+        sw = syn.random_bits(syn.seed_stream(120 + i), n + m - 1)
+        kw = syn.random_bits(syn.key_stream(120, i), n)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            h = pa.Hasher(n, m, to_dev(sw), stream=s)
+        hs.append(h)
+        keys.append(to_dev(kw))
+        outs.append(h.new_out())
+        streams.append(s)
+        wants.append(oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m) if n * m <= 5e11 else None)
+    torch.cuda.synchronize()
+    for rep in range(5):
+        for h, k, o, s in zip(hs, keys, outs, streams):
+            h.hash(k, o, stream=s)
+    torch.cuda.synchronize()
+    for (n, m), h, o, w in zip(cases, hs, outs, wants):
+        assert np.array_equal(from_dev(o, m), w), (n, m)
+        h.close()
