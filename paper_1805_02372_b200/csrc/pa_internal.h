@@ -23,7 +23,7 @@ struct Geometry {
     uint32_t smem1, smem2;  // dynamic shared bytes: K1/K3, K2
     uint32_t kbw;           // K0 bit-stream words per column group
     uint32_t pf2;           // K2: L2 prefetch distance in rows (0 = off)
-    uint32_t lr;            // work array: rows in blocks of 2^lr (route_a.cu wrow / wcol)
+    uint32_t lr;            // K2 -> K3 array: rows in blocks of 2^lr (route_a.cu wrow / wcol)
     bool k3t;               // K3 as the persistent TMEM-staged k3t_inv_columns (opt-in)
 };
 
@@ -39,7 +39,8 @@ struct RouteA {
     Geometry g;
     char *pblk = nullptr;      // persistent block: spec, tables, rev2, resid
     char *wblk = nullptr;      // work block: buf, kb for `cap` keys
-    double2 *buf = nullptr;    // [N2][N1] working array (also the seed's scratch)
+    double2 *buf = nullptr;    // [N2][N1] working array, row-major (also the seed's scratch)
+    double2 *buf2 = nullptr;   // K2's output for K3: == buf, or the row-block layout (g.lr > 0)
     double2 *spec = nullptr;   // [N2][N1] seed spectrum / M, in K2's position order
     double2 *tables = nullptr; // backing store of T's double2 tables
     RouteTables T{};

@@ -85,12 +85,12 @@ __device__ __forceinline__ unsigned smid()
 // Programmatic dependent launch: the prologue (tables, per-row constants) of a
 // kernel overlaps the tail of the previous one; grid_dep_wait() blocks until the
 // previous grid has completed and its memory is visible.
-// Work-array layout.  Element (row b, column a) of the [N2][N1] array: rows are grouped in
-// blocks of R = 2^lr and columns in groups of C, and an R x C block of a column group is
-// contiguous -- so K1's stores and K3's loads of a C-column group move runs of 16 C R bytes
-// (128 B for C = 2, R = 4) instead of 16 C, while K2's row reads become C-element pieces at a
-// 16 C R-byte stride that the R concurrent CTAs of a row block complete in L2.  lr = 0 is the
-// plain row-major layout.
+// Layout of the array K2 writes and K3 reads (buf2).  Element (row b, column a): rows are
+// grouped in blocks of R = 2^lr and columns in groups of C, and an R x C block of a column
+// group is contiguous -- K3's loads of a C-column group move runs of 16 C R bytes (128 B for
+// C = 2, R = 4) instead of 16 C, while K2 writes its row as C-element pieces at a 16 C R-byte
+// stride (stores do not stall; K2's reads stay row-major in buf: as pieces they measured 15%
+// slower).  lr = 0: plain row-major and buf2 == buf (K2 in place).
 __device__ __forceinline__ uint64_t wrow(const Geometry &g, uint32_t b)
 {
     return (((uint64_t)(b >> g.lr) * g.N1) << g.lr) + ((uint64_t)(b & ((1u << g.lr) - 1)) << g.logC);
@@ -345,10 +345,8 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
         dif_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
         StageCtx gx;
-        gx.gout = buf + ((uint64_t)a0 << g.lr);
-        gx.ld = g.N1 << g.lr;
-        gx.lr = g.lr;
-        gx.lc = logC;
+        gx.gout = buf + a0;
+        gx.ld = g.N1;
         stage_any<false, MODE_GCOL_OUT>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
         TSTAMPK(0, 4);
     } else {
@@ -356,7 +354,7 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
         grid_dep_launch();  // K2 may start its prologue
         TSTAMPK(0, 4);
         for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-            buf[wrow(g, e >> logC) + ((uint64_t)a0 << g.lr) + (e & (C - 1))] = sm[pidx(e)];
+            buf[(uint64_t)(e >> logC) * g.N1 + a0 + (e & (C - 1))] = sm[pidx(e)];
     }
     TSTAMPK(0, 5);
     TRACE_END(1);
@@ -401,8 +399,8 @@ __device__ __forceinline__ void fused_mid_any(const StageDesc &sd, double2 *sm, 
 // mode 0 (hash): in place, buf row -> tau -> DIF, * spec, DIT -> conj tau -> buf row.
 // mode 1 (create): buf row -> tau -> DIF -> * scale -> spec row.
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
-k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, RouteTables T, int mode,
-        double scale)
+k2_rows(double2 *__restrict__ buf, double2 *__restrict__ out2, double2 *__restrict__ spec, Geometry g,
+        RouteTables T, int mode, double scale)
 {
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
@@ -411,9 +409,11 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     // read from HBM once per batch and served from L2 to the other keys
     const uint32_t row = blockIdx.y;
     buf += (uint64_t)blockIdx.x * g.M;
+    out2 += (uint64_t)blockIdx.x * g.M;
     TRACE_BEGIN(2);
     TSTAMP(0);
-    double2 *rp = buf + wrow(g, row);  // element a of the row at rp[wcol(g, a)]
+    double2 *rp = buf + (uint64_t)row * N1;  // input row (row-major)
+    double2 *rq = out2 + wrow(g, row);        // output row: element a at rq[wcol(g, a)]
     double2 *sp = spec + (uint64_t)row * N1;
     load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
@@ -423,7 +423,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
     if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + wcol(g, e));
+        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
         cp_async_wait_all();
     }
     __syncthreads();
@@ -432,9 +432,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     StageCtx rt;
     rt.rlo = rlo;
     rt.rhi = rhi;
-    rt.gout = rp;
-    rt.lr = g.lr;
-    rt.lc = g.logC;
+    rt.gout = rq;
     if (P.S <= 1) {  // N1 <= 16: tau elementwise, then the single stage below runs plain
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
         __syncthreads();
@@ -457,7 +455,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
         return;
     }
     if (P.S == 0) {
-        if (threadIdx.x == 0) rp[0] = cmul(sm[0], sp[0]);
+        if (threadIdx.x == 0) rq[0] = cmul(sm[0], sp[0]);
         return;
     }
     TSTAMP(2);
@@ -466,10 +464,7 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
         // row's compute (multi-wave grids only, see ra_plan; C4 K2 1219 -> 1129 us.  Prefetching
         // the spectrum row as well, or K3's next column group, measured slower)
         const uint32_t q = threadIdx.x;
-        // row + pf2 lives in a block of R rows: this CTA takes the block's share of one row
-        const uint32_t nr = row + g.pf2;
-        const char *src = reinterpret_cast<const char *>(
-            buf + (((uint64_t)(nr >> g.lr) * N1) << g.lr) + (uint64_t)(nr & ((1u << g.lr) - 1)) * N1);
+        const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
         const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
         if (q * chunk < bytes) {
             const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
@@ -483,12 +478,14 @@ k2_rows(double2 *__restrict__ buf, double2 *__restrict__ spec, Geometry g, Route
     __syncthreads();
     if (P.S == 1) {
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x)
-            rp[wcol(g, e)] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
+            rq[wcol(g, e)] = cmulc(sm[pidx(e)], twiddle(rlo, rhi, e));
         return;
     }
     dit_stages(sm, P, 1, P.S - 1, 0, wlo, whi);
     grid_dep_launch();  // K3 may start its prologue
     TSTAMP(5);
+    rt.lr = g.lr;  // the output row in buf2's layout
+    rt.lc = g.logC;
     stage_any<true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
     TSTAMP(6);
     TRACE_END(2);
@@ -950,9 +947,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const bool pf = !e || atoi(e) != 0;
         g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
     }
-    // row blocks (opt-in PA_LR=1): 128-byte runs for 2- and 4-column groups.  Bit-exact, but
-    // K2's rows become 32-byte pieces shared by R CTAs: C4 K1 795 -> 691, K3 732 -> 628, K2
-    // 1130 -> 1295 us (net 0), C5d -2.4%, so row-major stays the default
+    // row blocks for K2's output / K3's input (opt-in PA_LR=1): 128-byte K3 runs for 2- and
+    // 4-column groups.  Bit-exact, but K2's stores become 32-byte pieces: C4 K3 725 -> 627, K2
+    // 1119 -> 1208 us (net 0), C5d -1.8%, so row-major stays the default
     {
         const char *e = getenv("PA_LR");
         const uint32_t lr = g->C == 2 ? 2u : g->C == 4 ? 1u : 0u;
@@ -983,16 +980,20 @@ size_t ra_persist_bytes(const Geometry &g)
 {
     return al256(g.M * sizeof(double2)) + al256(ntables(g) * sizeof(double2)) + al256(g.N2 * 4u) + al256(8);
 }
+// work block: buf [cap][M] | kb [cap][...] | buf2 [cap][M] (only with the row-block layout)
 size_t ra_work_bytes(const Geometry &g, uint32_t cap)
 {
-    return al256((size_t)cap * g.M * sizeof(double2)) + al256((size_t)cap * kb_bytes(g));
+    const size_t b = al256((size_t)cap * g.M * sizeof(double2));
+    return b + al256((size_t)cap * kb_bytes(g)) + (g.lr ? b : 0);
 }
 
 static void carve_work(RouteA &a, char *blk, uint32_t cap)
 {
+    const size_t b = al256((size_t)cap * a.g.M * sizeof(double2));
     a.wblk = blk;
     a.buf = reinterpret_cast<double2 *>(blk);
-    a.kb = reinterpret_cast<uint32_t *>(blk + al256((size_t)cap * a.g.M * sizeof(double2)));
+    a.kb = reinterpret_cast<uint32_t *>(blk + b);
+    a.buf2 = a.g.lr ? reinterpret_cast<double2 *>(blk + b + al256((size_t)cap * kb_bytes(a.g))) : a.buf;
     a.cap = cap;
 }
 
@@ -1082,7 +1083,7 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
     k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
-    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M);
+    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) seed transform launches");
     return PA_OK;
 }
@@ -1163,15 +1164,15 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
                out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
     prof_end(h, s);
     prof_begin(h, 1, s);
-    launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.spec, g, a.T, 0, 1.0);
+    launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf2, a.spec, g, a.T, 0, 1.0);
     prof_end(h, s);
     prof_begin(h, 2, s);
     if (g.k3t) {
         const uint32_t tiles = (g.N1 / g.C) * count;
-        launch_pdl(k3t_inv_columns, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1, s, a.buf, g, a.T,
+        launch_pdl(k3t_inv_columns, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1, s, a.buf2, g, a.T,
                    h->n, h->m, outs, a.resid, out_stride, count);
     } else {
-        launch_pdl(k3_inv_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf, g, a.T, h->n, h->m, outs,
+        launch_pdl(k3_inv_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf2, g, a.T, h->n, h->m, outs,
                    a.resid, out_stride);
     }
     prof_end(h, s);
