@@ -13,23 +13,28 @@
 //    so every transform is a plain complex DFT of length M (no real-to-complex
 //    post-pass), 16 bytes per 2 real points.
 //  * Four-step split M = N1 * N2, u = a + N1 b (a < N1 contiguous), frequency
-//    k = N2 k_a + k_b:
-//      K1  strided pass, C columns per CTA: DIF over b (N2 points) of the
-//          twisted key bits (stage 0 reads the bits directly), the last stage
-//          multiplies by tau(a, k_b) = zeta^a omega_M^{a k_b} and writes the
-//          [N2][N1] work array (row = DIF output position p, k_b = rev2[p]).
-//      K2  row pass, one row per CTA: cp.async row -> smem, DIF over a
-//          (natural -> digit-reversed), [last DIF stage * spectrum * first DIT
-//          stage] fused in registers (the spectrum is stored in the same
-//          digit-reversed order, scaled by 1/M), DIT back to natural order, the
-//          last stage storing straight to global memory (in place).
-//      K3  strided pass: cp.async the C-column tile, first DIT stage multiplies
-//          by conj tau, DIT over k_b -> natural b, the last stage feeds the
-//          epilogue: untwist by conj theta_b = zeta^{-N1 b}, keep t in
-//          [n-1, n+m-1) (Re part = c[u], Im part = c[u+M]), rint, &1,
-//          ballot-pack runs of C bits, atomicOr into the output words; records
-//          max |v - rint(v)| (the PA_ERR_PRECISION tripwire).
-//  * The seed goes through K1 and K2's forward half once at create.
+//    k = N2 k_a + k_b; all kernels launched with programmatic dependent launch:
+//      K0  bit transpose of the key into one bit stream per K1 column group
+//          (skipped when C = 16: K1 then gathers its 2-byte runs itself).
+//      K1  strided pass, C columns per CTA: z = (x_re + i x_im) theta_b
+//          (theta_b = zeta^{N1 b}), DIF over b (N2 points) in shared memory,
+//          stored to the [N2][N1] work array (row = DIF output position p,
+//          k_b = rev2[p]); zeroes the output words.
+//      K2  row pass, one row per CTA: the first DIF stage reads the row from
+//          HBM and multiplies by tau(a, k_b) = rho^a (four-step twiddle and
+//          column twist as one per-row power, tables built at create), DIF over
+//          a, [last DIF stage * spectrum * first DIT stage] fused in registers
+//          (spectrum in the same digit-reversed order, scaled by 1/M), DIT, the
+//          last stage multiplying by conj rho^a and storing to global memory.
+//      K3  strided pass: the C-column tile (cp.async, or read by the first DIT
+//          stage when C >= 4), DIT over k_b -> natural b, then the epilogue:
+//          untwist by conj theta_b, keep t in [n-1, n+m-1) (Re part = c[u], Im
+//          part = c[u+M]), rint, &1, ballot-pack runs of C bits, atomicXor into
+//          the output words; records max |v - rint(v)| (PA_ERR_PRECISION).
+//  * The seed goes through K0, K1 and K2's forward half once at create.
+//  * Opt-in variants (measured): a TMEM-staged persistent K3
+//    (k3t_inv_columns, PA_K3T=1) and a row-block layout of K2's output
+//    (PA_LR=1).
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -44,14 +49,13 @@
 namespace pa {
 namespace {
 
-constexpr uint32_t kSmemLimit = 232448;
+constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 #ifndef PA_TMAX
 #define PA_TMAX 512
 #endif
 #ifndef PA_MINB
 #define PA_MINB 1
 #endif
-  // 227 KB opt-in dynamic shared memory per CTA
 
 #ifdef PA_TIMING
 __device__ unsigned long long g_k2_clk[3][64][16];
