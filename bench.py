@@ -47,10 +47,18 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(syn.CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(syn.CONFIGS),
+                    help="workload (default C2; C4 for --split rows/cols, BASELINE configs[3])")
+    ap.add_argument("--split", default="keys", choices=["keys", "rows", "cols"],
+                    help="N > 1: independent keys per rank (weak scaling, default), or one key split "
+                         "across the ranks by output rows (all-gather) or by key columns (Eq. (4) blocks, "
+                         "XOR reduce-scatter + all-gather) -- strong scaling")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C1/C3/C4 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.config is None:
+        args.config = "C2" if args.split == "keys" else "C4"
+    return args
 
 
 def workload_desc(name):
@@ -192,14 +200,27 @@ def run_ours(args):
     torch.cuda.set_device(dev)
 
     name = args.config
-    n, m, sw, kw = syn.config_inputs(name, key_index=rank)
-    h = pa.Hasher(n, m, dev_words(torch, sw, dev))
-    key = dev_words(torch, kw, dev)
-    out = h.new_out()
+    split = args.split
+    n, m, sw, kw = syn.config_inputs(name, key_index=rank if split == "keys" else 0)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    res = {}
+    if split == "keys":
+        h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+        key = dev_words(torch, kw, dev)
+        out = h.new_out()
+        res["out"] = out
 
-    def step():
-        h.hash(key, out)
+        def step():
+            h.hash(key, out)
+    else:  # one key split across the ranks (paper_1805_02372_b200.dist)
+        from paper_1805_02372_b200 import dist as pd
+        seed_t = dev_words(torch, sw, dev)
+        sh = pd.RowSplit(n, m, seed_t) if split == "rows" else pd.ColSplit(n, m, seed_t)
+        key = dev_words(torch, kw, dev) if split == "rows" else sh.key_block(kw, dev)
+        h = sh.h
+
+        def step():
+            res["out"] = sh(key)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -220,7 +241,7 @@ def run_ours(args):
         import oracle
         rows = np.unique(np.concatenate([np.arange(64), np.arange(m - 64, m),
                                          np.random.default_rng(1).integers(0, m, 256)]))
-        got = oracle.unpack(out.cpu().numpy().view(np.uint32), m)[rows]
+        got = oracle.unpack(res["out"].cpu().numpy().view(np.uint32), m)[rows]
         verified = bool(np.array_equal(got, oracle.toeplitz_rows(n, m, sw, kw, rows)))
 
     # profiled pass: per-kernel CUDA-event times of the same K steps
@@ -233,15 +254,26 @@ def run_ours(args):
     # end to end through the public API with host buffers: every step copies the key from
     # pinned host memory and reads the output back (pa_hash_host_async = one CUDA graph of
     # H2D + kernels + D2H, stream-ordered; the synchronous pa_hash_host is timed too)
-    key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
     out_h = torch.empty(pa.words32(m), dtype=torch.int32).pin_memory()
     e2e_steps = max(3, min(args.steps, 100))
+    if split == "keys":
+        key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
+        e2e_fn = lambda: h.hash_host_async(key_h, out_h)  # noqa: E731
+    else:  # this rank's key words H2D, the sharded hash with its collectives, y D2H
+        key_h = key.cpu().pin_memory()
+
+        def e2e_fn():
+            key.copy_(key_h, non_blocking=True)
+            step()
+            out_h.copy_(res["out"][: out_h.numel()], non_blocking=True)
     for _ in range(3):
-        h.hash_host_async(key_h, out_h)
+        e2e_fn()
     torch.cuda.synchronize()
-    e2e_ms = time_steps(torch, lambda: h.hash_host_async(key_h, out_h), e2e_steps, flush)
-    e2e_ok = bool(np.array_equal(out_h.numpy().view(np.uint32), out.cpu().numpy().view(np.uint32)[:out_h.numel()]))
-    e2e_sync_ms = time_steps(torch, lambda: h.hash_host(key_h, out_h), max(3, min(args.steps, 30)), flush)
+    e2e_ms = time_steps(torch, e2e_fn, e2e_steps, flush)
+    e2e_ok = bool(np.array_equal(out_h.numpy().view(np.uint32),
+                                 res["out"].cpu().numpy().view(np.uint32)[:out_h.numel()]))
+    e2e_sync_ms = (time_steps(torch, lambda: h.hash_host(key_h, out_h), max(3, min(args.steps, 30)), flush)
+                   if split == "keys" else e2e_ms)
 
     # max over ranks
     t = torch.tensor([tot_ms, float(np.mean(e2e_ms)), float(np.mean(e2e_sync_ms))], dtype=torch.float64,
@@ -253,9 +285,9 @@ def run_ours(args):
     line = None
     if rank == 0:
         info = h.info
-        units = world * args.steps
-        value = n * units / (tot_ms * 1e-3) / 1e9
-        e2e_value = n * world / (e2e_mean * 1e-3) / 1e9
+        keys_per_step = world if split == "keys" else 1  # splits: one key across all ranks
+        value = n * keys_per_step * args.steps / (tot_ms * 1e-3) / 1e9
+        e2e_value = n * keys_per_step / (e2e_mean * 1e-3) / 1e9
         # roofline of the dominant kernel
         roof = None
         per = {k: v[1] / max(1, v[0]) for k, v in kern.items()}
@@ -287,26 +319,39 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if info["route"] == 1 else "u32",
+            "scaling": "weak" if split == "keys" else "strong", "vs_baseline": None,
+            "dtype": "f64" if info["route"] == 1 else "u32",
             "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits (SURVEY 8(d) streams)",
-            "config": {"workload": workload_desc(name), "n": n, "m": m, "keys_per_rank": 1,
+            "config": {"workload": workload_desc(name), "n": n, "m": m,
+                       "keys_per_rank": 1 if split == "keys" else 1.0 / world,
                        "route": h.route, "transform_len": info["transform_len"], "n1": info["n1"],
                        "n2": info["n2"], "cols_per_cta": info["cols_per_cta"],
-                       "parallelism": f"independent keys x {world} GPU(s), no data-path collective",
+                       "parallelism": {
+                           "keys": f"independent keys x {world} GPU(s), no data-path collective",
+                           "rows": f"one key, output rows split over {world} GPU(s) (rank 0's share shown), "
+                                   "NCCL all_gather_into_tensor",
+                           "cols": f"one key, Eq. (4) key blocks over {world} GPU(s) (rank 0's share shown), "
+                                   "XOR reduce-scatter (all_to_all_single + pa_xor_fold) + all_gather"}[split],
                        "l2": "flushed before every step (256 MiB memset, untimed)", "verified": verified},
             "roofline": roof,
             "kernels_us": {k: v[1] / max(1, v[0]) * 1e3 for k, v in kern.items()},
             "profiled_ms_per_step": float(np.mean(prof_ms)),
-            "e2e": {"value": e2e_value, "unit": "Gbit/s", "h2d_bytes_per_step": 4 * pa.words32(n),
+            "e2e": {"value": e2e_value, "unit": "Gbit/s", "h2d_bytes_per_step": 4 * key_h.numel(),
                     "d2h_bytes_per_step": 4 * pa.words32(m), "steps": e2e_steps, "verified": e2e_ok,
-                    "how": "pa_hash_host_async per step (CUDA graph: pinned host key -> H2D -> K0..K3 -> "
-                           "D2H to pinned host output), CUDA events around each step, L2 flushed between",
+                    "how": ("pa_hash_host_async per step (CUDA graph: pinned host key -> H2D -> K0..K3 -> "
+                            "D2H to pinned host output), CUDA events around each step, L2 flushed between")
+                    if split == "keys" else
+                    "per step: this rank's key words H2D from pinned memory, the sharded hash and its "
+                    "collectives, y D2H; CUDA events around each step, L2 flushed between",
                     "sync_api_value": n * world / (e2e_sync_mean * 1e-3) / 1e9,
                     "sync_api_how": "pa_hash_host (same, plus a stream synchronisation every step)"},
-            "gpu_launches": args.steps * info["kernels_per_hash"],
+            "gpu_launches": args.steps * (info["kernels_per_hash"] + (1 if split == "cols" and world > 1 else 0)),
             "clocks": clk.result(),
         }
-    h.close()
+    if split == "keys":
+        h.close()
+    else:
+        sh.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -195,3 +195,96 @@ def hash_keys(n: int, m: int, seed_t: torch.Tensor, keys: torch.Tensor, group=No
     if hash_fn is None:
         hf.close()
     return idx, outs
+
+
+# ---------------------------------------------------------------- persistent sharded hashers
+def _world_rank(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+class RowSplit:
+    """Output-row split of one (n, m) hash (BASELINE configs[3], "output rows sharded with NCCL
+    gather"): this rank owns rows row_ranges(m, W)[rank] and keeps a handle on the seed window
+    at offset r0 (n + m_g - 1 bits, P:88-92 per row block); each call hashes the full key
+    (device words, every rank holds it) and one all_gather_into_tensor assembles y.  Per-rank
+    transform >= n + m/W - 1: it barely shrinks."""
+
+    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None):
+        from . import Hasher
+        self.n, self.m, self.group = n, m, group
+        self.world, self.rank = _world_rank(group)
+        self.ranges = row_ranges(m, self.world)
+        r0, r1 = self.ranges[self.rank]
+        self.span = max((b - a + WORD - 1) // WORD for a, b in self.ranges)
+        self.h = Hasher(n, r1 - r0, seed_t, seed_bit_offset=row_seed_offset(r0), allow_wide=True) if r1 > r0 else None
+        dev = seed_t.device
+        self.mine = torch.zeros(self.span, dtype=torch.int32, device=dev)
+        self.gathered = torch.empty(self.world * self.span, dtype=torch.int32, device=dev)
+        self.out = torch.zeros((m + WORD - 1) // WORD, dtype=torch.int32, device=dev)
+
+    def __call__(self, key_t: torch.Tensor) -> torch.Tensor:
+        if self.h is not None:
+            part = self.h.hash(key_t)
+            w = min(self.span, part.numel())
+            self.mine[:w] = part[:w]
+        if self.world == 1:
+            return self.mine[: self.out.numel()]
+        dist.all_gather_into_tensor(self.gathered, self.mine, group=self.group)
+        for g, (a, b) in enumerate(self.ranges):
+            if b > a:
+                wa, wb = a // WORD, (b + WORD - 1) // WORD
+                self.out[wa:wb] = self.gathered[g * self.span: g * self.span + (wb - wa)]
+        return self.out
+
+    def close(self):
+        if self.h is not None:
+            self.h.close()
+
+
+class ColSplit:
+    """Input-column split (the paper's Eq. (4) key blocks, with the Eq. (7) modulo-2
+    merge): this rank owns key bits col_ranges(n, m, W)[rank] -- the layout when each
+    GPU already holds its own decoded key segment -- and keeps a handle on the seed
+    window at offset n - c1.  Each call hashes this rank's key block (device words, see
+    key_block) and merges: XOR reduce-scatter (one all_to_all_single + libpa's pa_xor_fold; NCCL
+    has no XOR op) then one all_gather_into_tensor.  Per-rank transform >= n/W + m - 1."""
+
+    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None):
+        from . import Hasher
+        self.n, self.m, self.group = n, m, group
+        self.world, self.rank = _world_rank(group)
+        self.c0, self.c1 = col_ranges(n, m, self.world)[self.rank]
+        ng = self.c1 - self.c0
+        self.h = Hasher(ng, m, seed_t, seed_bit_offset=col_seed_offset(n, self.c0, self.c1),
+                        allow_wide=m > ng) if ng > 0 else None
+        dev = seed_t.device
+        self.words = (m + WORD - 1) // WORD
+        self.slice_w = ((self.words + self.world - 1) // self.world + 3) // 4 * 4
+        self.mine = torch.zeros(self.world * self.slice_w, dtype=torch.int32, device=dev)
+        self.recv = torch.empty_like(self.mine)
+        self.gathered = torch.empty(self.world * self.slice_w, dtype=torch.int32, device=dev)
+
+    def key_block(self, key_words: np.ndarray, device) -> torch.Tensor:
+        """This rank's key bits [c0, c1) as word-aligned device words (host-side extraction)."""
+        ng = self.c1 - self.c0
+        blk = extract_bits(key_words, self.c0, ng)
+        kt = torch.zeros(_words4(ng), dtype=torch.int32)
+        kt[:blk.size] = torch.from_numpy(blk.view(np.int32))
+        return kt.to(device)
+
+    def __call__(self, key_block_t: torch.Tensor) -> torch.Tensor:
+        if self.h is not None:
+            part = self.h.hash(key_block_t)
+            self.mine[: self.words] = part[: self.words]
+        if self.world == 1:
+            return self.mine[: self.words]
+        dist.all_to_all_single(self.recv, self.mine, group=self.group)
+        myslice = _xor_fold_libpa(self.recv.view(self.world, self.slice_w))
+        dist.all_gather_into_tensor(self.gathered, myslice, group=self.group)
+        return self.gathered[: self.words]
+
+    def close(self):
+        if self.h is not None:
+            self.h.close()

@@ -325,6 +325,15 @@ def test_dist_driver_single_rank_nccl():
         for k in idx:
             wk = oracle.unpack(oracle.toeplitz_words(n, m, sw, syn.random_bits(syn.key_stream(72, k), n)), m)
             assert np.array_equal(from_dev(outs[k], m), wk)
+        # persistent sharded hashers (bench.py --split rows / cols), repeated calls
+        for cls in (pd.RowSplit, pd.ColSplit):
+            sh = cls(n, m, seed_t)
+            k = to_dev(kw) if cls is pd.RowSplit else sh.key_block(kw, DEV)
+            for _ in range(3):
+                y = sh(k)
+            torch.cuda.synchronize()
+            assert np.array_equal(from_dev(y, m), want), cls.__name__
+            sh.close()
     finally:
         dist.destroy_process_group()
 
