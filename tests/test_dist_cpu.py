@@ -90,3 +90,47 @@ def test_range_helpers():
     cr = pd.col_ranges(10, 3, 4)
     assert cr[0][0] == 0 and cr[-1][1] == 10 and sum(b - a for a, b in cr) == 10
     assert pd.col_seed_offset(100, 20, 50) == 50
+
+
+def _corrupt_worker(rank, world, port, n, m, q):
+    """Column split whose rank-1 partial has one flipped bit (SPEC S:475 corrupted-merge hook)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1805_02372_b200 import dist as pd
+        sw = syn.random_bits(syn.seed_stream(79), n + m - 1)
+        kw = syn.random_bits(syn.key_stream(79, 0), n)
+        seed_t = torch.from_numpy(sw.view(np.int32).copy())
+
+        def corrupt(nn, mm, s, off, k):
+            out = oracle_hash(nn, mm, s, off, k)
+            if rank == 1:
+                out[7] ^= 1 << 3  # bit 7 * 32 + 3 of this rank's partial
+            return out
+        cols = pd.hash_cols(n, m, seed_t, kw, hash_fn=corrupt, device=torch.device("cpu"))
+        q.put((rank, cols.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_corrupted_merge_is_detected_at_its_bit():
+    """Fault injection into the Eq. (7) merge: the merged output differs from the oracle at
+    exactly the corrupted bit, on every rank (the XOR merge uses every partial)."""
+    world, n, m = 2, 3001, 700
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_corrupt_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sw = syn.random_bits(syn.seed_stream(79), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(79, 0), n)
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    for rank, cols in res:
+        bad = np.flatnonzero(oracle.unpack(cols.view(np.uint32), m) != want)
+        assert list(bad) == [7 * 32 + 3], (rank, bad[:5])

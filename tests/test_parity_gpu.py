@@ -754,3 +754,43 @@ def test_concurrent_handles_on_streams():
     for (n, m), h, o, w in zip(cases, hs, outs, wants):
         assert np.array_equal(from_dev(o, m), w), (n, m)
         h.close()
+
+
+# ---------------------------------------------------------------- fault injection (SURVEY aux table)
+def test_fault_injection_flipped_output_bit_is_detected():
+    """The parity check is sensitive: one flipped output bit is reported at exactly its row."""
+    n, m = 1_000_003, 250_000
+    sw = syn.random_bits(syn.seed_stream(130), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(130, 0), n)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        out = h.hash(to_dev(kw))
+        torch.cuda.synchronize()
+    words = out.cpu().numpy().view(np.uint32).copy()
+    i = 123_457
+    words[i // 32] ^= np.uint32(1 << (i % 32))
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    bad = np.flatnonzero(oracle.unpack(words, m) != want)
+    assert list(bad) == [i]
+
+
+def test_fault_injection_corrupted_spectrum_trips_precision():
+    """The FP64 tripwire: scribbling over a handle's seed spectrum (reachable here because the
+    workspace is the caller's: spectrum first after the staging block) makes the window values
+    non-integers, and pa_residual reports PA_ERR_PRECISION."""
+    n, m = 1_000_003, 250_000
+    al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    need = pa.workspace_size(n, m, route="transform")
+    ws = torch.zeros(need, dtype=torch.uint8, device=DEV)
+    seed_t = to_dev(syn.random_bits(syn.seed_stream(131), n + m - 1))
+    with pa.Hasher(n, m, seed_t, route="transform", workspace=ws) as h:
+        key = to_dev(syn.random_bits(syn.key_stream(131, 0), n))
+        h.hash(key)
+        assert h.residual() < 1e-3
+        stage = al(4 * pa.words32(n)) + al(4 * pa.words32(m))
+        M = h.info["transform_len"] // 2
+        spec = ws[stage:stage + 16 * M].view(torch.float64)
+        spec.copy_(torch.rand(spec.numel(), dtype=torch.float64, device=DEV) * 1e-6)
+        h.hash(key)
+        with pytest.raises(pa.PaError) as e:
+            h.residual()
+        assert e.value.status == pa.PA_ERR_PRECISION and "residual" in pa.pa_last_error()
