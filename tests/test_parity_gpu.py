@@ -794,3 +794,57 @@ def test_fault_injection_corrupted_spectrum_trips_precision():
         with pytest.raises(pa.PaError) as e:
             h.residual()
         assert e.value.status == pa.PA_ERR_PRECISION and "residual" in pa.pa_last_error()
+
+
+def test_gigabit_under_2gib_budget_and_plan_consistency():
+    """SPEC acceptance criterion 7: a 1 Gbit input (2^30 key bits, m = n/10) amplifies
+    under a 2 GiB device-memory budget via the planner (pa_hash_blocked: row x column blocks of
+    <= 9e7 bits, one handle alive at a time; peak use sampled through NVML, inputs included),
+    sampled rows vs the oracle; and a 64 Mbit prefix hashed through two different plans agrees
+    with the single-transform hash."""
+    import threading
+    import pynvml
+    n = 1 << 30
+    m = n // 10
+    sw = syn.random_bits(syn.seed_stream(140), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(140, 0), n)
+    pynvml.nvmlInit()
+    hnd = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    base = pynvml.nvmlDeviceGetMemoryInfo(hnd).used
+    peak = [base]
+    stop = threading.Event()
+
+    def sample():
+        while not stop.is_set():
+            peak[0] = max(peak[0], pynvml.nvmlDeviceGetMemoryInfo(hnd).used)
+            stop.wait(0.0005)
+    th = threading.Thread(target=sample)
+    th.start()
+    try:
+        seed_t, key_t = to_dev(sw), to_dev(kw)
+        out = torch.zeros(pa.words32(m) + 4, dtype=torch.int32, device=DEV)
+        pa.pa_hash_blocked(n, m, seed_t.data_ptr(), key_t.data_ptr(), out.data_ptr(), 90_000_000, 0)
+        torch.cuda.synchronize()
+    finally:
+        stop.set()
+        th.join()
+    used = peak[0] - base
+    assert used <= 2 * 2**30, f"peak device memory {used / 2**30:.2f} GiB"
+    rows = sample_rows(m, 140, k=256)
+    assert np.array_equal(from_dev(out, m)[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+    del seed_t, key_t, out
+    # 64 Mbit prefix: the same data and seed through two plans and one transform
+    n2 = 1 << 26
+    m2 = n2 // 10
+    sw2, kw2 = sw[: (n2 + m2 - 1 + 63) // 64], kw[: n2 // 64]
+    seed2, key2 = to_dev(sw2), to_dev(kw2)
+    outs = []
+    for lim in (20_000_000, 7_000_001):
+        o = torch.zeros(pa.words32(m2) + 4, dtype=torch.int32, device=DEV)
+        pa.pa_hash_blocked(n2, m2, seed2.data_ptr(), key2.data_ptr(), o.data_ptr(), lim, 0)
+        outs.append(from_dev(o, m2))
+    with pa.Hasher(n2, m2, seed2) as h:
+        outs.append(from_dev(h.hash(key2), m2))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
