@@ -887,7 +887,14 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             // measured: every FFT stage pass (and the load / store / twiddle passes around
             // them) costs ~0.62 cycles per element per SM, largely independent of the radix
             const double M = (double)N1 * N2;
-            const double pass13 = p2.S + 2.0, pass2 = 2.0 * p1.S + 1.0;
+            // radix-16 / 8 stages take one or two rounds per thread; the low radices several and
+            // measured ~25% dearer per pass (C5a: 2304 = [3, 3, 16, 16] rows lose to 4096 = 16^3)
+            auto wsum = [](const FftPlan &p) {
+                double w = 0;
+                for (int i = 0; i < p.S; ++i) w += p.st[i].R >= 8 ? 1.0 : 1.25;
+                return w;
+            };
+            const double pass13 = p2.S + 2.0, pass2 = 2.0 * wsum(p1) + 1.0;
             const double cfac = C == 1 ? 1.5 : C == 2 ? 1.0 : 0.95;  // short HBM runs (K1/K3)
             const uint32_t occ13 = std::min<uint32_t>(2, kSmemLimit / s13);
             const uint32_t occ2 = std::min<uint32_t>(2, kSmemLimit / smem_k2(N1, p1));
@@ -896,7 +903,10 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
                 double waves = std::ceil(ctas / (148.0 * occ));
                 return std::max(thr, waves * passes * 1.3e-6) + 2e-6;
             };
-            double cost = 2 * ktime(pass13, cfac, occ13, (double)(N1 / C)) + ktime(pass2, 1.0, occ2, (double)N2);
+            // two CTAs per SM overlap one tile's HBM phases with the other's compute (measured:
+            // C3 at C = 4, 2 per SM, 192 us vs C = 8, 1 per SM, 206 us -- same waves)
+            const double ov13 = occ13 >= 2 ? 0.92 : 1.0, ov2 = occ2 >= 2 ? 0.92 : 1.0;
+            double cost = 2 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C)) + ktime(pass2, ov2, occ2, (double)N2);
             if (cost < best) {
                 best = cost;
                 found = true;
