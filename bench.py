@@ -389,6 +389,20 @@ def sweep(torch, pa, dev, steps=10):
         res[name + "_batched"] = {"n": n, "m": m, "keys": count, "ms_per_key": t,
                                   "gbit_s": n / (t * 1e-3) / 1e9, "transform_len": h.info["transform_len"]}
         h.close()
+    # the same C5a batch end to end from pinned host memory (pa_hash_host_batch: one H2D, one
+    # batched hash, one D2H, synchronised)
+    n, m, sw, kw = syn.config_inputs("C5a")
+    count = 256
+    h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+    kw32 = (n + 31) // 32
+    kh = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32)[:kw32].copy()).repeat(count, 1).pin_memory()
+    oh = torch.empty((count, pa.words32(m)), dtype=torch.int32).pin_memory()
+    h.hash_host_batch(kh, oh)
+    ms = time_steps(torch, lambda: h.hash_host_batch(kh, oh), 3, flush)
+    t = float(np.mean(ms)) / count
+    res["C5a_batched_e2e"] = {"n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
+                              "note": "pa_hash_host_batch: pinned host keys in, host outputs out"}
+    h.close()
     # C1 throughput: 2^16 keys against one seed, route (b) batched on the grid
     n, m, sw, kw = syn.config_inputs("C1")
     count = 1 << 16

@@ -24,7 +24,8 @@ from ._lib import (PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISI
                    PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
                    pa_get_info, pa_hash, pa_hash_batch, pa_hash_blocked, pa_hash_host, pa_hash_host_async, pa_hash_u64, pa_last_error,
                    pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_set_seed, pa_xor_fold, pa_residual, pa_status_string,
-                   pa_version, pa_workspace_size, pa_create_ws, pa_hash_fresh_batch, pa_seed_from_paper_eq1)
+                   pa_version, pa_workspace_size, pa_create_ws, pa_hash_fresh_batch, pa_seed_from_paper_eq1,
+                   pa_hash_host_batch)
 
 ROUTES = {"auto": PA_ROUTE_AUTO, "transform": PA_ROUTE_TRANSFORM, "bitpacked": PA_ROUTE_BITPACKED}
 
@@ -175,6 +176,21 @@ class Hasher:
             pa_hash_fresh_batch(self._h, seeds.data_ptr(), st[0], keys.data_ptr(), st[1], outs.data_ptr(), st[2],
                                 count, _stream_ptr(stream))
         return outs
+
+    def hash_host_batch(self, keys_host: torch.Tensor, outs_host: torch.Tensor, stream=None) -> torch.Tensor:
+        """Host (pinned) keys (count, words) in, host outputs (count, words) out, one transfer each
+        way and one batched hash (pa_hash_host_batch)."""
+        if keys_host.is_cuda or outs_host.is_cuda or keys_host.dim() != 2 or outs_host.dim() != 2:
+            raise ValueError("hash_host_batch takes 2-D CPU tensors (count, words)")
+        count = keys_host.shape[0]
+        if outs_host.shape[0] < count or keys_host.stride(1) != 1 or outs_host.stride(1) != 1:
+            raise ValueError("outs_host needs a row per key; rows must be contiguous")
+        ks = keys_host.stride(0) * keys_host.element_size() // 4
+        os_ = outs_host.stride(0) * outs_host.element_size() // 4
+        with torch.cuda.device(self.device):
+            pa_hash_host_batch(self._h, keys_host.data_ptr(), ks, outs_host.data_ptr(), os_, count,
+                               _stream_ptr(stream))
+        return outs_host
 
     def set_seed(self, seed: torch.Tensor, stream=None) -> None:
         """Fresh seed for the next hashes (pa_set_seed; same n, m, seed_bit_offset)."""

@@ -33,7 +33,8 @@ EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
             "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked",
-            "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1"]
+            "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1",
+            "pa_hash_host_batch"]
 
 
 class PaError(RuntimeError):
@@ -79,6 +80,7 @@ _sig = {
     "pa_hash_batch": (_st, [_H, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
     "pa_hash_host": (_st, [_H, _p, _p, _p]),
     "pa_hash_host_async": (_st, [_H, _p, _p, _p]),
+    "pa_hash_host_batch": (_st, [_H, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
     "pa_hash_blocked": (_st, [_u64, _u64, _p, _p, _p, _u64, _p]),
     "pa_create_u64": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, _p]),
     "pa_hash_u64": (_st, [_H, _p, _p, _p]),
@@ -240,3 +242,9 @@ def pa_hash_fresh_batch(h: int, seeds_ptr: int, seed_stride_words: int, keys_ptr
 
 def pa_seed_from_paper_eq1(s_ptr: int, t_ptr: int, n: int, m: int, stream: int = 0) -> None:
     _check(_lib.pa_seed_from_paper_eq1(s_ptr, t_ptr, n, m, stream))
+
+
+def pa_hash_host_batch(h: int, keys_host_ptr: int, key_stride_words: int, outs_host_ptr: int,
+                       out_stride_words: int, count: int, stream: int = 0) -> None:
+    _check(_lib.pa_hash_host_batch(h, keys_host_ptr, key_stride_words, outs_host_ptr, out_stride_words, count,
+                                   stream))

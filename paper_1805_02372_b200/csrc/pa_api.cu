@@ -215,6 +215,7 @@ static void destroy_ctx(pa_ctx *h)
     ra_destroy(h);
     rb_destroy(h);
     dev_free(h, h->stage_blk);
+    if (h->bstage) cudaFree(h->bstage);
     if (h->own_arena) delete h->arena;
     delete h;
 }
@@ -802,6 +803,63 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
         if ((e = cudaGraphLaunch(h->host_exec, s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host graph launch");
     }
     if (sync && (e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host sync");
+    return PA_OK;
+}
+
+pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t key_stride_words,
+                             uint32_t *outs_host, uint64_t out_stride_words, uint32_t count, void *stream)
+{
+    if (!h || !keys_host || !outs_host) {
+        set_error("pa_hash_host_batch: NULL argument");
+        return PA_ERR_INVALID_ARG;
+    }
+    const uint64_t kw = (h->n + 31) / 32, ow = (h->m + 31) / 32;
+    if (key_stride_words < kw || out_stride_words < ow) {
+        set_error("pa_hash_host_batch: key_stride_words = %llu (need >= %llu), out_stride_words = %llu (need >= "
+                  "%llu)", (unsigned long long)key_stride_words, (unsigned long long)kw,
+                  (unsigned long long)out_stride_words, (unsigned long long)ow);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (count == 0) return PA_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->arena) {  // a workspace handle allocates nothing more: one key at a time
+        for (uint32_t k = 0; k < count; ++k) {
+            pa_status st = hash_host_impl(h, keys_host + k * key_stride_words, outs_host + k * out_stride_words,
+                                          stream, k + 1 == count);
+            if (st != PA_OK) return st;
+        }
+        return PA_OK;
+    }
+    const uint64_t kw4 = (kw + 3) / 4 * 4, ow4 = (ow + 3) / 4 * 4;
+    const size_t need = (size_t)count * (kw4 + ow4) * 4;
+    cudaError_t e;
+    if (need > h->bstage_bytes) {
+        if (h->bstage) {
+            cudaStreamSynchronize(s);
+            cudaFree(h->bstage);
+            h->bstage = nullptr;
+            h->bstage_bytes = 0;
+        }
+        if ((e = cudaMalloc(&h->bstage, need)) != cudaSuccess) {
+            h->bstage = nullptr;
+            cudaGetLastError();
+            set_error("pa_hash_host_batch: staging of %llu bytes: %s", (unsigned long long)need,
+                      cudaGetErrorString(e));
+            return PA_ERR_NOMEM;
+        }
+        h->bstage_bytes = need;
+    }
+    if (count > 1 && batch_grows(h, count)) drop_host_graph(h);  // work buffers are about to move
+    uint32_t *dk = (uint32_t *)h->bstage, *dout = dk + (size_t)count * kw4;
+    if ((e = cudaMemcpy2DAsync(dk, kw4 * 4, keys_host, key_stride_words * 4, kw * 4, count,
+                               cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "pa_hash_host_batch H2D");
+    pa_status st = batch_impl(h, dk, kw4, dout, ow4, count, ow, s);
+    if (st != PA_OK) return st;
+    if ((e = cudaMemcpy2DAsync(outs_host, out_stride_words * 4, dout, ow4 * 4, ow * 4, count,
+                               cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "pa_hash_host_batch D2H");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host_batch sync");
     return PA_OK;
 }
 

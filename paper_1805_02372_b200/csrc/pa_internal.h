@@ -97,6 +97,9 @@ struct pa_ctx {
     // staging for pa_hash_host (one block: key words, then output words)
     char *stage_blk = nullptr;
     uint32_t *stage_key = nullptr, *stage_out = nullptr;
+    // staging for pa_hash_host_batch (cudaMalloc, grown on demand; never in a workspace)
+    char *bstage = nullptr;
+    size_t bstage_bytes = 0;
     // device memory: the caller's workspace (nullptr: cudaMalloc)
     pa::Arena *arena = nullptr;
     bool own_arena = false;

@@ -848,3 +848,24 @@ def test_gigabit_under_2gib_budget_and_plan_consistency():
     with pa.Hasher(n2, m2, seed2) as h:
         outs.append(from_dev(h.hash(key2), m2))
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("n,m,count,kwargs", [(1_048_576, 104_857, 64, {}), (4096, 1024, 500, {}),
+                                              (300_007, 60_001, 5, {"max_transform_len": 200_000})])
+def test_hash_host_batch(n, m, count, kwargs):
+    """pa_hash_host_batch: pinned host keys (strided rows) -> one H2D, one batched hash, one D2H;
+    every output vs the oracle (sampled for the 500-key case), tail bits zero."""
+    sw = syn.random_bits(syn.seed_stream(150), n + m - 1)
+    kw32 = pa.words32(n)
+    rng = np.random.default_rng(150)
+    keys = rng.integers(0, 2**32, (count, kw32 + 3), dtype=np.uint64).astype(np.uint32)
+    kh = torch.from_numpy(keys.view(np.int32)).pin_memory()
+    oh = torch.full((count, pa.words32(m) + 5), -1, dtype=torch.int32).pin_memory()
+    with pa.Hasher(n, m, to_dev(sw), **kwargs) as h:
+        h.hash_host_batch(kh, oh)
+    got = oh.numpy().view(np.uint32)
+    check_k = range(count) if count <= 64 else np.unique(np.r_[0, count - 1, rng.integers(0, count, 40)])
+    for k in check_k:
+        want = oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[k, :kw32].copy()), m)
+        assert np.array_equal(oracle.unpack(got[k], m), want), k
+        assert not oracle.unpack(got[k][: pa.words32(m)], 32 * pa.words32(m))[m:].any()
