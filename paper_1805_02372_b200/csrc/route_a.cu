@@ -403,9 +403,10 @@ __device__ __forceinline__ void fused_mid_any(const StageDesc &sd, double2 *sm, 
 // mode 0 (hash): in place, buf row -> tau -> DIF, * spec, DIT -> conj tau -> buf row.
 // mode 1 (create): buf row -> tau -> DIF -> * scale -> spec row.
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
-k2_rows(double2 *__restrict__ buf, double2 *__restrict__ out2, double2 *__restrict__ spec, Geometry g,
-        RouteTables T, int mode, double scale)
+k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, RouteTables T, int mode,
+        double scale)
 {
+    // buf and out2 may be the same array (K2 in place when lr = 0): no __restrict__ on them
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
     double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi + g.f1.ntw, *rhi = rlo + 64;
