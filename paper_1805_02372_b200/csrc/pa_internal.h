@@ -25,6 +25,7 @@ struct Geometry {
     uint32_t pf2;           // K2: L2 prefetch distance in rows (0 = off)
     uint32_t lr;            // K2 -> K3 array: rows in blocks of 2^lr (route_a.cu wrow / wcol)
     bool k3t;               // K3 as the persistent TMEM-staged k3t_inv_columns (opt-in)
+    bool k2r16;             // K2 as k2_rows16 (all row stages radix 16)
 };
 
 struct RouteTables {

@@ -496,6 +496,63 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     TRACE_END(2);
 }
 
+// ------------------------------------------------------------------ K2 for radix-16 rows
+// The hash path of k2_rows for row plans made only of radix-16 stages (N1 = 4096: C2, C3, C5),
+// calling the radix-16 stage routines directly: the general kernel's radix switch instantiates
+// every radix and mode, and K2's speed at these sizes is sensitive to its code.
+__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
+k2_rows16(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T)
+{
+    extern __shared__ double2 sm[];
+    const uint32_t N1 = g.N1;
+    double2 *wlo = sm + g.tile2, *whi = wlo + 64, *rlo = whi + g.f1.nhi + g.f1.ntw, *rhi = rlo + 64;
+    const uint32_t row = blockIdx.y;
+    buf += (uint64_t)blockIdx.x * g.M;
+    out2 += (uint64_t)blockIdx.x * g.M;
+    double2 *rp = buf + (uint64_t)row * N1;
+    double2 *rq = out2 + wrow(g, row);
+    const double2 *sp = spec + (uint64_t)row * N1;
+    load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
+    {
+        const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
+        load_tables(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
+    }
+    grid_dep_wait();  // K1's work array
+    __syncthreads();
+    const FftPlan &P = g.f1;
+    StageCtx rt;
+    rt.rlo = rlo;
+    rt.rhi = rhi;
+    rt.gin = rp;
+    stage_smem<16, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
+    __syncthreads();
+    if (g.pf2 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
+        const uint32_t q = threadIdx.x;
+        const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
+        const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
+        if (q * chunk < bytes) {
+            const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)q * chunk), "r"(sz) : "memory");
+        }
+    }
+    for (int i = 1; i < P.S - 1; ++i) {
+        stage_smem<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
+        __syncthreads();
+    }
+    fused_mid<16>(P.st[P.S - 1], sm, sp);
+    __syncthreads();
+    for (int i = P.S - 2; i >= 1; --i) {
+        stage_smem<16, true, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
+        __syncthreads();
+    }
+    grid_dep_launch();  // K3 may start its prologue
+    rt.gin = nullptr;
+    rt.gout = rq;
+    rt.lr = g.lr;
+    rt.lc = g.logC;
+    stage_smem<16, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+}
+
 // ------------------------------------------------------------------ K3
 // Rows b of column group a0 that hold output-window bits: [b_lo, b_hi).
 __device__ __forceinline__ void k3_window_rows(const Geometry &g, uint32_t a0, uint32_t C, uint64_t n, uint64_t m,
@@ -962,6 +1019,13 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const bool pf = !e || atoi(e) != 0;
         g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
     }
+    // K2 specialised for all-radix-16 row plans (developer override PA_K2_16=0)
+    {
+        const char *e = getenv("PA_K2_16");
+        bool all16 = g->f1.S >= 2;
+        for (int i = 0; i < g->f1.S; ++i) all16 = all16 && g->f1.st[i].R == 16;
+        g->k2r16 = (!e || atoi(e) != 0) && all16;
+    }
     // row blocks for K2's output / K3's input (opt-in PA_LR=1): 128-byte K3 runs for 2- and
     // 4-column groups.  Bit-exact, but K2's stores become 32-byte pieces: C4 K3 725 -> 627, K2
     // 1119 -> 1208 us (net 0), C5d -1.8%, so row-major stays the default
@@ -1092,6 +1156,8 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k3_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k2_rows16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k3t_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
@@ -1179,7 +1245,10 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
                out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
     prof_end(h, s);
     prof_begin(h, 1, s);
-    launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf2, a.spec, g, a.T, 0, 1.0);
+    if (g.k2r16)
+        launch_pdl(k2_rows16, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf2, (const double2 *)a.spec, g, a.T);
+    else
+        launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf2, a.spec, g, a.T, 0, 1.0);
     prof_end(h, s);
     prof_begin(h, 2, s);
     if (g.k3t) {
