@@ -496,12 +496,14 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     TRACE_END(2);
 }
 
-// ------------------------------------------------------------------ K2 for radix-16 rows
-// The hash path of k2_rows for row plans made only of radix-16 stages (N1 = 4096: C2, C3, C5),
-// calling the radix-16 stage routines directly: the general kernel's radix switch instantiates
-// every radix and mode, and K2's speed at these sizes is sensitive to its code.
+// ------------------------------------------------------------------ K2 for fixed radix shapes
+// The hash path of k2_rows for row plans [R0, R1, 16, ..., 16] (S >= 3): 4096 = [16, 16, 16]
+// (C2, C3, C5), 10240 = [5, 8, 16, 16] (C4, C5d), 6144 = [3, 8, 16, 16], 7168 = [7, 4, 16, 16],
+// calling those stage routines directly: the general kernel's radix switch instantiates every
+// radix and mode, and K2's speed is sensitive to its code.
+template <int R0, int R1>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
-k2_rows16(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T)
+k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T)
 {
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
@@ -524,7 +526,7 @@ k2_rows16(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     rt.rlo = rlo;
     rt.rhi = rhi;
     rt.gin = rp;
-    stage_smem<16, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
+    stage_smem<R0, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
     __syncthreads();
     if (g.pf2 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
         const uint32_t q = threadIdx.x;
@@ -535,22 +537,36 @@ k2_rows16(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)q * chunk), "r"(sz) : "memory");
         }
     }
-    for (int i = 1; i < P.S - 1; ++i) {
+    stage_smem<R1, false, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
+    __syncthreads();
+    for (int i = 2; i < P.S - 1; ++i) {
         stage_smem<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
     fused_mid<16>(P.st[P.S - 1], sm, sp);
     __syncthreads();
-    for (int i = P.S - 2; i >= 1; --i) {
+    for (int i = P.S - 2; i >= 2; --i) {
         stage_smem<16, true, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
+    stage_smem<R1, true, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
+    __syncthreads();
     grid_dep_launch();  // K3 may start its prologue
     rt.gin = nullptr;
     rt.gout = rq;
     rt.lr = g.lr;
     rt.lc = g.logC;
-    stage_smem<16, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+    stage_smem<R0, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+}
+
+// the shapes k2_rows_t is instantiated for (g.k2shape: 0 = general k2_rows)
+static int k2_shape(const FftPlan &p)
+{
+    if (p.S < 3) return 0;
+    for (int i = 2; i < p.S; ++i)
+        if (p.st[i].R != 16) return 0;
+    const uint32_t a = p.st[0].R, b = p.st[1].R;
+    return a == 16 && b == 16 ? 1 : a == 5 && b == 8 ? 2 : a == 3 && b == 8 ? 3 : a == 7 && b == 4 ? 4 : 0;
 }
 
 // ------------------------------------------------------------------ K3
@@ -1019,12 +1035,10 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const bool pf = !e || atoi(e) != 0;
         g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
     }
-    // K2 specialised for all-radix-16 row plans (developer override PA_K2_16=0)
+    // K2 specialised for the common row-plan shapes (developer override PA_K2_T=0)
     {
-        const char *e = getenv("PA_K2_16");
-        bool all16 = g->f1.S >= 2;
-        for (int i = 0; i < g->f1.S; ++i) all16 = all16 && g->f1.st[i].R == 16;
-        g->k2r16 = (!e || atoi(e) != 0) && all16;
+        const char *e = getenv("PA_K2_T");
+        g->k2shape = (!e || atoi(e) != 0) ? k2_shape(g->f1) : 0;
     }
     // row blocks for K2's output / K3's input (opt-in PA_LR=1): 128-byte K3 runs for 2- and
     // 4-column groups.  Bit-exact, but K2's stores become 32-byte pieces: C4 K3 725 -> 627, K2
@@ -1156,7 +1170,13 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k3_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (e = cudaFuncSetAttribute(k2_rows_t<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemLimit)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k2_rows_t<5, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemLimit)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k2_rows_t<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemLimit)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k2_rows_t<7, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k3t_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
@@ -1245,10 +1265,17 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
                out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
     prof_end(h, s);
     prof_begin(h, 1, s);
-    if (g.k2r16)
-        launch_pdl(k2_rows16, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf2, (const double2 *)a.spec, g, a.T);
-    else
-        launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf2, a.spec, g, a.T, 0, 1.0);
+    {
+        const dim3 g2(count, g.N2);
+        const double2 *sp = a.spec;
+        switch (g.k2shape) {
+        case 1: launch_pdl(k2_rows_t<16, 16>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
+        case 2: launch_pdl(k2_rows_t<5, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
+        case 3: launch_pdl(k2_rows_t<3, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
+        case 4: launch_pdl(k2_rows_t<7, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
+        default: launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, a.spec, g, a.T, 0, 1.0);
+        }
+    }
     prof_end(h, s);
     prof_begin(h, 2, s);
     if (g.k3t) {
