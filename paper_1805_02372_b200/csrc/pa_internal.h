@@ -26,6 +26,7 @@ struct Geometry {
     uint32_t lr;            // K2 -> K3 array: rows in blocks of 2^lr (route_a.cu wrow / wcol)
     bool k3t;               // K3 as the persistent TMEM-staged k3t_inv_columns (opt-in)
     int k2shape;            // K2 as k2_rows_t<R0, R1> (1: 16,16  2: 5,8  3: 3,8  4: 7,4), 0: k2_rows
+    int k13;                // K1/K3 instantiation (route_a.cu kK13), 0: general
 };
 
 struct RouteTables {

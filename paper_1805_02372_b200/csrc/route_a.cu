@@ -283,6 +283,39 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
 
 // ------------------------------------------------------------------ K1
 // Column DIF of C adjacent columns; input = this group's bit stream from K0.
+// Column-pass stage dispatch for plans [A, B, (C), 16, ...] known at compile time (A = 0: the
+// general radix switch).  Instantiating only the radices a plan uses keeps K1/K3's code small,
+// which measurably matters (k2_rows_t).
+template <bool INV, int MODE, int A, int B, int C>
+__device__ __forceinline__ void stage_t(double2 *sm, const FftPlan &P, int i, uint32_t logC, const double2 *wlo,
+                                        const double2 *whi, const StageCtx &x = StageCtx{})
+{
+    if (A == 0) stage_any<INV, MODE>(sm, P.st[i], logC, wlo, whi, x);
+    else if (i == 0) stage_smem<A ? A : 16, INV, MODE>(sm, P.st[0], logC, wlo, whi, x);
+    else if (i == 1) stage_smem<B ? B : 16, INV, MODE>(sm, P.st[1], logC, wlo, whi, x);
+    else if (i == 2 && C) stage_smem<C ? C : 16, INV, MODE>(sm, P.st[2], logC, wlo, whi, x);
+    else stage_smem<16, INV, MODE>(sm, P.st[i], logC, wlo, whi, x);
+}
+template <int A, int B, int C>
+__device__ __forceinline__ void dif_t(double2 *sm, const FftPlan &P, int i0, int i1, uint32_t logC,
+                                      const double2 *wlo, const double2 *whi)
+{
+    for (int i = i0; i < i1; ++i) {
+        stage_t<false, MODE_PLAIN, A, B, C>(sm, P, i, logC, wlo, whi);
+        __syncthreads();
+    }
+}
+template <int A, int B, int C>
+__device__ __forceinline__ void dit_t(double2 *sm, const FftPlan &P, int i0, int i1, uint32_t logC,
+                                      const double2 *wlo, const double2 *whi)
+{
+    for (int i = i1 - 1; i >= i0; --i) {
+        stage_t<true, MODE_PLAIN, A, B, C>(sm, P, i, logC, wlo, whi);
+        __syncthreads();
+    }
+}
+
+template <int RA, int RB, int RC>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
                uint32_t *__restrict__ zero_out, uint64_t zero_words, uint64_t out_stride,
@@ -346,15 +379,15 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     // stage writes it straight to global when the per-row chunk is >= 64 B (see K3)
     const bool direct = g.f2.S > 1 && C >= 4;
     if (direct) {
-        dif_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+        dif_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
         StageCtx gx;
         gx.gout = buf + a0;
         gx.ld = g.N1;
-        stage_any<false, MODE_GCOL_OUT>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
+        stage_t<false, MODE_GCOL_OUT, RA, RB, RC>(sm, g.f2, g.f2.S - 1, logC, wlo, whi, gx);
         TSTAMPK(0, 4);
     } else {
-        dif_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+        dif_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
         TSTAMPK(0, 4);
         for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
@@ -569,6 +602,7 @@ static int k2_shape(const FftPlan &p)
     return a == 16 && b == 16 ? 1 : a == 5 && b == 8 ? 2 : a == 3 && b == 8 ? 3 : a == 7 && b == 4 ? 4 : 0;
 }
 
+
 // ------------------------------------------------------------------ K3
 // Rows b of column group a0 that hold output-window bits: [b_lo, b_hi).
 __device__ __forceinline__ void k3_window_rows(const Geometry &g, uint32_t a0, uint32_t C, uint64_t n, uint64_t m,
@@ -644,6 +678,7 @@ __device__ __forceinline__ void k3_residual(double rmax, unsigned long long *res
     if ((threadIdx.x & 31) == 0 && rmax > 0.0) atomicMax(resid, (unsigned long long)__double_as_longlong(rmax));
 }
 
+template <int RA, int RB, int RC>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint64_t n, uint64_t m,
                uint32_t *__restrict__ out, unsigned long long *__restrict__ resid, uint64_t out_stride)
@@ -679,11 +714,11 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
         gx.ld = g.N1 << g.lr;
         gx.lr = g.lr;
         gx.lc = logC;
-        stage_any<true, MODE_GCOL>(sm, g.f2.st[g.f2.S - 1], logC, wlo, whi, gx);
+        stage_t<true, MODE_GCOL, RA, RB, RC>(sm, g.f2, g.f2.S - 1, logC, wlo, whi, gx);
         __syncthreads();
-        dit_stages(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+        dit_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
     } else {
-        dit_stages(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+        dit_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
     }
     TSTAMPK(2, 2);
     const double rmax = k3_epilogue(sm, g, a0, logC, n, m, thlo, thhi, out, (uint32_t)b_lo, (uint32_t)b_hi,
@@ -845,6 +880,41 @@ k3t_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint
     if (!loader) k3_residual(rmax, resid);
     cta_sync_tmem();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
+// K1 / K3 instantiations for column plans [A, B, (C), 16, ...]: 0 general, then C2 [5, 2, 16],
+// C3 [7, 3, 4, 16], C4 [3, 8, 16, 16], C5a/c [3, 3, 16(, 16)], C5b [7, 4, 16], C5d [7, 3, 8, 16]
+using K1Fn = void (*)(const uint32_t *, double2 *, Geometry, RouteTables, uint32_t *, uint64_t, uint64_t,
+                      const uint32_t *, uint64_t, uint64_t);
+using K3Fn = void (*)(const double2 *, Geometry, RouteTables, uint64_t, uint64_t, uint32_t *, unsigned long long *,
+                      uint64_t);
+struct K13 {
+    int a, b, c;
+    K1Fn k1;
+    K3Fn k3;
+};
+static const K13 kK13[] = {
+    {0, 0, 0, k1_fwd_columns<0, 0, 0>, k3_inv_columns<0, 0, 0>},
+    {5, 2, 0, k1_fwd_columns<5, 2, 0>, k3_inv_columns<5, 2, 0>},
+    {7, 3, 4, k1_fwd_columns<7, 3, 4>, k3_inv_columns<7, 3, 4>},
+    {3, 8, 0, k1_fwd_columns<3, 8, 0>, k3_inv_columns<3, 8, 0>},
+    {3, 3, 0, k1_fwd_columns<3, 3, 0>, k3_inv_columns<3, 3, 0>},
+    {7, 4, 0, k1_fwd_columns<7, 4, 0>, k3_inv_columns<7, 4, 0>},
+    {7, 3, 8, k1_fwd_columns<7, 3, 8>, k3_inv_columns<7, 3, 8>},
+};
+
+static int k13_shape(const FftPlan &p)
+{
+    if (p.S < 2) return 0;
+    const int a = (int)p.st[0].R, b = (int)p.st[1].R;
+    const int c = p.S >= 3 && p.st[2].R != 16 ? (int)p.st[2].R : 0;
+    const int from = c ? 3 : 2;
+    if (p.S < from + 1) return 0;
+    for (int i = from; i < p.S; ++i)
+        if (p.st[i].R != 16) return 0;
+    for (int k = 1; k < (int)(sizeof kK13 / sizeof kK13[0]); ++k)
+        if (kK13[k].a == a && kK13[k].b == b && kK13[k].c == c) return k;
+    return 0;
 }
 
 // ------------------------------------------------------------------ host plan
@@ -1035,10 +1105,12 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const bool pf = !e || atoi(e) != 0;
         g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
     }
-    // K2 specialised for the common row-plan shapes (developer override PA_K2_T=0)
+    // K1/K2/K3 specialised for the common plan shapes (developer override PA_K2_T=0 / PA_K13_T=0)
     {
         const char *e = getenv("PA_K2_T");
         g->k2shape = (!e || atoi(e) != 0) ? k2_shape(g->f1) : 0;
+        const char *e13 = getenv("PA_K13_T");
+        g->k13 = (!e13 || atoi(e13) != 0) ? k13_shape(g->f2) : 0;
     }
     // row blocks for K2's output / K3's input (opt-in PA_LR=1): 128-byte K3 runs for 2- and
     // 4-column groups.  Bit-exact, but K2's stores become 32-byte pieces: C4 K3 725 -> 627, K2
@@ -1164,11 +1236,14 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     const Geometry &g = a.g;
     cudaError_t e;
     // per call: the attribute is per device and a process may drive several
-    if ((e = cudaFuncSetAttribute(k1_fwd_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess ||
+    for (const K13 &f : kK13)
+        if ((e = cudaFuncSetAttribute(f.k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(f.k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
+                cudaSuccess)
+            return cuda_fail(e, "route (a) cudaFuncSetAttribute");
+    if (
         (e = cudaFuncSetAttribute(k2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k3_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k2_rows_t<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
@@ -1183,7 +1258,7 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
-    k1_fwd_columns<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
+    kK13[g.k13].k1<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
     k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) seed transform launches");
     return PA_OK;
@@ -1261,7 +1336,7 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         prof_end(h, s);
     }
     prof_begin(h, 0, s);
-    launch_pdl(k1_fwd_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
+    launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
                out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
     prof_end(h, s);
     prof_begin(h, 1, s);
@@ -1283,7 +1358,7 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         launch_pdl(k3t_inv_columns, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1, s, a.buf2, g, a.T,
                    h->n, h->m, outs, a.resid, out_stride, count);
     } else {
-        launch_pdl(k3_inv_columns, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf2, g, a.T, h->n, h->m, outs,
+        launch_pdl(kK13[g.k13].k3, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf2, g, a.T, h->n, h->m, outs,
                    a.resid, out_stride);
     }
     prof_end(h, s);
