@@ -295,8 +295,8 @@ __device__ __forceinline__ uint32_t grow_off(const StageCtx &x, uint32_t a)
 // Not inlined: one copy per (R, direction, mode) per kernel keeps the code in
 // the instruction cache.
 template <int R, bool INV, int MODE>
-__device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
-                                        const double2 *whi, StageCtx x)
+__device__ __forceinline__ void stage_inl(double2 *sm, const StageDesc &sd, uint32_t logC, const double2 *wlo,
+                                          const double2 *whi, const StageCtx &x)
 {
     const uint32_t nb = sd.nb << logC;
     const uint32_t cm = (1u << logC) - 1;
@@ -329,6 +329,15 @@ __device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC
             }
         }
     }
+}
+
+// The same stage as a call (one copy per kernel for the general kernels' radix switch; the
+// shape-specialised kernels may inline stage_inl instead).
+template <int R, bool INV, int MODE>
+__device__ __noinline__ void stage_smem(double2 *sm, StageDesc sd, uint32_t logC, const double2 *wlo,
+                                        const double2 *whi, StageCtx x)
+{
+    stage_inl<R, INV, MODE>(sm, sd, logC, wlo, whi, x);
 }
 
 template <bool INV, int MODE = MODE_PLAIN>

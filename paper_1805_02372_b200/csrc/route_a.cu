@@ -286,15 +286,21 @@ k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, 
 // Column-pass stage dispatch for plans [A, B, (C), 16, ...] known at compile time (A = 0: the
 // general radix switch).  Instantiating only the radices a plan uses keeps K1/K3's code small,
 // which measurably matters (k2_rows_t).
+// K1/K3 keep their stages as calls: inlining them (K13_STAGE=stage_inl) helped the
+// throughput configs a little (C5d 1026 -> 1014 us) but cost the cold small ones more
+// (C2 37.9 -> 40 us, C3 188 -> 194 us: more code to fetch cold); K2 inlines (below)
+#ifndef K13_STAGE
+#define K13_STAGE stage_smem
+#endif
 template <bool INV, int MODE, int A, int B, int C>
 __device__ __forceinline__ void stage_t(double2 *sm, const FftPlan &P, int i, uint32_t logC, const double2 *wlo,
                                         const double2 *whi, const StageCtx &x = StageCtx{})
 {
     if (A == 0) stage_any<INV, MODE>(sm, P.st[i], logC, wlo, whi, x);
-    else if (i == 0) stage_smem<A ? A : 16, INV, MODE>(sm, P.st[0], logC, wlo, whi, x);
-    else if (i == 1) stage_smem<B ? B : 16, INV, MODE>(sm, P.st[1], logC, wlo, whi, x);
-    else if (i == 2 && C) stage_smem<C ? C : 16, INV, MODE>(sm, P.st[2], logC, wlo, whi, x);
-    else stage_smem<16, INV, MODE>(sm, P.st[i], logC, wlo, whi, x);
+    else if (i == 0) K13_STAGE<A ? A : 16, INV, MODE>(sm, P.st[0], logC, wlo, whi, x);
+    else if (i == 1) K13_STAGE<B ? B : 16, INV, MODE>(sm, P.st[1], logC, wlo, whi, x);
+    else if (i == 2 && C) K13_STAGE<C ? C : 16, INV, MODE>(sm, P.st[2], logC, wlo, whi, x);
+    else K13_STAGE<16, INV, MODE>(sm, P.st[i], logC, wlo, whi, x);
 }
 template <int A, int B, int C>
 __device__ __forceinline__ void dif_t(double2 *sm, const FftPlan &P, int i0, int i1, uint32_t logC,
@@ -534,6 +540,11 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 // (C2, C3, C5), 10240 = [5, 8, 16, 16] (C4, C5d), 6144 = [3, 8, 16, 16], 7168 = [7, 4, 16, 16],
 // calling those stage routines directly: the general kernel's radix switch instantiates every
 // radix and mode, and K2's speed is sensitive to its code.
+// K2's shape-specialised kernel inlines its stages (same-box A/B: C4 K2 1114 -> 1019 us,
+// C3 192.5 -> 188.5 us, C2 unchanged)
+#ifndef K2T_STAGE
+#define K2T_STAGE stage_inl
+#endif
 template <int R0, int R1>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T)
@@ -559,7 +570,7 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     rt.rlo = rlo;
     rt.rhi = rhi;
     rt.gin = rp;
-    stage_smem<R0, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
+    K2T_STAGE<R0, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
     __syncthreads();
     if (g.pf2 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
         const uint32_t q = threadIdx.x;
@@ -570,26 +581,26 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)q * chunk), "r"(sz) : "memory");
         }
     }
-    stage_smem<R1, false, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
+    K2T_STAGE<R1, false, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
     __syncthreads();
     for (int i = 2; i < P.S - 1; ++i) {
-        stage_smem<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
+        K2T_STAGE<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
     fused_mid<16>(P.st[P.S - 1], sm, sp);
     __syncthreads();
     for (int i = P.S - 2; i >= 2; --i) {
-        stage_smem<16, true, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
+        K2T_STAGE<16, true, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
-    stage_smem<R1, true, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
+    K2T_STAGE<R1, true, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
     __syncthreads();
     grid_dep_launch();  // K3 may start its prologue
     rt.gin = nullptr;
     rt.gout = rq;
     rt.lr = g.lr;
     rt.lc = g.logC;
-    stage_smem<R0, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+    K2T_STAGE<R0, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
 }
 
 // the shapes k2_rows_t is instantiated for (g.k2shape: 0 = general k2_rows)
