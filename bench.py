@@ -138,9 +138,13 @@ def peak_hbm():
 def ncu_kernel(config, kernel):
     """The committed `ncu --set full` summary of `kernel` (profiles/ncu_<config>.json)."""
     path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+
+    def base(name):  # k2_rows_t<16, 16> / k1_fwd_columns<5, 2, 0> -> k2_rows / k1_fwd_columns
+        name = name.split("<", 1)[0].strip()
+        return name[:-2] if name.endswith("_t") else name
     try:
         for d in json.load(open(path)):
-            if d.get("kernel") == kernel:
+            if base(d.get("kernel", "")) == kernel:
                 return d
     except Exception:
         pass
