@@ -342,8 +342,9 @@ def run_ours(args):
             "profiled_ms_per_step": float(np.mean(prof_ms)),
             "e2e": {"value": e2e_value, "unit": "Gbit/s", "h2d_bytes_per_step": 4 * key_h.numel(),
                     "d2h_bytes_per_step": 4 * pa.words32(m), "steps": e2e_steps, "verified": e2e_ok,
-                    "how": ("pa_hash_host_async per step (CUDA graph: pinned host key -> H2D -> K0..K3 -> "
-                            "D2H to pinned host output), CUDA events around each step, L2 flushed between")
+                    "how": ("pa_hash_host_async per step (CUDA graph: pinned host key -> copy kernel over the mapped "
+                            "pages -> K0..K3 -> copy kernel to the pinned host output), CUDA events around "
+                            "each step, L2 flushed between")
                     if split == "keys" else
                     "per step: this rank's key words H2D from pinned memory, the sharded hash and its "
                     "collectives, y D2H; CUDA events around each step, L2 flushed between",
@@ -442,7 +443,13 @@ def cpu_oracle_baseline(name, budget_s=12.0, max_rows=None):
     import oracle
     n, m, sw, kw = syn.config_inputs(name)
     cores = oracle.max_threads()
-    rows = np.arange(m if max_rows is None else min(m, max_rows), dtype=np.uint64)
+    if max_rows is None:  # bound the sample: probe one row's cost, then fit ~budget_s / 4 per repeat
+        probe = np.arange(min(m, 1024), dtype=np.uint64)
+        t0 = time.perf_counter()
+        oracle.toeplitz_rows(n, m, sw, kw, probe)
+        per_row = (time.perf_counter() - t0) / probe.size
+        max_rows = max(1024, int(budget_s / 4 / max(per_row, 1e-12)))
+    rows = np.arange(min(m, max_rows), dtype=np.uint64)
     t0 = time.perf_counter()
     reps = 0
     while True:

@@ -174,7 +174,10 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
 
 /* End-to-end variant with HOST buffers (pinned memory recommended): copies the
  * key host->device, hashes, copies the output device->host, and synchronises
- * the stream before returning. key_host: ceil(n/32) words; out_host: ceil(m/32). */
+ * the stream before returning. key_host: ceil(n/32) words; out_host: ceil(m/32).
+ * Pinned buffers (cudaHostAlloc / cudaHostRegister, e.g. torch pin_memory()) are moved by two
+ * copy kernels over the mapped pages inside one cached CUDA graph; pageable buffers by plain
+ * stream-ordered copies.  Host pointers need only 4-byte alignment. */
 pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream);
 
 /* pa_hash_host without the final synchronisation: the copies and kernels are

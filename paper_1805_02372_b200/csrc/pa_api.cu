@@ -695,6 +695,82 @@ pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_
     return PA_OK;
 }
 
+// pa_hash_host's transfers.  When both host buffers are pinned (mapped into the device's
+// address space), two copy kernels move the key in and the output out, PDL-chained to the hash
+// kernels, instead of copy-engine nodes: the engines' latency around the hash cost more than the
+// bytes (tools/dev/h2d_kernel.cu: 15.5 vs 10.2 us for 125 KB in + 31 KB out).  Measured e2e,
+// Gbit/s, engines -> kernels: C2 17.9 -> 21.1, C3 41.2 -> 45.2, C4 32.1 -> 33.5, C5c 33.4 -> 42.8,
+// so there is no size threshold by default.  Pageable buffers use plain copies (no graph).
+__global__ void k_host_copy(const uint32_t *__restrict__ src, uint32_t *__restrict__ dst, uint64_t nw)
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // whatever wrote src precedes us
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i0 = 0;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+        const uint64_t n4 = nw / 4;
+        for (uint64_t i = tid; i < n4; i += nth) ((uint4 *)dst)[i] = ((const uint4 *)src)[i];
+        i0 = 4 * n4;
+    }
+    for (uint64_t i = i0 + tid; i < nw; i += nth) dst[i] = src[i];
+}
+
+static uint64_t host_copy_max_bytes()
+{
+    static const uint64_t v = [] {
+        const char *e = getenv("PA_HOST_COPY_MAX");  // developer override: 0 = always the copy engines
+        return e ? (uint64_t)strtoull(e, nullptr, 0) : ~(uint64_t)0;
+    }();
+    return v;
+}
+
+// device-side address of a pinned host buffer, or NULL when it is pageable / not mapped
+static void *mapped_ptr(const void *p)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+// 0: pageable buffer(s) -- plain stream-ordered copies, no graph (a captured copy needs pinned
+// memory); 1: pinned, large -- graph with copy-engine nodes; 2: pinned, small -- graph with
+// copy kernels
+static int pick_host_copy(const pa_ctx *h, const void *key_host, const void *out_host)
+{
+    if (!mapped_ptr(key_host) || !mapped_ptr(out_host)) return 0;
+    return (h->n + 31) / 32 * 4 > host_copy_max_bytes() ? 1 : 2;
+}
+
+static cudaError_t launch_host_copy(const uint32_t *src, uint32_t *dst, uint64_t nw, cudaStream_t s)
+{
+    const uint64_t blocks = (nw / 4 + 255) / 256;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(blocks < 1 ? 1 : blocks > 296 ? 296 : blocks));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_host_copy, src, dst, nw);
+}
+
+static cudaError_t set_copy_node(cudaGraphExec_t ex, cudaGraphNode_t node, const uint32_t *src, uint32_t *dst,
+                                 uint64_t nw)
+{
+    cudaKernelNodeParams p;
+    cudaError_t e = cudaGraphKernelNodeGetParams(node, &p);
+    if (e != cudaSuccess) return e;
+    void *args[] = {(void *)&src, (void *)&dst, (void *)&nw};
+    p.kernelParams = args;
+    p.extra = nullptr;
+    return cudaGraphExecKernelNodeSetParams(ex, node, &p);
+}
+
 static void drop_host_graph(pa_ctx *h)
 {
     if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
@@ -702,13 +778,15 @@ static void drop_host_graph(pa_ctx *h)
     h->host_exec = nullptr;
     h->host_graph = nullptr;
     h->h2d_node = h->d2h_node = nullptr;
+    h->host_copy = 0;
     h->g_key_host = nullptr;
     h->g_out_host = nullptr;
 }
 
 // Capture H2D + the hash kernels + D2H once; later calls patch the two memcpy
 // nodes' host pointers and relaunch: one graph launch instead of six API calls.
-static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t *out_host, size_t kb, size_t ob)
+static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t *out_host, size_t kb, size_t ob,
+                                  int mode)
 {
     cudaStream_t cs;
     cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
@@ -718,9 +796,11 @@ static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t 
         cudaStreamDestroy(cs);
         return cuda_fail(e, "pa_hash_host begin capture");
     }
-    cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, cs);
+    if (mode == 2) launch_host_copy((const uint32_t *)mapped_ptr(key_host), h->stage_key, kb / 4, cs);
+    else cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, cs);
     st = hash_impl(h, h->stage_key, h->stage_out, (h->m + 31) / 32, cs, false);
-    cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, cs);
+    if (mode == 2) launch_host_copy(h->stage_out, (uint32_t *)mapped_ptr(out_host), ob / 4, cs);
+    else cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, cs);
     cudaGraph_t g = nullptr;
     e = cudaStreamEndCapture(cs, &g);
     cudaStreamDestroy(cs);
@@ -738,7 +818,16 @@ static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t 
     for (size_t i = 0; i < nn; ++i) {
         cudaGraphNodeType ty;
         cudaGraphNodeGetType(nodes[i], &ty);
-        if (ty != cudaGraphNodeTypeMemcpy) continue;
+        if (mode == 2 && ty == cudaGraphNodeTypeKernel) {
+            cudaKernelNodeParams kp;
+            cudaGraphKernelNodeGetParams(nodes[i], &kp);
+            if (kp.func != (void *)k_host_copy) continue;
+            const uint32_t *dst = *(uint32_t *const *)kp.kernelParams[1];
+            if (dst == h->stage_key) h2d = nodes[i];
+            else d2h = nodes[i];
+            continue;
+        }
+        if (mode != 1 || ty != cudaGraphNodeTypeMemcpy) continue;
         cudaMemcpy3DParms pr;
         cudaGraphMemcpyNodeGetParams(nodes[i], &pr);
         if (pr.kind == cudaMemcpyHostToDevice || pr.dstPtr.ptr == h->stage_key) h2d = nodes[i];
@@ -754,6 +843,7 @@ static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t 
     h->host_exec = ex;
     h->h2d_node = h2d;
     h->d2h_node = d2h;
+    h->host_copy = mode;
     h->g_key_host = key_host;
     h->g_out_host = out_host;
     return PA_OK;
@@ -776,7 +866,9 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
         h->stage_key = (uint32_t *)h->stage_blk;
         h->stage_out = (uint32_t *)(h->stage_blk + al256(kb));
     }
-    if (h->prof.on) {  // per-launch profiling events need the plain launches
+    const bool moved = key_host != h->g_key_host || out_host != h->g_out_host;
+    const int mode = h->host_exec && !moved ? h->host_copy : pick_host_copy(h, key_host, out_host);
+    if (h->prof.on || mode == 0) {  // per-launch profiling events need the plain launches
         if ((e = cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
             return cuda_fail(e, "pa_hash_host H2D");
         pa_status st = hash_impl(h, h->stage_key, h->stage_out, (h->m + 31) / 32, s, false);
@@ -784,20 +876,25 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
         if ((e = cudaMemcpyAsync(out_host, h->stage_out, ob, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
             return cuda_fail(e, "pa_hash_host D2H");
     } else {
+        if (h->host_exec && mode != h->host_copy) drop_host_graph(h);  // pinned <-> pageable: other nodes
         if (!h->host_exec) {
-            pa_status st = build_host_graph(h, key_host, out_host, kb, ob);
+            pa_status st = build_host_graph(h, key_host, out_host, kb, ob, mode);
             if (st != PA_OK) return st;
         }
         if (key_host != h->g_key_host) {
-            if ((e = cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->h2d_node, h->stage_key, key_host, kb,
-                                                        cudaMemcpyHostToDevice)) != cudaSuccess)
-                return cuda_fail(e, "pa_hash_host graph update (key)");
+            e = mode == 2 ? set_copy_node(h->host_exec, h->h2d_node, (const uint32_t *)mapped_ptr(key_host),
+                                          h->stage_key, kb / 4)
+                          : cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->h2d_node, h->stage_key, key_host,
+                                                               kb, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cuda_fail(e, "pa_hash_host graph update (key)");
             h->g_key_host = key_host;
         }
         if (out_host != h->g_out_host) {
-            if ((e = cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->d2h_node, out_host, h->stage_out, ob,
-                                                        cudaMemcpyDeviceToHost)) != cudaSuccess)
-                return cuda_fail(e, "pa_hash_host graph update (out)");
+            e = mode == 2 ? set_copy_node(h->host_exec, h->d2h_node, h->stage_out,
+                                          (uint32_t *)mapped_ptr(out_host), ob / 4)
+                          : cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->d2h_node, out_host, h->stage_out,
+                                                               ob, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return cuda_fail(e, "pa_hash_host graph update (out)");
             h->g_out_host = out_host;
         }
         if ((e = cudaGraphLaunch(h->host_exec, s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host graph launch");

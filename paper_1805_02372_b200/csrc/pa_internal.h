@@ -118,6 +118,7 @@ struct pa_ctx {
     cudaGraph_t host_graph = nullptr;
     cudaGraphExec_t host_exec = nullptr;
     cudaGraphNode_t h2d_node = nullptr, d2h_node = nullptr;
+    int host_copy = 0;  // how the graph moves the key / output: 1 copy engines, 2 copy kernels (mapped pages)
     const void *g_key_host = nullptr;
     void *g_out_host = nullptr;
 };

@@ -358,6 +358,36 @@ def test_host_async_graph_repoints_buffers():
             assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, w, rows))
 
 
+def test_host_copy_modes_pinned_pageable_misaligned():
+    """pa_hash_host moves a small key / output with copy kernels over mapped pinned pages and
+    falls back to the copy engines for pageable buffers; switching between the two (and
+    4-byte-aligned host pointers, the kernels' scalar path) re-builds or re-points the graph
+    and every result stays exact."""
+    n, m = 1_000_003, 250_000
+    kw_, ow = pa.words32(n), pa.words32(m)
+    sw = syn.random_bits(syn.seed_stream(83), n + m - 1)
+    keys = [syn.random_bits(syn.key_stream(83, k), n) for k in range(6)]
+    rows = sample_rows(m, 11, 512)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        for k, w in enumerate(keys):
+            kind = ("pinned", "pageable", "pinned+4", "pinned", "pageable+4", "pinned+4")[k]
+            pin = kind.startswith("pinned")
+            off = 1 if kind.endswith("+4") else 0
+            kbuf = torch.zeros(kw_ + 4, dtype=torch.int32)
+            obuf = torch.full((ow + 4,), -1, dtype=torch.int32)
+            if pin:
+                kbuf, obuf = kbuf.pin_memory(), obuf.pin_memory()
+            kbuf[off:off + kw_] = torch.from_numpy(w.view(np.int32)[:kw_].copy())
+            kh, oh = kbuf[off:off + kw_], obuf[off:off + ow]
+            assert (kh.data_ptr() % 16 != 0) == bool(off)
+            (h.hash_host if k % 2 else h.hash_host_async)(kh, oh)
+            torch.cuda.synchronize()
+            got = oracle.unpack(oh.numpy().view(np.uint32), 32 * ow)
+            assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, w, rows)), kind
+            assert not got[m:].any(), kind
+            assert (obuf[:off] == -1).all() and (obuf[off + ow:] == -1).all(), kind  # nothing outside
+
+
 @pytest.mark.parametrize("n,m,maxb", [(20_000, 7_000, 5_000), (50_001, 20_000, 16_384), (3001, 3000, 700),
                                       (100_000, 10_000, 0)])
 def test_length_compatible_blocked(n, m, maxb):
