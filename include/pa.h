@@ -188,9 +188,10 @@ pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host
 pa_status pa_hash_host_async(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream);
 
 /* Batched end to end with HOST buffers (pinned memory recommended): count keys at key_host +
- * k*key_stride_words are copied host->device in one transfer, hashed as one pa_hash_batch
- * (same seed), and the count outputs copied back to out_host + k*out_stride_words in one
- * transfer; synchronises `stream` before returning.  Strides in uint32 words (>= ceil(n/32) and
+ * k*key_stride_words are hashed with the handle's seed and the outputs written to out_host +
+ * k*out_stride_words.  Keys move in chunks through two device staging slots: chunk i+1's
+ * host->device copy and chunk i-1's device->host copy (copy engines, on a stream of the handle)
+ * overlap chunk i's hash on `stream`.  Synchronises `stream` before returning.  Strides in uint32 words (>= ceil(n/32) and
  * ceil(m/32)).  Staging grows on demand (a workspace handle: PA_ERR_NOMEM beyond count = 1). */
 pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t key_stride_words,
                              uint32_t *outs_host, uint64_t out_stride_words, uint32_t count, void *stream);

@@ -216,6 +216,9 @@ static void destroy_ctx(pa_ctx *h)
     rb_destroy(h);
     dev_free(h, h->stage_blk);
     if (h->bstage) cudaFree(h->bstage);
+    for (cudaEvent_t &ev : h->pev)
+        if (ev) cudaEventDestroy(ev);
+    if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->own_arena) delete h->arena;
     delete h;
 }
@@ -927,8 +930,15 @@ pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t ke
         }
         return PA_OK;
     }
+    // Chunks of keys in a software pipeline over two staging slots: the copy stream moves chunk
+    // i+1's keys in and chunk i-1's outputs out (copy engines, PCIe) while `stream` hashes chunk
+    // i, so the transfers hide behind the kernels except the first chunk's H2D and the last D2H.
     const uint64_t kw4 = (kw + 3) / 4 * 4, ow4 = (ow + 3) / 4 * 4;
-    const size_t need = (size_t)count * (kw4 + ow4) * 4;
+    const pa_ctx *leaf = h->nsub ? h->sub[0] : h;
+    uint32_t chunk = leaf->route == PA_ROUTE_TRANSFORM ? ra_batch_keys(leaf) : 4096;
+    if (chunk > count) chunk = count;
+    const uint32_t nslot = count > chunk ? 2 : 1;
+    const size_t slot_words = (size_t)chunk * (kw4 + ow4), need = nslot * slot_words * 4;
     cudaError_t e;
     if (need > h->bstage_bytes) {
         if (h->bstage) {
@@ -946,16 +956,47 @@ pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t ke
         }
         h->bstage_bytes = need;
     }
-    if (count > 1 && batch_grows(h, count)) drop_host_graph(h);  // work buffers are about to move
-    uint32_t *dk = (uint32_t *)h->bstage, *dout = dk + (size_t)count * kw4;
-    if ((e = cudaMemcpy2DAsync(dk, kw4 * 4, keys_host, key_stride_words * 4, kw * 4, count,
-                               cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        return cuda_fail(e, "pa_hash_host_batch H2D");
-    pa_status st = batch_impl(h, dk, kw4, dout, ow4, count, ow, s);
-    if (st != PA_OK) return st;
-    if ((e = cudaMemcpy2DAsync(outs_host, out_stride_words * 4, dout, ow4 * 4, ow * 4, count,
-                               cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-        return cuda_fail(e, "pa_hash_host_batch D2H");
+    if (!h->cstream) {
+        if ((e = cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "pa_hash_host_batch copy stream");
+        for (cudaEvent_t &ev : h->pev)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "pa_hash_host_batch events");
+    }
+    if (chunk > 1 && batch_grows(h, chunk)) drop_host_graph(h);  // work buffers are about to move
+    cudaStream_t cs = h->cstream;
+    cudaEvent_t *h2d = h->pev, *comp = h->pev + 2, start = h->pev[4];
+    auto kslot = [&](uint32_t i) { return (uint32_t *)h->bstage + (i % nslot) * slot_words; };
+    auto oslot = [&](uint32_t i) { return kslot(i) + (size_t)chunk * kw4; };
+    auto keys_of = [&](uint32_t i) { return count - i * chunk < chunk ? count - i * chunk : chunk; };
+    auto h2d_chunk = [&](uint32_t i) {
+        return cudaMemcpy2DAsync(kslot(i), kw4 * 4, keys_host + (size_t)i * chunk * key_stride_words,
+                                 key_stride_words * 4, kw * 4, keys_of(i), cudaMemcpyHostToDevice, cs);
+    };
+    const uint32_t nch = (count + chunk - 1) / chunk;
+    cudaEventRecord(start, s);  // earlier work on `stream` may still use the staging / work buffers
+    cudaStreamWaitEvent(cs, start, 0);
+    if ((e = h2d_chunk(0)) != cudaSuccess) return cuda_fail(e, "pa_hash_host_batch H2D");
+    cudaEventRecord(h2d[0], cs);
+    for (uint32_t i = 0; i < nch; ++i) {
+        const uint32_t sl = i % nslot;
+        if (i + 1 < nch) {  // next chunk's keys, once chunk i-1 (same slot) has consumed its own
+            if (i >= 1) cudaStreamWaitEvent(cs, comp[(i + 1) % nslot], 0);
+            if ((e = h2d_chunk(i + 1)) != cudaSuccess) return cuda_fail(e, "pa_hash_host_batch H2D");
+            cudaEventRecord(h2d[(i + 1) % nslot], cs);
+        }
+        // chunk i-2's outputs left this slot before chunk i's keys arrived (copy stream order)
+        cudaStreamWaitEvent(s, h2d[sl], 0);
+        pa_status st = batch_impl(h, kslot(i), kw4, oslot(i), ow4, keys_of(i), ow, s);
+        if (st != PA_OK) return st;
+        cudaEventRecord(comp[sl], s);
+        cudaStreamWaitEvent(cs, comp[sl], 0);
+        if ((e = cudaMemcpy2DAsync(outs_host + (size_t)i * chunk * out_stride_words, out_stride_words * 4, oslot(i),
+                                   ow4 * 4, ow * 4, keys_of(i), cudaMemcpyDeviceToHost, cs)) != cudaSuccess)
+            return cuda_fail(e, "pa_hash_host_batch D2H");
+    }
+    cudaEventRecord(start, cs);
+    cudaStreamWaitEvent(s, start, 0);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host_batch sync");
     return PA_OK;
 }

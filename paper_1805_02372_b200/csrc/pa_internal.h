@@ -102,6 +102,9 @@ struct pa_ctx {
     // staging for pa_hash_host_batch (cudaMalloc, grown on demand; never in a workspace)
     char *bstage = nullptr;
     size_t bstage_bytes = 0;
+    // pa_hash_host_batch pipeline: copies on their own stream, overlapped with the hashes
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t pev[5] = {};  // h2d[2], comp[2], start/done
     // device memory: the caller's workspace (nullptr: cudaMalloc)
     pa::Arena *arena = nullptr;
     bool own_arena = false;

@@ -881,10 +881,15 @@ def test_gigabit_under_2gib_budget_and_plan_consistency():
 
 
 @pytest.mark.parametrize("n,m,count,kwargs", [(1_048_576, 104_857, 64, {}), (4096, 1024, 500, {}),
-                                              (300_007, 60_001, 5, {"max_transform_len": 200_000})])
+                                              (300_007, 60_001, 5, {"max_transform_len": 200_000}),
+                                              (1_048_576, 104_857, 150, {}),
+                                              (300_007, 60_001, 133, {"max_transform_len": 200_000}),
+                                              (4096, 1024, 9000, {})])
 def test_hash_host_batch(n, m, count, kwargs):
-    """pa_hash_host_batch: pinned host keys (strided rows) -> one H2D, one batched hash, one D2H;
-    every output vs the oracle (sampled for the 500-key case), tail bits zero."""
+    """pa_hash_host_batch: pinned host keys (strided rows) -> chunks of keys pipelined through two
+    staging slots (H2D / hash / D2H overlapped; several chunks with a ragged last one for the
+    larger counts); every output vs the oracle (sampled above 64 keys), tail bits zero, and
+    nothing written past each output row."""
     sw = syn.random_bits(syn.seed_stream(150), n + m - 1)
     kw32 = pa.words32(n)
     rng = np.random.default_rng(150)
@@ -899,3 +904,4 @@ def test_hash_host_batch(n, m, count, kwargs):
         want = oracle.unpack(oracle.toeplitz_words(n, m, sw, keys[k, :kw32].copy()), m)
         assert np.array_equal(oracle.unpack(got[k], m), want), k
         assert not oracle.unpack(got[k][: pa.words32(m)], 32 * pa.words32(m))[m:].any()
+    assert (oh[:, pa.words32(m):] == -1).all()
