@@ -555,6 +555,8 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     const uint32_t row = blockIdx.y;
     buf += (uint64_t)blockIdx.x * g.M;
     out2 += (uint64_t)blockIdx.x * g.M;
+    TRACE_BEGIN(2);
+    TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *rq = out2 + wrow(g, row);
     const double2 *sp = spec + (uint64_t)row * N1;
@@ -565,6 +567,7 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     }
     grid_dep_wait();  // K1's work array
     __syncthreads();
+    TSTAMP(1);
     const FftPlan &P = g.f1;
     StageCtx rt;
     rt.rlo = rlo;
@@ -572,6 +575,7 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     rt.gin = rp;
     K2T_STAGE<R0, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
     __syncthreads();
+    TSTAMP(2);
     if (g.pf2 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
         const uint32_t q = threadIdx.x;
         const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
@@ -587,8 +591,10 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
         K2T_STAGE<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
+    TSTAMP(3);
     fused_mid<16>(P.st[P.S - 1], sm, sp);
     __syncthreads();
+    TSTAMP(4);
     for (int i = P.S - 2; i >= 2; --i) {
         K2T_STAGE<16, true, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
@@ -596,11 +602,14 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     K2T_STAGE<R1, true, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
     __syncthreads();
     grid_dep_launch();  // K3 may start its prologue
+    TSTAMP(5);
     rt.gin = nullptr;
     rt.gout = rq;
     rt.lr = g.lr;
     rt.lc = g.logC;
     K2T_STAGE<R0, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+    TSTAMP(6);
+    TRACE_END(2);
 }
 
 // the shapes k2_rows_t is instantiated for (g.k2shape: 0 = general k2_rows)
