@@ -17,6 +17,9 @@ struct Geometry {
     uint64_t M;             // complex transform length
     uint32_t N1, N2;        // rows are N1 long (contiguous), N2 rows
     uint32_t C, logC;       // columns per CTA in the strided passes (power of two <= 16)
+    uint32_t C3, logC3;     // K3's column groups (C, or C / 2 when that fits two CTAs per SM)
+    uint32_t t3, tile3, smem3;  // K3's threads / tile / shared bytes for C3
+    uint32_t k1gout;        // K1's last stage stores to global directly when C >= k1gout
     FftPlan f1, f2;         // stage plans of N1 (row pass) and N2 (strided passes)
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)
     uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)

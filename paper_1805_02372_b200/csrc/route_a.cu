@@ -59,7 +59,10 @@ constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic shared memory 
 
 #ifdef PA_TIMING
 __device__ unsigned long long g_k2_clk[3][64][16];
-#define TSTAMPK(k, i) do { __syncthreads(); const unsigned _lb = blockIdx.x + gridDim.x * blockIdx.y; \
+#ifndef PA_STAMP_BASE
+#define PA_STAMP_BASE 0  // first CTA recorded (e.g. 2048: a steady-state wave of a many-wave grid)
+#endif
+#define TSTAMPK(k, i) do { __syncthreads(); const unsigned _lb = blockIdx.x + gridDim.x * blockIdx.y - PA_STAMP_BASE; \
     if (threadIdx.x == 0 && _lb < 64) g_k2_clk[k][_lb][i] = clock64(); } while (0)
 #define TSTAMP(i) TSTAMPK(1, i)
 __device__ unsigned long long g_trace[4][8192][3];  // per kernel (K0..K3), per CTA: smid, start, end ns
@@ -382,8 +385,8 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     __syncthreads();
     TSTAMPK(0, 3);
     // row p of the work array = DIF output position p (k_b = rev2[p]).  The last forward
-    // stage writes it straight to global when the per-row chunk is >= 64 B (see K3)
-    const bool direct = g.f2.S > 1 && C >= 4;
+    // stage writes it straight to global when C >= g.k1gout (2: 32-byte row pieces)
+    const bool direct = g.f2.S > 1 && C >= g.k1gout;
     if (direct) {
         dif_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
@@ -1150,7 +1153,42 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     }
     if (const char *e = getenv("PA_FORCE_T1")) g->t1 = (uint32_t)atoi(e);  // developer overrides
     if (const char *e = getenv("PA_FORCE_T2")) g->t2 = (uint32_t)atoi(e);
+    // K3's column groups: half of K1's when K1's tile allows one CTA per SM and the half tile
+    // two -- a second CTA's loads overlap the first one's stages, worth more than the longer
+    // 16-byte row pieces (C4: K3 721 -> 630 us; K1 itself measured slower at C = 1, 778 -> 919
+    // us, so it keeps C).  Needs the row-major K2 -> K3 array (lr = 0; wcol is C-specific).
+    // Developer override PA_K3_HALF=0.
+    {
+        // K1's last stage stores straight to global from C = 2 up (32-byte row pieces; same-box
+        // C4 2481 -> 2459 us, C5c 336.9 -> 333.8, C5d 1030 -> 1026); developer override
+        const char *e = getenv("PA_K1_GOUT_MINC");
+        g->k1gout = e ? (uint32_t)atoi(e) : 2u;
+    }
+    g->C3 = g->C;
+    {
+        const char *e = getenv("PA_K3_HALF");
+        if ((!e || atoi(e) != 0) && g->lr == 0 && !g->k3t && g->C >= 2 && 2 * g->smem1 > kSmemLimit &&
+            2 * smem_k13(g->N2, g->C / 2, g->f2) <= kSmemLimit)
+            g->C3 = g->C / 2;
+    }
+    g->logC3 = 0;
+    while ((1u << g->logC3) < g->C3) ++g->logC3;
+    g->tile3 = tile_bytes((uint64_t)g->N2 * g->C3) / 16;
+    g->smem3 = smem_k13(g->N2, g->C3, g->f2);
+    g->t3 = g->C3 == g->C ? g->t1 : 2 * g->smem3 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
     return PA_OK;
+}
+
+// K3 runs on its own column groups (C3): the same geometry with K1's group fields replaced
+static Geometry k3_geometry(const Geometry &g)
+{
+    Geometry r = g;
+    r.C = g.C3;
+    r.logC = g.logC3;
+    r.t1 = g.t3;
+    r.tile1 = g.tile3;
+    r.smem1 = g.smem3;
+    return r;
 }
 
 static size_t ntables(const Geometry &g)
@@ -1378,7 +1416,8 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         launch_pdl(k3t_inv_columns, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1, s, a.buf2, g, a.T,
                    h->n, h->m, outs, a.resid, out_stride, count);
     } else {
-        launch_pdl(kK13[g.k13].k3, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.buf2, g, a.T, h->n, h->m, outs,
+        const Geometry g3 = k3_geometry(g);
+        launch_pdl(kK13[g.k13].k3, dim3(g3.N1 / g3.C, count), g3.t1, g3.smem1, s, a.buf2, g3, a.T, h->n, h->m, outs,
                    a.resid, out_stride);
     }
     prof_end(h, s);
