@@ -145,6 +145,17 @@ __device__ __forceinline__ void load_tables(double2 *wlo, double2 *whi, const do
     }
 }
 
+// the same with cp.async: the table loads overlap whatever the CTA issues next (the key bits,
+// its row or tile); cp_async_wait_all() + __syncthreads() before the first use
+__device__ __forceinline__ void load_tables_async(double2 *wlo, double2 *whi, const double2 *glo,
+                                                  const double2 *ghi, uint32_t nhi)
+{
+    for (uint32_t i = threadIdx.x; i < 64 + nhi; i += blockDim.x) {
+        if (i < 64) cp_async16(wlo + i, glo + i);
+        else cp_async16(whi + i - 64, ghi + i - 64);
+    }
+}
+
 // ------------------------------------------------------------------ tables
 __global__ void k_tables(Geometry g, RouteTables T)
 {
@@ -341,8 +352,8 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     const uint32_t tot = g.N2 << logC;
     TRACE_BEGIN(1);
     TSTAMPK(0, 0);
-    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
-    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
+    load_tables_async(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     grid_dep_wait();  // K0's bit streams
     if (zero_out) {  // K3 XORs this hash's output bits in (zero_words = 0: accumulate)
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
@@ -369,6 +380,7 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
         const uint32_t *src = kb + (uint64_t)blockIdx.x * g.kbw;
         for (uint32_t i = threadIdx.x; i < g.kbw; i += blockDim.x) rowbits[i] = __ldg(src + i);
     }
+    cp_async_wait_all();  // the tables
     TSTAMPK(0, 1);
     __syncthreads();
     TSTAMPK(0, 2);
@@ -462,17 +474,17 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     double2 *rp = buf + (uint64_t)row * N1;  // input row (row-major)
     double2 *rq = out2 + wrow(g, row);        // output row: element a at rq[wcol(g, a)]
     double2 *sp = spec + (uint64_t)row * N1;
-    load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
+    load_tables_async(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
-        load_tables(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
+        load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
     if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
-        cp_async_wait_all();
     }
+    cp_async_wait_all();  // tables (and the staged row)
     __syncthreads();
     TSTAMP(1);
     const FftPlan &P = g.f1;
@@ -563,12 +575,13 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *rq = out2 + wrow(g, row);
     const double2 *sp = spec + (uint64_t)row * N1;
-    load_tables(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
+    load_tables_async(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
-        load_tables(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
+        load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
     grid_dep_wait();  // K1's work array
+    cp_async_wait_all();  // the tables
     __syncthreads();
     TSTAMP(1);
     const FftPlan &P = g.f1;
@@ -715,8 +728,8 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     const uint32_t tot = g.N2 << logC;
     TRACE_BEGIN(3);
     TSTAMPK(2, 0);
-    load_tables(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
-    load_tables(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
+    load_tables_async(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     grid_dep_wait();  // K2's rows
     // first inverse stage reads the columns straight from global when the per-row chunk is
     // >= 64 B (C >= 4); with 32 B chunks (C = 2) the staged cp.async copy is faster (round 1:
@@ -725,8 +738,8 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     if (!direct) {
         for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
             cp_async16(sm + pidx(e), buf + wrow(g, e >> logC) + ((uint64_t)a0 << g.lr) + (e & (C - 1)));
-        cp_async_wait_all();
     }
+    cp_async_wait_all();  // tables (and the staged tile)
     __syncthreads();
     int64_t b_lo, b_hi;
     k3_window_rows(g, a0, C, n, m, &b_lo, &b_hi);
