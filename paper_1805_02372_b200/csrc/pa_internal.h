@@ -19,6 +19,7 @@ struct Geometry {
     uint32_t C, logC;       // columns per CTA in the strided passes (power of two <= 16)
     uint32_t C3, logC3;     // K3's column groups (C, or C / 2 when that fits two CTAs per SM)
     uint32_t t3, tile3, smem3;  // K3's threads / tile / shared bytes for C3
+    uint32_t pfs;           // K2: L2 prefetch of the CTA's own spectrum row (one CTA per SM)
     uint32_t k1gout;        // K1's last stage stores to global directly when C >= k1gout
     FftPlan f1, f2;         // stage plans of N1 (row pass) and N2 (strided passes)
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)

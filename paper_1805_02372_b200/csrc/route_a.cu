@@ -156,6 +156,19 @@ __device__ __forceinline__ void load_tables_async(double2 *wlo, double2 *whi, co
     }
 }
 
+// bulk L2 prefetch of one N1-element row (warp 0 issues 32 pieces)
+__device__ __forceinline__ void l2_prefetch_row(const double2 *row, uint32_t N1)
+{
+    const uint32_t q = threadIdx.x;
+    if (q >= 32) return;
+    const char *src = reinterpret_cast<const char *>(row);
+    const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
+    if (q * chunk < bytes) {
+        const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)q * chunk), "r"(sz) : "memory");
+    }
+}
+
 // ------------------------------------------------------------------ tables
 __global__ void k_tables(Geometry g, RouteTables T)
 {
@@ -479,6 +492,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
+    if (g.pfs && mode == 0) l2_prefetch_row(sp, N1);
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
     if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
@@ -521,7 +535,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     if (g.pf2 && mode == 0 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
         // the CTA one wave ahead will load row + pf2: start pulling it into L2 now, under this
         // row's compute (multi-wave grids only, see ra_plan; C4 K2 1219 -> 1129 us.  Prefetching
-        // the spectrum row as well, or K3's next column group, measured slower)
+        // the next spectrum row as well, or K3's next column group, measured slower)
         const uint32_t q = threadIdx.x;
         const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
         const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
@@ -580,6 +594,7 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
+    if (g.pfs) l2_prefetch_row(sp, N1);  // this row's spectrum, pulled in under the forward stages
     grid_dep_wait();  // K1's work array
     cp_async_wait_all();  // the tables
     __syncthreads();
@@ -1176,6 +1191,13 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         // C4 2481 -> 2459 us, C5c 336.9 -> 333.8, C5d 1030 -> 1026); developer override
         const char *e = getenv("PA_K1_GOUT_MINC");
         g->k1gout = e ? (uint32_t)atoi(e) : 2u;
+    }
+    // K2: L2 prefetch of the CTA's own spectrum row at its start, under the forward stages, when
+    // one CTA runs per SM (C4 2453 -> 2421 us, C5d -0.7%; at two CTAs per SM it measured slower,
+    // C3 187 -> 193 us).  Developer override PA_PFS=0/1
+    {
+        const char *e = getenv("PA_PFS");
+        g->pfs = e ? (uint32_t)atoi(e) : g->t2 == PA_TMAX ? 1u : 0u;
     }
     g->C3 = g->C;
     {
