@@ -533,7 +533,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     }
     TSTAMP(2);
     if (g.pf2 && mode == 0 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
-        // the CTA one wave ahead will load row + pf2: start pulling it into L2 now, under this
+        // a CTA pf2 rows later will load row + pf2: start pulling it into L2 now, under this
         // row's compute (multi-wave grids only, see ra_plan; C4 K2 1219 -> 1129 us.  Prefetching
         // the next spectrum row as well, or K3's next column group, measured slower)
         const uint32_t q = threadIdx.x;
@@ -1149,12 +1149,15 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // 256 threads when two CTAs share an SM (<= 128 registers each), else 512
     g->t1 = 2 * g->smem1 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
     g->t2 = 2 * g->smem2 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
-    // K2: L2 prefetch of the row one wave ahead when one CTA per SM runs > 2 waves (C4); it
-    // measured slower at two CTAs per SM.  Developer override PA_PF=0 turns it off
+    // K2: L2 prefetch of the row pf2 rows ahead when one CTA per SM runs > 2 waves (C4, C5d); it
+    // measured slower at two CTAs per SM
     {
         const char *e = getenv("PA_PF");
-        const bool pf = !e || atoi(e) != 0;
-        g->pf2 = pf && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? 148u : 0;
+        // distance in rows: 56 (a third of a wave; same-box sweep C4 / C5d: 8 -> 1040 us at C5d,
+        // 37-74 -> 2405-2410 / 1010-1012 us, 148 -> 2424 / 1019, 296 -> 2494 / 1070, off -> 2529 /
+        // 1067).  Developer override PA_PF=0 (off) or PA_PF=d
+        const uint32_t dist = e ? (uint32_t)atoi(e) : 56u;
+        g->pf2 = dist && g->t2 == PA_TMAX && g->N2 > 2 * 148u ? dist : 0;
     }
     // K1/K2/K3 specialised for the common plan shapes (developer override PA_K2_T=0 / PA_K13_T=0)
     {
