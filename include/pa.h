@@ -103,6 +103,8 @@ typedef struct pa_info {
     uint64_t workspace_bytes; /* device bytes owned by the handle */
     uint64_t kernels_per_hash;/* kernel launches enqueued by one pa_hash */
     uint64_t column_blocks;   /* key blocks of the Eq. (4) split (1 = unsplit) */
+    uint64_t k3_cols_per_cta; /* route (a): columns per CTA of the inverse column pass (K3):
+                                 cols_per_cta, or half of it when that fits two CTAs per SM */
 } pa_info;
 
 /* Fill *opt with defaults (route AUTO, offset 0, library batch width, no split). */

@@ -55,7 +55,7 @@ class pa_info(ctypes.Structure):
                 ("device", ctypes.c_int32), ("transform_len", ctypes.c_uint64),
                 ("n1", ctypes.c_uint64), ("n2", ctypes.c_uint64), ("cols_per_cta", ctypes.c_uint64),
                 ("workspace_bytes", ctypes.c_uint64), ("kernels_per_hash", ctypes.c_uint64),
-                ("column_blocks", ctypes.c_uint64)]
+                ("column_blocks", ctypes.c_uint64), ("k3_cols_per_cta", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -1123,6 +1123,7 @@ pa_status pa_plan(uint64_t n, uint64_t m, pa_info *info)
     info->n1 = g.N1;
     info->n2 = g.N2;
     info->cols_per_cta = g.C;
+    info->k3_cols_per_cta = g.C3;
     pa_options o;
     pa_options_init(&o);
     o.route = PA_ROUTE_TRANSFORM;
@@ -1155,6 +1156,7 @@ pa_status pa_get_info(pa_handle h, pa_info *info)
         info->n1 = b->a.g.N1;
         info->n2 = b->a.g.N2;
         info->cols_per_cta = b->a.g.C;
+        info->k3_cols_per_cta = b->a.g.C3;
     }
     info->kernels_per_hash = h->kernels_per_hash;
     return PA_OK;

@@ -737,6 +737,35 @@ def test_row_block_layout_opt_in(n, m, monkeypatch):
         assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m]), k3t
 
 
+@pytest.mark.parametrize("n,m,plan", [(10_000_000, 1_000_000, "4096,1792,4"), (3_000_000, 300_000, "1024,3600,2"),
+                                       (2_000_003, 400_000, "1536,4096,2")])
+def test_k3_half_column_groups(n, m, plan, monkeypatch):
+    """K3 on half of K1's column groups (Geometry::C3, taken when K1's tile allows one CTA per SM
+    and the half tile two): forced plans that trigger it at moderate sizes, bit-exact against
+    the oracle (sampled rows), the full unit-key closed form, and PA_K3_HALF=0 (K3 on K1's
+    groups) giving the same output."""
+    monkeypatch.setenv("PA_FORCE_PLAN", plan)
+    sw = syn.random_bits(syn.seed_stream(121), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(121, 0), n)
+    s01 = oracle.unpack(sw, n + m - 1)
+    outs = []
+    for half in ("1", "0"):
+        monkeypatch.setenv("PA_K3_HALF", half)
+        with pa.Hasher(n, m, to_dev(sw), route="transform") as h:
+            assert "%d,%d,%d" % (h.info["n1"], h.info["n2"], h.info["cols_per_cta"]) == plan
+            assert h.info["k3_cols_per_cta"] == h.info["cols_per_cta"] // (2 if half == "1" else 1)
+            got = from_dev(h.hash(to_dev(kw)), m)
+            j = n // 2 + 1
+            unit = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
+            torch.cuda.synchronize()
+            assert h.residual() < 1e-3
+        assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m]), half
+        outs.append(got)
+    assert np.array_equal(outs[0], outs[1])
+    rows = sample_rows(m, 12)
+    assert np.array_equal(outs[0][rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+
+
 def test_no_device_memory_leak_across_handles():
     """200 create / hash / destroy cycles over both routes, split, workspace-backed and host-path
     handles return device memory to its starting level (libpa cudaMallocs are all freed)."""
