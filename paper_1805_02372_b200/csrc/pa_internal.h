@@ -21,6 +21,7 @@ struct Geometry {
     uint32_t t3, tile3, smem3;  // K3's threads / tile / shared bytes for C3
     uint32_t pfs;           // K2: L2 prefetch of the CTA's own spectrum row (one CTA per SM)
     uint32_t k1gout;        // K1's last stage stores to global directly when C >= k1gout
+    uint32_t ntb;           // K1's first stage from the key bits: 2^R0 x R0 table entries (0 = off)
     FftPlan f1, f2;         // stage plans of N1 (row pass) and N2 (strided passes)
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)
     uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)
@@ -39,6 +40,7 @@ struct RouteTables {
     double2 *thlo, *thhi;   // theta_b = exp(i pi b / (2 N2)) = zeta^{N1 b}, two-level
     uint32_t *rev2;         // K1 DIF output position p -> frequency index k_b
     double2 *rho;           // [N2][64 + N1/64]: row p's two-level table of rho = e^{2 pi i (1-4k_b)/4M}
+    double2 *tb;            // [2^R0][R0]: T[p][k] = sum_{r in p} e^{i pi r (1 - 4k) / 2R0} (K1 first stage)
 };
 
 struct RouteA {

@@ -170,6 +170,28 @@ __device__ __forceinline__ void l2_prefetch_row(const double2 *row, uint32_t N1)
 }
 
 // ------------------------------------------------------------------ tables
+// K1's first DIF stage reads x, not z: with b = j + r Ls (Ls = N2 / R), theta_b = theta_j c_r,
+// c_r = e^{i pi r / 2R}, so DFT_R(z)_k = theta_j (T[p_re][k] + i T[p_im][k]) where p_re / p_im
+// hold the R real / imaginary key bits of the butterfly and T[p][k] = sum_{r in p} c_r w_R^{rk}
+// = sum_{r in p} e^{i pi r (1 - 4k) / 2R} (each term an exactly-argued sincospi)
+__global__ void k_bits_table(uint32_t R, double2 *tb)
+{
+    for (uint32_t e = threadIdx.x; e < (1u << R) * R; e += blockDim.x) {
+        const uint32_t p = e / R, k = e % R;
+        double re = 0.0, im = 0.0;
+        for (uint32_t r = 0; r < R; ++r) {
+            if (!((p >> r) & 1u)) continue;
+            // angle r (1 - 4k) / 2R in half turns, reduced mod 2 exactly in integers
+            const int64_t num = ((int64_t)r * (1 - 4 * (int64_t)k)) % (int64_t)(4 * R);
+            double s, c;
+            sincospi((double)num / (double)(2 * R), &s, &c);
+            re += c;
+            im += s;
+        }
+        tb[e] = make_double2(re, im);
+    }
+}
+
 __global__ void k_tables(Geometry g, RouteTables T)
 {
     uint64_t tot = std::max<uint64_t>(std::max<uint64_t>(g.N1, g.N2), 64);
@@ -348,6 +370,42 @@ __device__ __forceinline__ void dit_t(double2 *sm, const FftPlan &P, int i0, int
     }
 }
 
+// K1's stage 0 (radix R, span N2, G = 1) straight from the key bits (k_bits_table): per
+// butterfly (column c, j < Ls) the R real and R imaginary bits of rows j + r Ls index the table,
+// v_k = theta_j (T[p_re][k] + i T[p_im][k]) * w_N2^{jk}, written where stage 0 writes.  Replaces
+// the z generation pass and stage 0's DFT.
+template <int R>
+__device__ __forceinline__ void k1_first_stage_bits(double2 *sm, const StageDesc &sd, uint32_t logC,
+                                                    const uint32_t *rowbits, const double2 *tb,
+                                                    const double2 *thlo, const double2 *thhi,
+                                                    const double2 *wlo, const double2 *whi)
+{
+    const uint32_t C = 1u << logC, twoC = 2 * C, epw = 32 / twoC;
+    const uint32_t nb = sd.nb << logC, cm = C - 1, stride = sd.Ls << logC;
+    for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
+        const uint32_t c = q & cm, j = q >> logC;
+        uint32_t pr = 0, pi = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t b = j + r * sd.Ls;
+            const uint32_t rb = rowbits[b / epw] >> ((b % epw) * twoC);
+            pr |= ((rb >> c) & 1u) << r;
+            pi |= ((rb >> (C + c)) & 1u) << r;
+        }
+        const double2 th = twiddle(thlo, thhi, j);
+        double2 v[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const double2 a = tb[pr * R + k], bi = tb[pi * R + k];
+            v[k] = cmul(make_double2(a.x - bi.y, a.y + bi.x), th);
+        }
+        if (j) apply_twiddles<R, false>(v, stage_twiddle(sd, j, wlo, whi));
+        const uint32_t base = (j << logC) + c;
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[pidx(base + r * stride)] = v[r];
+    }
+}
+
 template <int RA, int RB, int RC>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
@@ -361,12 +419,19 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     const uint32_t logC = g.logC, C = 1u << logC;
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
     uint32_t *rowbits = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
+    double2 *tb = reinterpret_cast<double2 *>(rowbits + g.kbw);  // g.ntb entries (first stage from bits)
+    // first stage from the key bits for R0 <= 4 only: same-box, R0 = 3 gains (C4 K1 781 -> 738 us,
+    // C5a 37.8 -> 35.8 us) but R0 = 5 / 7 lose (C2 37.9 -> 39.9 us, C3 188 -> 199 us: 2.5 / 14 KB
+    // tables, bank-conflicted lookups, more code)
+    constexpr bool kBits = RA >= 2 && RA <= 4;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
     TRACE_BEGIN(1);
     TSTAMPK(0, 0);
     load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
     load_tables_async(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    if (kBits)
+        for (uint32_t i = threadIdx.x; i < g.ntb; i += blockDim.x) cp_async16(tb + i, T.tb + i);
     grid_dep_wait();  // K0's bit streams
     if (zero_out) {  // K3 XORs this hash's output bits in (zero_words = 0: accumulate)
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
@@ -399,13 +464,19 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     TSTAMPK(0, 2);
     // z(b, c) = (x[a + N1 b] + i x[a + N1 b + M]) * theta_b; entry b of the stream holds
     // the C real-part bits then the C imaginary-part bits of row b
-    const uint32_t twoC = 2 * C, epw = 32 / twoC;
-    for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        const uint32_t b = e >> logC, c = e & (C - 1);
-        const uint32_t rb = rowbits[b / epw] >> ((b % epw) * twoC);
-        const double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (C + c)) & 1u);
-        const double2 th = twiddle(thlo, thhi, b);
-        sm[pidx(e)] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
+    int s0 = 0;  // first stage still to run
+    if (kBits && g.ntb) {
+        k1_first_stage_bits<kBits ? RA : 2>(sm, g.f2.st[0], logC, rowbits, tb, thlo, thhi, wlo, whi);
+        s0 = 1;
+    } else {
+        const uint32_t twoC = 2 * C, epw = 32 / twoC;
+        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
+            const uint32_t b = e >> logC, c = e & (C - 1);
+            const uint32_t rb = rowbits[b / epw] >> ((b % epw) * twoC);
+            const double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (C + c)) & 1u);
+            const double2 th = twiddle(thlo, thhi, b);
+            sm[pidx(e)] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
+        }
     }
     __syncthreads();
     TSTAMPK(0, 3);
@@ -413,7 +484,7 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     // stage writes it straight to global when C >= g.k1gout (2: 32-byte row pieces)
     const bool direct = g.f2.S > 1 && C >= g.k1gout;
     if (direct) {
-        dif_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+        dif_t<RA, RB, RC>(sm, g.f2, s0, g.f2.S - 1, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
         StageCtx gx;
         gx.gout = buf + a0;
@@ -421,7 +492,7 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
         stage_t<false, MODE_GCOL_OUT, RA, RB, RC>(sm, g.f2, g.f2.S - 1, logC, wlo, whi, gx);
         TSTAMPK(0, 4);
     } else {
-        dif_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+        dif_t<RA, RB, RC>(sm, g.f2, s0, g.f2.S, logC, wlo, whi);
         grid_dep_launch();  // K2 may start its prologue
         TSTAMPK(0, 4);
         for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
@@ -1166,6 +1237,22 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const char *e13 = getenv("PA_K13_T");
         g->k13 = (!e13 || atoi(e13) != 0) ? k13_shape(g->f2) : 0;
     }
+    // K1's first stage straight from the key bits through a 2^R0 x R0 table (radix R0 <= 4 of a
+    // shape-specialised K1, see k1_fwd_columns; not when the extra shared memory would cost a CTA
+    // per SM).
+    // Developer override PA_K1_BITS=0
+    g->ntb = 0;
+    {
+        const char *e = getenv("PA_K1_BITS");
+        const uint32_t R0 = g->f2.S ? g->f2.st[0].R : 16u;
+        if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 2 && R0 <= 4) {
+            const uint32_t ntb = (1u << R0) * R0, s1 = g->smem1 + ntb * 16;
+            if (s1 <= kSmemLimit && (2 * g->smem1 > kSmemLimit || 2 * s1 <= kSmemLimit)) {
+                g->ntb = ntb;
+                g->smem1 = s1;
+            }
+        }
+    }
     // row blocks for K2's output / K3's input (opt-in PA_LR=1): 128-byte K3 runs for 2- and
     // 4-column groups.  Bit-exact, but K2's stores become 32-byte pieces: C4 K3 725 -> 627, K2
     // 1119 -> 1208 us (net 0), C5d -1.8%, so row-major stays the default
@@ -1231,7 +1318,8 @@ static Geometry k3_geometry(const Geometry &g)
 
 static size_t ntables(const Geometry &g)
 {
-    return 64 + g.f1.nhi + g.f1.ntw + 64 + g.f2.nhi + g.f2.ntw + 64 + g.f2.nhi + (size_t)g.N2 * (64 + g.f1.nhi);
+    return 64 + g.f1.nhi + g.f1.ntw + 64 + g.f2.nhi + g.f2.ntw + 64 + g.f2.nhi + (size_t)g.N2 * (64 + g.f1.nhi) +
+           g.ntb;
 }
 static size_t kb_bytes(const Geometry &g) { return (size_t)(g.N1 / g.C) * g.kbw * 4; }
 
@@ -1310,6 +1398,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     T.thlo = p; p += 64;
     T.thhi = p; p += g.f2.nhi;
     T.rho = p; p += (size_t)g.N2 * (64 + g.f1.nhi);
+    T.tb = g.ntb ? p : nullptr; p += g.ntb;
 
     cudaError_t e;
     if ((e = cudaMemsetAsync(a.resid, 0, sizeof(unsigned long long), s)) != cudaSuccess)
@@ -1319,6 +1408,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     k_rho_tables<<<g.N2, 128, 0, s>>>(g, T);
     k_stage_tables<<<4, 256, 0, s>>>(g.f1, T.W1hi);
     k_stage_tables<<<4, 256, 0, s>>>(g.f2, T.W2hi);
+    if (g.ntb) k_bits_table<<<1, 256, 0, s>>>(g.f2.st[0].R, T.tb);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) table launch");
     h->kernels_per_hash = k1_direct(g) ? 3 : 4;
     return ra_seed(h, seed, s);
