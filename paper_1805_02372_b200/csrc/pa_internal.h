@@ -22,6 +22,7 @@ struct Geometry {
     uint32_t pfs;           // K2: L2 prefetch of the CTA's own spectrum row (one CTA per SM)
     uint32_t k1gout;        // K1's last stage stores to global directly when C >= k1gout
     uint32_t ntb;           // K1's first stage from the key bits: 2^R0 x R0 table entries (0 = off)
+    uint32_t k0rb, k0cb;    // K0 tile: rows x columns per CTA
     FftPlan f1, f2;         // stage plans of N1 (row pass) and N2 (strided passes)
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)
     uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)

@@ -274,8 +274,8 @@ __global__ void k_rho_tables(Geometry g, RouteTables T)
 constexpr uint32_t kK0Rows = 64, kK0Cols = 1024;  // largest tile (shared arrays sized for it)
 
 // tile rows x cols: 64 x 1024 for large transforms, 16 x 256 for small ones (more CTAs)
-__host__ __device__ inline uint32_t k0_rows(const Geometry &g) { return g.N2 >= 2048 ? 64 : 16; }
-__host__ __device__ inline uint32_t k0_cols(const Geometry &g) { return g.N1 >= 8192 ? 1024 : 256; }
+__host__ __device__ inline uint32_t k0_rows(const Geometry &g) { return g.k0rb; }
+__host__ __device__ inline uint32_t k0_cols(const Geometry &g) { return g.k0cb; }
 
 __global__ void __launch_bounds__(256)
 k0_bits_transpose(const uint32_t *__restrict__ w, uint64_t off, uint64_t nbits, uint32_t *__restrict__ kb,
@@ -1241,6 +1241,15 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // shape-specialised K1, see k1_fwd_columns; not when the extra shared memory would cost a CTA
     // per SM).
     // Developer override PA_K1_BITS=0
+    {
+        // K0 tile (developer overrides PA_K0_RB / PA_K0_CB).  Larger tiles (fewer CTAs) measured
+        // slower: C3 64 x 256 / 64 x 512 / 64 x 1024 -> K0 9.7-13.8 / 20.2 us vs 10.3 us at 16 x 256
+        const char *er = getenv("PA_K0_RB"), *ec = getenv("PA_K0_CB");
+        g->k0rb = er ? (uint32_t)atoi(er) : g->N2 >= 2048 ? 64u : 16u;
+        g->k0cb = ec ? (uint32_t)atoi(ec) : g->N1 >= 8192 ? 1024u : 256u;
+        if (g->k0rb % 16 || g->k0rb > kK0Rows || g->k0rb == 0) g->k0rb = 16;
+        if (g->k0cb % 32 || g->k0cb > kK0Cols || g->k0cb == 0) g->k0cb = 256;
+    }
     g->ntb = 0;
     {
         const char *e = getenv("PA_K1_BITS");
