@@ -423,7 +423,7 @@ def sweep(torch, pa, dev, steps=10):
     h.close()
     # fresh seed per key (NEXT-2): seed transform + hash per key, C2 shape
     n, m, sw, kw = syn.config_inputs("C2")
-    count = 8
+    count = 64
     seeds = torch.stack([dev_words(torch, syn.random_bits(syn.seed_stream(900 + k), n + m - 1), dev)
                          for k in range(count)])
     keys = torch.stack([dev_words(torch, kw, dev)] * count)
@@ -433,7 +433,8 @@ def sweep(torch, pa, dev, steps=10):
     ms = time_steps(torch, lambda: h.hash_fresh_batch(seeds, keys, outs), 3, flush)
     t = float(np.mean(ms)) / count
     res["C2_fresh_seed"] = {"n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
-                            "note": "pa_hash_fresh_batch: new seed transform + hash per key"}
+                            "note": "pa_hash_fresh_batch: a distinct seed per key; the chunk's seeds transformed "
+                                    "as one batch into per-key spectra, then its keys hashed as one batch"}
     h.close()
     return res
 

@@ -145,8 +145,12 @@ pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream);
 /* Fresh seed per key (Sec. 2.3 Step 1: every privacy-amplification round draws a
  * new uniform seed): for k < count, rebind the handle to seed k (seeds +
  * k*seed_stride_words, n+m-1 bits at the handle's seed_bit_offset) and hash key k into
- * output k -- pa_set_seed + pa_hash per key, i.e. three transforms per key on route (a).
- * Strides in uint32 words, multiples of 4.  Afterwards the handle holds the last seed. */
+ * output k -- the result of pa_set_seed + pa_hash per key, i.e. three transforms per key on
+ * route (a).  An unsplit route-(a) handle without a workspace transforms the seeds of a chunk of
+ * keys as one batch into per-key spectra (extra device memory: chunk x the spectrum, grown on
+ * demand) and hashes the chunk's keys as one batch; otherwise (or if that memory is not
+ * available) one key at a time.  Strides in uint32 words, multiples of 4.  Afterwards the
+ * handle holds the last seed. */
 pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_stride_words,
                               const uint32_t *keys, uint64_t key_stride_words, uint32_t *outs,
                               uint64_t out_stride_words, uint32_t count, void *stream);

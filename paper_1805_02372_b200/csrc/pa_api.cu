@@ -689,7 +689,12 @@ pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_
     if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    for (uint32_t k = 0; k < count; ++k) {
+    if (h->route == PA_ROUTE_TRANSFORM && !h->nsub) {  // batched seed transforms + batched hashes
+        st = ra_fresh_batch(h, seeds, seed_stride_words, keys, key_stride_words, outs, out_stride_words, count,
+                            (h->m + 31) / 32, s);
+        if (st != PA_ERR_UNSUPPORTED && st != PA_ERR_NOMEM) return st;
+    }
+    for (uint32_t k = 0; k < count; ++k) {  // one key at a time: set_seed + hash (less memory)
         if ((st = seed_impl(h, seeds + k * seed_stride_words, s)) != PA_OK) return st;
         if ((st = hash_impl(h, keys + k * key_stride_words, outs + k * out_stride_words, (h->m + 31) / 32, s,
                             false)) != PA_OK)

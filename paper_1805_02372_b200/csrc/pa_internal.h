@@ -57,6 +57,8 @@ struct RouteA {
     uint32_t *kb = nullptr;    // K0 output: per-column-group bit streams of the input
     uint32_t cap = 0;          // keys the work buffers (buf, kb) hold
     bool shared_w = false;     // work block borrowed from the first column block (not owned)
+    double2 *fspec = nullptr;  // pa_hash_fresh_batch: one spectrum per key of a chunk
+    uint32_t fcap = 0;         // keys fspec holds
 };
 
 // ---------------------------------------------------------------- route (b)
@@ -143,7 +145,11 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,
                   cudaStream_t s);
 pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
-                        uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s);
+                        uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s,
+                        const double2 *spec = nullptr, uint64_t spec_stride = 0);
+pa_status ra_fresh_batch(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride, const uint32_t *keys,
+                         uint64_t key_stride, uint32_t *outs, uint64_t out_stride, uint32_t count,
+                         uint64_t zero_words, cudaStream_t s);
 uint32_t ra_batch_keys(const pa_ctx *h);
 void ra_destroy(pa_ctx *h);
 

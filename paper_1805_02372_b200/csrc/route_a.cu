@@ -542,7 +542,7 @@ __device__ __forceinline__ void fused_mid_any(const StageDesc &sd, double2 *sm, 
 // mode 1 (create): buf row -> tau -> DIF -> * scale -> spec row.
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, RouteTables T, int mode,
-        double scale)
+        double scale, uint64_t spec_stride)
 {
     // buf and out2 may be the same array (K2 in place when lr = 0): no __restrict__ on them
     extern __shared__ double2 sm[];
@@ -557,7 +557,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;  // input row (row-major)
     double2 *rq = out2 + wrow(g, row);        // output row: element a at rq[wcol(g, a)]
-    double2 *sp = spec + (uint64_t)row * N1;
+    double2 *sp = spec + blockIdx.x * spec_stride + (uint64_t)row * N1;  // per-key spectra: fresh seeds
     load_tables_async(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
@@ -647,7 +647,8 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 #endif
 template <int R0, int R1>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
-k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T)
+k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T,
+          uint64_t spec_stride)
 {
     extern __shared__ double2 sm[];
     const uint32_t N1 = g.N1;
@@ -659,7 +660,7 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *rq = out2 + wrow(g, row);
-    const double2 *sp = spec + (uint64_t)row * N1;
+    const double2 *sp = spec + blockIdx.x * spec_stride + (uint64_t)row * N1;
     load_tables_async(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
@@ -1454,7 +1455,7 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
     kK13[g.k13].k1<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
-    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M);
+    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M, 0);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) seed transform launches");
     return PA_OK;
 }
@@ -1517,7 +1518,8 @@ uint32_t ra_batch_keys(const pa_ctx *h)
 }
 
 pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
-                        uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s)
+                        uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s,
+                        const double2 *spec, uint64_t spec_stride)
 {
     pa_status st = ra_reserve(h, count);
     if (st != PA_OK) return st;
@@ -1537,13 +1539,14 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
     prof_begin(h, 1, s);
     {
         const dim3 g2(count, g.N2);
-        const double2 *sp = a.spec;
+        const double2 *sp = spec ? spec : a.spec;  // fresh seeds: one spectrum per key
+        const uint64_t ss = spec ? spec_stride : 0;
         switch (g.k2shape) {
-        case 1: launch_pdl(k2_rows_t<16, 16>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
-        case 2: launch_pdl(k2_rows_t<5, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
-        case 3: launch_pdl(k2_rows_t<3, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
-        case 4: launch_pdl(k2_rows_t<7, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T); break;
-        default: launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, a.spec, g, a.T, 0, 1.0);
+        case 1: launch_pdl(k2_rows_t<16, 16>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 2: launch_pdl(k2_rows_t<5, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 3: launch_pdl(k2_rows_t<3, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 4: launch_pdl(k2_rows_t<7, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        default: launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
         }
     }
     prof_end(h, s);
@@ -1568,6 +1571,55 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
     return ra_hash_batch(h, key, 0, out, 0, 1, zero_words, s);
 }
 
+// Fresh seed per key, batched (pa_hash_fresh_batch): for chunks of the work buffers' capacity,
+// the chunk's seeds are transformed as one batch (K0 -> K1 -> K2 mode 1, grid over keys) into
+// per-key spectra, then its keys are hashed as one batch against them.  Afterwards the handle's
+// own spectrum is the last seed's (one device copy).  PA_ERR_UNSUPPORTED: caller loops instead.
+pa_status ra_fresh_batch(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride, const uint32_t *keys,
+                         uint64_t key_stride, uint32_t *outs, uint64_t out_stride, uint32_t count,
+                         uint64_t zero_words, cudaStream_t s)
+{
+    RouteA &a = h->a;
+    const Geometry &g = a.g;
+    const uint32_t chunk = std::min(count, ra_batch_keys(h));
+    const size_t spec_bytes = (size_t)g.M * sizeof(double2);
+    if (h->arena || h->parent || chunk < 2 || (size_t)chunk * spec_bytes > (size_t(4) << 30))
+        return PA_ERR_UNSUPPORTED;
+    pa_status st = ra_reserve(h, chunk);
+    if (st != PA_OK) return st;
+    if (a.fcap < chunk) {
+        cudaStreamSynchronize(s);  // the old spectra may still be read by enqueued hashes
+        dev_free(h, a.fspec);
+        h->ws_bytes -= (size_t)a.fcap * spec_bytes;
+        a.fspec = nullptr;
+        a.fcap = 0;
+        if ((st = dev_alloc(h, (void **)&a.fspec, (size_t)chunk * spec_bytes, "fresh-seed spectra")) != PA_OK)
+            return st;
+        a.fcap = chunk;
+    }
+    for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
+        const uint32_t c = std::min(chunk, count - k0);
+        const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), c);
+        launch_pdl(k0_bits_transpose, g0, dim3(256), 0, s, seeds + k0 * seed_stride, h->off, h->L, a.kb, g,
+                   seed_stride);
+        launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, c), g.t1, g.smem1, s, (const uint32_t *)a.kb, a.buf, g, a.T,
+                   (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0, (const uint32_t *)nullptr, (uint64_t)0,
+                   (uint64_t)0);
+        launch_pdl(k2_rows, dim3(c, g.N2), g.t2, g.smem2, s, a.buf, a.buf, a.fspec, g, a.T, 1, 1.0 / (double)g.M,
+                   (uint64_t)g.M);
+        if ((st = ra_hash_batch(h, keys + k0 * key_stride, key_stride, outs + k0 * out_stride, out_stride, c,
+                                zero_words, s, a.fspec, g.M)) != PA_OK)
+            return st;
+        if (k0 + c == count) {
+            cudaError_t e = cudaMemcpyAsync(a.spec, a.fspec + (size_t)(c - 1) * g.M, spec_bytes,
+                                            cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e, "fresh-seed spectrum copy");
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PA_OK : cuda_fail(e, "fresh-seed batch launches");
+}
+
 #ifdef PA_TIMING
 extern "C" int pa_debug_k2_clocks(unsigned long long *out)
 {
@@ -1584,6 +1636,7 @@ void ra_destroy(pa_ctx *h)
     RouteA &a = h->a;
     dev_free(h, a.pblk);
     if (!a.shared_w) dev_free(h, a.wblk);
+    dev_free(h, a.fspec);
     a = RouteA{};
 }
 

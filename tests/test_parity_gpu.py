@@ -511,20 +511,25 @@ def test_max_transform_len_too_small_is_unsupported():
 
 
 # ---------------------------------------------------------------- fresh seed per key
-@pytest.mark.parametrize("route,maxlen", [("bitpacked", 0), ("transform", 0), ("transform", 150_000)])
-def test_hash_fresh_batch_per_key_seeds(route, maxlen):
-    """NEXT-2: key k hashed with its own seed k, three transforms per key."""
+@pytest.mark.parametrize("route,maxlen,count", [("bitpacked", 0, 5), ("transform", 0, 5), ("transform", 150_000, 5),
+                                                ("transform", 0, 70), ("transform", 0, 1)])
+def test_hash_fresh_batch_per_key_seeds(route, maxlen, count):
+    """NEXT-2: key k hashed with its own seed k, three transforms per key.  Unsplit route
+    (a) transforms a chunk's seeds as one batch into per-key spectra and hashes the chunk against
+    them (70 keys: two chunks, the second ragged); afterwards the handle holds the last seed."""
     n, m = (3_001, 1_000) if route == "bitpacked" else (120_001, 30_000)
-    count = 5
     seeds = [syn.random_bits(syn.seed_stream(70 + k), n + m - 1) for k in range(count)]
     keys = [syn.random_bits(syn.key_stream(70, k), n) for k in range(count)]
     st, kt = torch.stack([to_dev(s) for s in seeds]), torch.stack([to_dev(k) for k in keys])
+    probe = syn.random_bits(syn.key_stream(71, 0), n)
     with pa.Hasher(n, m, st[0], route=route, max_transform_len=maxlen) as h:
         outs = h.hash_fresh_batch(st, kt)
+        after = from_dev(h.hash(to_dev(probe)), m)
         torch.cuda.synchronize()
     for k in range(count):
         want = oracle.unpack(oracle.toeplitz_words(n, m, seeds[k], keys[k]), m)
         assert np.array_equal(from_dev(outs[k], m), want), k
+    assert np.array_equal(after, oracle.unpack(oracle.toeplitz_words(n, m, seeds[-1], probe), m))
 
 
 # ---------------------------------------------------------------- Eq. (1) seed converter
