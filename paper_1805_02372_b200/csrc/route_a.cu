@@ -40,6 +40,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include "bits.cuh"
@@ -1431,7 +1432,12 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     RouteA &a = h->a;
     const Geometry &g = a.g;
     cudaError_t e;
-    // per call: the attribute is per device and a process may drive several
+    // the attribute is per device (a process may drive several): set once per device
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = dev < 64 ? 1ull << dev : 0;
+    if (bit && (attr_done.load() & bit)) goto launch;
     for (const K13 &f : kK13)
         if ((e = cudaFuncSetAttribute(f.k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
                 cudaSuccess ||
@@ -1452,6 +1458,8 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         (e = cudaFuncSetAttribute(k3t_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
+    attr_done.fetch_or(bit);
+launch:
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
     k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
     kK13[g.k13].k1<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
