@@ -646,7 +646,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 #ifndef K2T_STAGE
 #define K2T_STAGE stage_inl
 #endif
-template <int R0, int R1>
+template <int R0, int R1, int NS>
 __global__ void __launch_bounds__(PA_TMAX, PA_MINB)
 k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T,
           uint64_t spec_stride)
@@ -691,15 +691,17 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     }
     K2T_STAGE<R1, false, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
     __syncthreads();
-    for (int i = 2; i < P.S - 1; ++i) {
+#pragma unroll
+    for (int i = 2; i < NS - 1; ++i) {
         K2T_STAGE<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
     TSTAMP(3);
-    fused_mid<16>(P.st[P.S - 1], sm, sp);
+    fused_mid<16>(P.st[NS - 1], sm, sp);
     __syncthreads();
     TSTAMP(4);
-    for (int i = P.S - 2; i >= 2; --i) {
+#pragma unroll
+    for (int i = NS - 2; i >= 2; --i) {
         K2T_STAGE<16, true, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
         __syncthreads();
     }
@@ -722,8 +724,9 @@ static int k2_shape(const FftPlan &p)
     if (p.S < 3) return 0;
     for (int i = 2; i < p.S; ++i)
         if (p.st[i].R != 16) return 0;
-    const uint32_t a = p.st[0].R, b = p.st[1].R;
-    return a == 16 && b == 16 ? 1 : a == 5 && b == 8 ? 2 : a == 3 && b == 8 ? 3 : a == 7 && b == 4 ? 4 : 0;
+    const uint32_t a = p.st[0].R, b = p.st[1].R;  // the stage count is a template parameter too
+    return a == 16 && b == 16 && p.S == 3 ? 1 : a == 5 && b == 8 && p.S == 4 ? 2 : a == 3 && b == 8 && p.S == 4 ? 3
+           : a == 7 && b == 4 && p.S == 4 ? 4 : 0;
 }
 
 
@@ -1447,13 +1450,13 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     if (
         (e = cudaFuncSetAttribute(k2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (e = cudaFuncSetAttribute(k2_rows_t<16, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<5, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (e = cudaFuncSetAttribute(k2_rows_t<5, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (e = cudaFuncSetAttribute(k2_rows_t<3, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<7, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (e = cudaFuncSetAttribute(k2_rows_t<7, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k3t_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
@@ -1550,10 +1553,10 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         const double2 *sp = spec ? spec : a.spec;  // fresh seeds: one spectrum per key
         const uint64_t ss = spec ? spec_stride : 0;
         switch (g.k2shape) {
-        case 1: launch_pdl(k2_rows_t<16, 16>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        case 2: launch_pdl(k2_rows_t<5, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        case 3: launch_pdl(k2_rows_t<3, 8>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        case 4: launch_pdl(k2_rows_t<7, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 1: launch_pdl(k2_rows_t<16, 16, 3>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 2: launch_pdl(k2_rows_t<5, 8, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 3: launch_pdl(k2_rows_t<3, 8, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
+        case 4: launch_pdl(k2_rows_t<7, 4, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
         default: launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
         }
     }
