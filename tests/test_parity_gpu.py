@@ -532,6 +532,32 @@ def test_hash_fresh_batch_per_key_seeds(route, maxlen, count):
     assert np.array_equal(after, oracle.unpack(oracle.toeplitz_words(n, m, seeds[-1], probe), m))
 
 
+@pytest.mark.parametrize("n,m,off,count,kwargs", [(120_001, 30_000, 77, 9, {}), (1_000_003, 250_000, 5, 4, {}),
+                                                   (50_001, 9_000, 3, 6, {"batch_keys": 2})])
+def test_hash_fresh_batch_seed_offset_and_workspace(n, m, off, count, kwargs):
+    """Fresh seeds at a seed_bit_offset (each row's window starts `off` bits in; the batched seed
+    transform reads it through K0's offset), on a large shape (sampled rows) and on a
+    workspace-backed handle (one key at a time)."""
+    L = n + m - 1
+    raw = [syn.random_bits(syn.seed_stream(130 + k), off + L) for k in range(count)]
+    win = [oracle.pack(oracle.unpack(r, off + L)[off:], 32) for r in raw]  # the window, re-based
+    keys = [syn.random_bits(syn.key_stream(130, k), n) for k in range(count)]
+    st, kt = torch.stack([to_dev(r) for r in raw]), torch.stack([to_dev(k) for k in keys])
+    ws = None
+    opts = dict(kwargs)
+    if "batch_keys" in opts:
+        nbytes = pa.workspace_size(n, m, route="transform", seed_bit_offset=off, batch_keys=opts["batch_keys"])
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+        opts["workspace"] = ws
+    with pa.Hasher(n, m, st[0], route="transform", seed_bit_offset=off, **opts) as h:
+        outs = h.hash_fresh_batch(st, kt)
+        torch.cuda.synchronize()
+    rows = sample_rows(m, 13, 512)
+    for k in range(count):
+        got = from_dev(outs[k], m)
+        assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, win[k], keys[k], rows)), k
+
+
 # ---------------------------------------------------------------- Eq. (1) seed converter
 @pytest.mark.parametrize("n,m", [(1, 1), (3, 2), (31, 2), (32, 32), (33, 7), (100, 61), (4096, 1024),
                                  (100_003, 9_999)])
