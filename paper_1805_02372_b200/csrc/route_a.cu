@@ -1022,7 +1022,7 @@ struct K13 {
 };
 static const K13 kK13[] = {
     {0, 0, 0, k1_fwd_columns<0, 0, 0>, k3_inv_columns<0, 0, 0>},
-    {5, 2, 0, k1_fwd_columns<5, 2, 0>, k3_inv_columns<5, 2, 0>},
+    {2, 5, 0, k1_fwd_columns<2, 5, 0>, k3_inv_columns<2, 5, 0>},
     {7, 3, 4, k1_fwd_columns<7, 3, 4>, k3_inv_columns<7, 3, 4>},
     {3, 8, 0, k1_fwd_columns<3, 8, 0>, k3_inv_columns<3, 8, 0>},
     {3, 3, 0, k1_fwd_columns<3, 3, 0>, k3_inv_columns<3, 3, 0>},
@@ -1056,7 +1056,13 @@ std::vector<uint32_t> smooth_numbers(uint32_t limit)
     return v;
 }
 
-bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16)
+static bool asc_off()  // developer override PA_K13_ASC=0: K1/K3 plans in the default radix order
+{
+    const char *e = getenv("PA_K13_ASC");
+    return e && atoi(e) == 0;
+}
+
+bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16, bool ascending = false)
 {
     uint32_t L = Lt;
     int e2 = 0, e3 = 0, e5 = 0, e7 = 0;
@@ -1084,6 +1090,12 @@ bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16)
         if (e2 % 3 == 2) push(4);
         for (int i = 0; i < e2 / 3; ++i) push(8);
     }
+    // ascending radices (K1/K3 plans of 16-column groups, where the lanes of a warp span the
+    // columns and stage order does not matter for banks): the smallest radix comes first, so
+    // K1's first stage can read the key bits through a small table (k_bits_table).  C2: [2, 5,
+    // 16], K1 14.0 -> 13.2 us; for 8-column groups (C5b [4, 7, 16]) it measured slower (K1 22.9
+    // -> 25.3 us) and they keep the default order
+    if (ascending) std::stable_sort(R, R + S);
     P->S = S;
     P->Lt = Lt;
     P->nhi = (Lt + 63) / 64;
@@ -1216,7 +1228,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     g->logC = logC;
     const char *r1 = getenv("PA_FORCE_RMAX1");  // developer override: row-plan radix cap
     make_plan(g->N1, &g->f1, r1 ? (uint32_t)atoi(r1) : 16);
-    make_plan(g->N2, &g->f2);
+    make_plan(g->N2, &g->f2, 16, g->C >= 16 && !asc_off());
     g->tile1 = tile_bytes((uint64_t)g->N2 * g->C) / 16;
     g->tile2 = tile_bytes(g->N1) / 16;
     g->smem1 = smem_k13(g->N2, g->C, g->f2);
