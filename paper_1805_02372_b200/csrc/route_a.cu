@@ -1009,8 +1009,8 @@ k3t_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
-// K1 / K3 instantiations for column plans [A, B, (C), 16, ...]: 0 general, then C2 [5, 2, 16],
-// C3 [7, 3, 4, 16], C4 [3, 8, 16, 16], C5a/c [3, 3, 16(, 16)], C5b [7, 4, 16], C5d [7, 3, 8, 16]
+// K1 / K3 instantiations for column plans [A, B, (C), 16, ...]: 0 general, then C2 [2, 5, 16],
+// C3 [3, 4, 7, 16], C4 [3, 8, 16, 16], C5a/c [3, 3, 16(, 16)], C5b [7, 4, 16], C5d [3, 7, 8, 16]
 using K1Fn = void (*)(const uint32_t *, double2 *, Geometry, RouteTables, uint32_t *, uint64_t, uint64_t,
                       const uint32_t *, uint64_t, uint64_t);
 using K3Fn = void (*)(const double2 *, Geometry, RouteTables, uint64_t, uint64_t, uint32_t *, unsigned long long *,
@@ -1023,11 +1023,11 @@ struct K13 {
 static const K13 kK13[] = {
     {0, 0, 0, k1_fwd_columns<0, 0, 0>, k3_inv_columns<0, 0, 0>},
     {2, 5, 0, k1_fwd_columns<2, 5, 0>, k3_inv_columns<2, 5, 0>},
-    {7, 3, 4, k1_fwd_columns<7, 3, 4>, k3_inv_columns<7, 3, 4>},
+    {3, 4, 7, k1_fwd_columns<3, 4, 7>, k3_inv_columns<3, 4, 7>},
     {3, 8, 0, k1_fwd_columns<3, 8, 0>, k3_inv_columns<3, 8, 0>},
     {3, 3, 0, k1_fwd_columns<3, 3, 0>, k3_inv_columns<3, 3, 0>},
     {7, 4, 0, k1_fwd_columns<7, 4, 0>, k3_inv_columns<7, 4, 0>},
-    {7, 3, 8, k1_fwd_columns<7, 3, 8>, k3_inv_columns<7, 3, 8>},
+    {3, 7, 8, k1_fwd_columns<3, 7, 8>, k3_inv_columns<3, 7, 8>},
 };
 
 static int k13_shape(const FftPlan &p)
@@ -1090,11 +1090,7 @@ bool make_plan(uint32_t Lt, FftPlan *P, uint32_t rmax = 16, bool ascending = fal
         if (e2 % 3 == 2) push(4);
         for (int i = 0; i < e2 / 3; ++i) push(8);
     }
-    // ascending radices (K1/K3 plans of 16-column groups, where the lanes of a warp span the
-    // columns and stage order does not matter for banks): the smallest radix comes first, so
-    // K1's first stage can read the key bits through a small table (k_bits_table).  C2: [2, 5,
-    // 16], K1 14.0 -> 13.2 us; for 8-column groups (C5b [4, 7, 16]) it measured slower (K1 22.9
-    // -> 25.3 us) and they keep the default order
+    // ascending: the smallest radix first (K1/K3, see ra_plan)
     if (ascending) std::stable_sort(R, R + S);
     P->S = S;
     P->Lt = Lt;
@@ -1228,7 +1224,16 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     g->logC = logC;
     const char *r1 = getenv("PA_FORCE_RMAX1");  // developer override: row-plan radix cap
     make_plan(g->N1, &g->f1, r1 ? (uint32_t)atoi(r1) : 16);
-    make_plan(g->N2, &g->f2, 16, g->C >= 16 && !asc_off());
+    // K1/K3: the radices in ascending order when that puts a radix-2 or -3 stage first (K1 then
+    // reads the key bits through an 8- or 24-entry table, k_bits_table).  Same-box: C2 [2, 5, 16]
+    // K1 14.2 -> 12.8 us (bench 26.4 -> 27.1 Gbit/s), C3 [3, 4, 7, 16] 186.4 -> 182.3 us, C5d
+    // [3, 7, 8, 16] 1005.6 -> 983 us; C5b's [4, 7, 16] (radix 4 first) measured slower and keeps
+    // [7, 4, 16]
+    make_plan(g->N2, &g->f2);
+    if (!asc_off()) {
+        FftPlan q;
+        if (make_plan(g->N2, &q, 16, true) && q.S >= 2 && q.st[0].R <= 3 && q.st[0].R < g->f2.st[0].R) g->f2 = q;
+    }
     g->tile1 = tile_bytes((uint64_t)g->N2 * g->C) / 16;
     g->tile2 = tile_bytes(g->N1) / 16;
     g->smem1 = smem_k13(g->N2, g->C, g->f2);
