@@ -302,6 +302,44 @@ __device__ __forceinline__ void stage_inl(double2 *sm, const StageDesc &sd, uint
     const uint32_t cm = (1u << logC) - 1;
     const uint32_t stride = sd.Ls << logC;
     const uint32_t nth = x.nth ? x.nth : blockDim.x;
+    if constexpr (MODE == MODE_TAU_IN && R <= 8) {
+        // K2's first stage from global with several butterflies per thread (10240-point rows):
+        // the next butterfly's row loads are issued before this one's arithmetic
+        if (x.gin) {
+            auto first = [&](uint32_t q) {
+                const uint32_t t = q >> logC, g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
+                return g * sd.L + (t - g * sd.Ls);
+            };
+            double2 nv[R];
+            uint32_t q = threadIdx.x;
+            if (q < nb) {
+                const uint32_t i0 = first(q);
+#pragma unroll
+                for (int r = 0; r < R; ++r) nv[r] = x.gin[grow_off(x, i0 + r * sd.Ls)];
+            }
+            for (; q < nb; q += nth) {
+                const uint32_t c = q & cm, t = q >> logC;
+                const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
+                const uint32_t j = t - g * sd.Ls;
+                const uint32_t idx0 = g * sd.L + j;
+                const uint32_t base = (idx0 << logC) + c;
+                double2 v[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = nv[r];
+                if (q + nth < nb) {
+                    const uint32_t i1 = first(q + nth);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) nv[r] = x.gin[grow_off(x, i1 + r * sd.Ls)];
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
+                butterfly<R, INV>(v, j, sd, wlo, whi);
+#pragma unroll
+                for (int r = 0; r < R; ++r) sm[pidx(base + r * stride)] = v[r];
+            }
+            return;
+        }
+    }
     for (uint32_t q = threadIdx.x; q < nb; q += nth) {
         const uint32_t c = q & cm, t = q >> logC;
         const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
