@@ -754,9 +754,15 @@ __device__ __forceinline__ void k3_window_rows(const Geometry &g, uint32_t a0, u
 // Window + parity + packing of one column group (threads tid, tid + nth, ...; nth a multiple
 // of 32 and of C).  Element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M].
 // Returns this thread's largest |v - rint v| over window values.
+// FR = 2 or 3: the last inverse stage (radix FR, span N2, Ls = N2 / FR) is not run over the
+// whole tile; each window element takes it here from the previous stage's output instead:
+// row b = j + k Ls gets sum_r v[j + r Ls] conj(w_N2^{r b}) (the stage's twiddle and inverse
+// DFT_R in one), so only window rows pay for it.
+template <int FR = 0>
 __device__ __forceinline__ double k3_epilogue(const double2 *sm, const Geometry &g, uint32_t a0, uint32_t logC,
                                               uint64_t n, uint64_t m, const double2 *thlo, const double2 *thhi,
-                                              uint32_t *out, uint32_t b_lo, uint32_t b_hi, uint32_t tid, uint32_t nth)
+                                              uint32_t *out, uint32_t b_lo, uint32_t b_hi, uint32_t tid, uint32_t nth,
+                                              const double2 *wlo = nullptr, const double2 *whi = nullptr)
 {
     const uint32_t C = 1u << logC;
     const int64_t t0 = (int64_t)n - 1, t1 = t0 + (int64_t)m;
@@ -767,7 +773,18 @@ __device__ __forceinline__ double k3_epilogue(const double2 *sm, const Geometry 
     const uint32_t e_hi = b_hi > b_lo ? (b_hi << logC) : 0;
     for (uint32_t e = e_lo + tid; e < e_hi; e += nth) {
         const uint32_t b = e >> logC, c = e & (C - 1);
-        const double2 wv = cmulc(sm[pidx(e)], twiddle(thlo, thhi, b));
+        double2 x;
+        if constexpr (FR == 2 || FR == 3) {
+            const uint32_t Ls = g.N2 / FR;
+            const uint32_t k = b >= Ls ? (FR == 3 && b >= 2 * Ls ? 2u : 1u) : 0u;
+            const uint32_t j = b - k * Ls;
+            const double2 w1 = twiddle(wlo, whi, b);  // w_N2^b
+            x = cadd(sm[pidx((j << logC) + c)], cmulc(sm[pidx(((j + Ls) << logC) + c)], w1));
+            if (FR == 3) x = cadd(x, cmulc(sm[pidx(((j + 2 * Ls) << logC) + c)], cmul(w1, w1)));
+        } else {
+            x = sm[pidx(e)];
+        }
+        const double2 wv = cmulc(x, twiddle(thlo, thhi, b));
         const int64_t u = (int64_t)a0 + c + (int64_t)g.N1 * b;
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
@@ -817,6 +834,9 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
+    // the last inverse stage (radix RA = 2 or 3 of a specialised plan, S >= 2) is taken inside
+    // the epilogue for the window rows only
+    constexpr bool kFuse = RA == 2 || RA == 3;
     TRACE_BEGIN(3);
     TSTAMPK(2, 0);
     load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
@@ -843,13 +863,13 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
         gx.lc = logC;
         stage_t<true, MODE_GCOL, RA, RB, RC>(sm, g.f2, g.f2.S - 1, logC, wlo, whi, gx);
         __syncthreads();
-        dit_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S - 1, logC, wlo, whi);
+        dit_t<RA, RB, RC>(sm, g.f2, kFuse ? 1 : 0, g.f2.S - 1, logC, wlo, whi);
     } else {
-        dit_t<RA, RB, RC>(sm, g.f2, 0, g.f2.S, logC, wlo, whi);
+        dit_t<RA, RB, RC>(sm, g.f2, kFuse ? 1 : 0, g.f2.S, logC, wlo, whi);
     }
     TSTAMPK(2, 2);
-    const double rmax = k3_epilogue(sm, g, a0, logC, n, m, thlo, thhi, out, (uint32_t)b_lo, (uint32_t)b_hi,
-                                    threadIdx.x, blockDim.x);
+    const double rmax = k3_epilogue<kFuse ? RA : 0>(sm, g, a0, logC, n, m, thlo, thhi, out, (uint32_t)b_lo,
+                                                    (uint32_t)b_hi, threadIdx.x, blockDim.x, wlo, whi);
     TSTAMPK(2, 3);
     k3_residual(rmax, resid);
     TRACE_END(3);
