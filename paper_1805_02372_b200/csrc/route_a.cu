@@ -754,7 +754,7 @@ __device__ __forceinline__ void k3_window_rows(const Geometry &g, uint32_t a0, u
 // Window + parity + packing of one column group (threads tid, tid + nth, ...; nth a multiple
 // of 32 and of C).  Element (b, c) is w[u], u = a0 + c + N1 b; Re -> c[u], Im -> c[u + M].
 // Returns this thread's largest |v - rint v| over window values.
-// FR = 2 or 3: the last inverse stage (radix FR, span N2, Ls = N2 / FR) is not run over the
+// FR >= 2: the last inverse stage (radix FR, span N2, Ls = N2 / FR) is not run over the
 // whole tile; each window element takes it here from the previous stage's output instead:
 // row b = j + k Ls gets sum_r v[j + r Ls] conj(w_N2^{r b}) (the stage's twiddle and inverse
 // DFT_R in one), so only window rows pay for it.
@@ -774,13 +774,17 @@ __device__ __forceinline__ double k3_epilogue(const double2 *sm, const Geometry 
     for (uint32_t e = e_lo + tid; e < e_hi; e += nth) {
         const uint32_t b = e >> logC, c = e & (C - 1);
         double2 x;
-        if constexpr (FR == 2 || FR == 3) {
-            const uint32_t Ls = g.N2 / FR;
-            const uint32_t k = b >= Ls ? (FR == 3 && b >= 2 * Ls ? 2u : 1u) : 0u;
-            const uint32_t j = b - k * Ls;
+        if constexpr (FR >= 2) {
+            const uint32_t Ls = g.f2.st[0].Ls;
+            const uint32_t j = b - (uint32_t)(((uint64_t)b * g.f2.st[0].magic) >> 40) * Ls;  // b mod Ls
             const double2 w1 = twiddle(wlo, whi, b);  // w_N2^b
+            double2 p = w1;
             x = cadd(sm[pidx((j << logC) + c)], cmulc(sm[pidx(((j + Ls) << logC) + c)], w1));
-            if (FR == 3) x = cadd(x, cmulc(sm[pidx(((j + 2 * Ls) << logC) + c)], cmul(w1, w1)));
+#pragma unroll
+            for (int r = 2; r < FR; ++r) {
+                p = cmul(p, w1);  // w_N2^{r b}
+                x = cadd(x, cmulc(sm[pidx(((j + r * Ls) << logC) + c)], p));
+            }
         } else {
             x = sm[pidx(e)];
         }
@@ -834,9 +838,9 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
     const uint32_t a0 = blockIdx.x * C;
     const uint32_t tot = g.N2 << logC;
-    // the last inverse stage (radix RA = 2 or 3 of a specialised plan, S >= 2) is taken inside
-    // the epilogue for the window rows only
-    constexpr bool kFuse = RA == 2 || RA == 3;
+    // the last inverse stage (radix RA <= 7 of a specialised plan, S >= 2) is taken inside the
+    // epilogue for the window rows only
+    constexpr bool kFuse = RA >= 2 && RA <= 7;
     TRACE_BEGIN(3);
     TSTAMPK(2, 0);
     load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
