@@ -1,6 +1,6 @@
 import ctypes, os, sys
 import numpy as np, torch
-os.environ["PA_LIB"] = os.path.join(os.getcwd(), "paper_1805_02372_b200/libpa_T.so")
+os.environ.setdefault("PA_LIB", os.path.join(os.getcwd(), "paper_1805_02372_b200/libpa_T.so"))
 sys.path.insert(0, os.getcwd())
 import pa_synth as syn, paper_1805_02372_b200 as pa
 from paper_1805_02372_b200 import _lib
