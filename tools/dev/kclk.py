@@ -11,8 +11,13 @@ for name in sys.argv[1:]:
     dw = lambda w: torch.from_numpy(np.ascontiguousarray(w).view(np.int32).copy()).cuda()
     h = pa.Hasher(n, m, dw(sw)); key = dw(kw); out = h.new_out()
     for _ in range(3): h.hash(key, out)
-    if os.environ.get("COLD"):  # flush L2 before the recorded hash
-        torch.empty(256 << 20, dtype=torch.uint8, device="cuda").zero_()
+    if os.environ.get("COLD"):  # flush L2 before the recorded hash (COLD=read: clean lines only)
+        fb = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        if os.environ["COLD"] == "read":
+            fb.sum(dtype=torch.int64).item()
+        else:
+            fb.zero_()
         h.hash(key, out)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (3 * 64 * 16))()
