@@ -93,7 +93,7 @@ def test_configs_full(name):
         check(n, m, sw, kw, route, full=True)
 
 
-@pytest.mark.parametrize("name", ["C3", "C4", "C5a", "C5c"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C5a", "C5b", "C5c", "C5d"])
 def test_configs_sampled_and_closed_forms(name):
     """BASELINE.json sizes, same launch configuration as bench.py: sampled rows
     vs the oracle, plus full-output closed forms (all-ones key, unit keys)."""
