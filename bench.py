@@ -1,31 +1,37 @@
 #!/usr/bin/env python
 """bench.py -- Toeplitz privacy-amplification throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+                    [--split rows|cols|auto] [--no-sweep] [--no-cpu] [--selftest-cpu]
 
-One step = one pass of the whole hot path (pa_hash: y = T x over GF(2)) over one
-synthetic n-bit key against a seed bound at pa_create, inputs resident in HBM.
-The workload at N = 1 is BASELINE.json configs[1] (C2: n = 1,000,003 key bits,
-m = 250,000 output bits).  For N > 1 (torchrun, one process per GPU) every rank
-hashes its own key of the same shape (independent keys -- weak scaling, no
-collective on the data path); the timed region is bracketed by a barrier and
-torch.cuda.synchronize() and the maximum over ranks is reported.
+One step = one pass of the whole hot path (pa_hash: y = T x over GF(2), every kernel of
+route (a)) over one synthetic n-bit key against a seed bound at pa_create, inputs resident
+in HBM.  Workload: BASELINE.json configs[3], C4 (n = 10^8 key bits, m = 2*10^7 output bits,
+m/n = 0.2), the largest configuration that fits one GPU; at N = 1 it is the G = 1 point of
+its 1/2/4/8 curve.  For N > 1 (one process per GPU; the driver's torchrun, or --gpus N
+re-executes this script under torch.distributed.run) the same key is split across the ranks
+by output rows as configured ("output rows sharded ... with NCCL gather", --split rows; the
+column split and the cost-model choice are measured beside it), and the C5 batches are
+dealt across the ranks (keys pre-distributed, no collective).
 
-Timing: W untimed warm-up steps, then K steps, each timed with CUDA events on the
-launching stream; the L2 is flushed (a 256 MiB buffer larger than the 126 MB L2
-is zeroed) before every step, outside the events.  value = n * keys / sum of step
-times (decimal Gbit/s of input key).  A second pass of K steps with libpa's
-per-launch event profiling gives the per-kernel times behind `roofline`.  `e2e`
-is the same metric through the public API with host buffers (pa_hash_host:
-pinned host key -> device -> hash -> host output, synchronised, every step).
-`cpu_baseline` is the CPU oracle (oracle/, OpenMP on all host cores) on the same
-workload.  --impl reference times that oracle as the reference arm.
+Timing: W untimed warm-up steps, then K steps, each timed with CUDA events on the launching
+stream; before every step a 256 MiB buffer (> the 126 MB L2) is zeroed outside the events
+(the C4 working set, 2 GB, exceeds L2 anyway).  value = n * keys / sum of step times
+(decimal Gbit/s of input key), max over ranks.  A second pass of K steps with libpa's
+per-launch event profiling gives each kernel's launch time behind `roofline`.  `e2e` is
+the same metric through the public API with host buffers (pinned key in, host output out,
+copies inside the timed region).  `cpu_baseline` is the CPU oracle (oracle/, OpenMP) on a
+bounded sample of the same workload, all host cores and one core.  --impl reference times
+that oracle as the reference arm.  --selftest-cpu runs the multi-rank plumbing (gloo, the
+CPU oracle injected as the per-rank hash) and prints a check line -- not a measurement.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -39,31 +45,46 @@ import pa_synth as syn  # noqa: E402
 
 METRIC = "PA throughput, input Gbit/s vs input length n, 1/2/4/8 B200; % of HBM roofline"
 FLUSH_BYTES = 256 << 20
+C5_KEYS = 1024
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=sorted(syn.CONFIGS),
-                    help="workload (default C2; C4 for --split rows/cols, BASELINE configs[3])")
-    ap.add_argument("--split", default="keys", choices=["keys", "rows", "cols"],
-                    help="N > 1: independent keys per rank (weak scaling, default), or one key split "
-                         "across the ranks by output rows (all-gather) or by key columns (Eq. (4) blocks, "
-                         "XOR reduce-scatter + all-gather) -- strong scaling")
-    ap.add_argument("--no-sweep", action="store_true", help="skip the C1/C3/C4 side measurements")
+    ap.add_argument("--config", default="C4", choices=sorted(syn.CONFIGS),
+                    help="headline workload (default C4, BASELINE configs[3])")
+    ap.add_argument("--split", default="rows", choices=["rows", "cols", "auto"],
+                    help="N > 1: how the key is split (rows = configured; auto = dist.choose_split)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the other-config side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline")
-    args = ap.parse_args()
-    if args.config is None:
-        args.config = "C2" if args.split == "keys" else "C4"
-    return args
+    ap.add_argument("--selftest-cpu", action="store_true",
+                    help="multi-rank plumbing check on CPU (gloo, oracle as the per-rank hash)")
+    return ap.parse_args()
 
 
 def workload_desc(name):
     c = syn.CONFIGS[name]
     return f"{name}: {c['desc']} (n={c['n']}, m={c['m']})"
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def respawn(args):
+    """--gpus N without a torchrun environment: run N ranks of this script under
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -105,7 +126,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self._h is not None:
@@ -120,8 +141,7 @@ class ClockSampler:
 
     def result(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                    "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
@@ -130,7 +150,7 @@ class ClockSampler:
 def peak_hbm():
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy bandwidth)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
@@ -151,20 +171,20 @@ def ncu_kernel(config, kernel):
     return None
 
 
-def ncu_traffic(config, kernel):
-    """dram__bytes_read+write per launch of `kernel` from the committed ncu summary."""
-    d = ncu_kernel(config, kernel)
-    return None if d is None else float(d["dram_read"] + d["dram_write"]) * 1e9
-
-
 def alg_bytes(kernel, info):
-    """Algorithmic HBM bytes of one launch: M complex doubles = 16 M bytes."""
+    """Algorithmic HBM bytes of one launch (DESIGN.md Sec. 5 / SURVEY 8(d)), M = n1 * n2 complex
+    doubles (16 bytes each) per key."""
     M = info["n1"] * info["n2"]
     n, m = info["n"], info["m"]
     return {"k0_bits_transpose": n / 8.0 + M / 4.0,          # key bits in, 2M bits of streams out
             "k1_fwd_columns": M / 4.0 + 16 * M,             # bit streams in, work array out
             "k2_rows": 48 * M,                              # row in, spectrum in, row out
             "k3_inv_columns": 16 * M + m / 8.0}.get(kernel)  # work array in, output bits out
+
+
+def hash_bytes(n, m, M):
+    """SURVEY 8(d) route (a) FP64 model per hash: 40 N + (n+m)/8 bytes, N = 2M real points."""
+    return 80.0 * M + (n + m) / 8.0
 
 
 def dev_words(torch, w64, device):
@@ -175,16 +195,89 @@ def dev_words(torch, w64, device):
     return torch.from_numpy(w.copy()).to(device)
 
 
-def time_steps(torch, fn, steps, flush):
-    """Per-step CUDA-event times (ms) with an L2 flush before each step (untimed)."""
+def time_steps(torch, fn, steps, flush, stream=None):
+    """Per-step CUDA-event times (ms) on the launching stream, L2 flushed before each step."""
+    st = stream or torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for e0, e1 in ev:
         flush.zero_()
-        e0.record()
+        e0.record(st)
         fn()
-        e1.record()
+        e1.record(st)
     torch.cuda.synchronize()
     return [e0.elapsed_time(e1) for e0, e1 in ev]
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    """Logical CPUs this process may run on (torchrun sets OMP_NUM_THREADS=1; the oracle's
+    thread count is passed explicitly instead)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def sampled_rows(m, k=128, seed=1):
+    return np.unique(np.concatenate([np.arange(min(m, 32)), np.arange(max(0, m - 32), m),
+                                     np.random.default_rng(seed).integers(0, m, k)])).astype(np.uint64)
+
+
+def verify_rows(n, m, seed_w, key_w, out_words_np, rows):
+    import oracle
+    got = oracle.unpack(out_words_np.view(np.uint32), m)[rows.astype(np.int64)]
+    return bool(np.array_equal(got, oracle.toeplitz_rows(n, m, seed_w, key_w, rows)))
+
+
+def roofline(kern, info, name, steps_per_launch=1):
+    """Per-kernel roofline from libpa's per-launch event times: achieved = algorithmic bytes per
+    launch / average launch time vs the measured HBM copy bandwidth; `traffic` = ncu DRAM bytes
+    of that kernel (committed capture profiles/ncu_<config>.json)."""
+    peak, peak_src = peak_hbm()
+    per = {k: v[1] / max(1, v[0]) for k, v in kern.items()}  # ms per launch
+    if not per:
+        return None
+    kernels = {}
+    for k, t in per.items():
+        b = alg_bytes(k, info)
+        nk = ncu_kernel(name, k) or {}
+        tr = (float(nk["dram_read"] + nk["dram_write"]) * 1e9) if nk else None
+        kernels[k] = {"avg_launch_us": t * 1e3, "alg_bytes_per_launch": b,
+                      "achieved": (b / (t * 1e-3) / 1e9) if b else None,
+                      "frac": (b / (t * 1e-3) / 1e9 / peak) if b else None, "traffic": tr,
+                      "fp64_pipe_frac_ncu": (nk.get("fp64_pipe_pct") or 0) / 100 or None,
+                      "issue_active_frac_ncu": (nk.get("issue_pct") or 0) / 100 or None}
+    top = max(per, key=per.get)
+    if top == "k_toeplitz_bitpacked":
+        bp = float(info["n"]) * info["m"]
+        achieved = bp / (per[top] * 1e-3) / 1e12
+        alu_peak = 1024 * 148 * 1965e6 / 1e12
+        return {"kernel": top, "bound": "alu", "achieved": achieved, "peak": alu_peak,
+                "unit": "Tbit-products/s", "frac": achieved / alu_peak, "traffic": None,
+                "peak_source": "derived (DESIGN.md Sec. 6): 148 SMs x 64 ALU lanes/clk x 16 bit-products "
+                               "per op (SHF + LOP3 per 32) x 1.965 GHz", "kernels": kernels}
+    k = kernels[top]
+    M = info["n1"] * info["n2"]
+    tot_ms = sum(per.values())
+    hb = hash_bytes(info["n"], info["m"], M)
+    return {"kernel": top, "bound": "hbm", "achieved": k["achieved"], "peak": peak, "unit": "GB/s",
+            "frac": k["frac"], "traffic": k["traffic"], "alg_bytes_per_launch": k["alg_bytes_per_launch"],
+            "avg_launch_us": k["avg_launch_us"], "peak_source": peak_src, "kernels": kernels,
+            "whole_hash": {"alg_bytes": hb, "sum_launch_us": tot_ms * 1e3,
+                           "achieved": hb / (tot_ms * 1e-3) / 1e9, "frac": hb / (tot_ms * 1e-3) / 1e9 / peak},
+            "note": "achieved = algorithmic HBM bytes (SURVEY 8(d): K1 16M+M/4, K2 48M, K3 16M+m/8 per key, "
+                    "M complex points) / CUDA-event launch time (libpa pa_profile, events on the launch "
+                    "stream) vs the measured copy bandwidth; fp64/issue fractions from the committed ncu "
+                    "capture (DESIGN.md Sec. 9)"}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -193,38 +286,37 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1805_02372_b200 as pa
+    from paper_1805_02372_b200 import dist as pd
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     name = args.config
-    split = args.split
-    n, m, sw, kw = syn.config_inputs(name, key_index=rank if split == "keys" else 0)
+    n, m, sw, kw = syn.config_inputs(name)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    seed_t = dev_words(torch, sw, dev)
+    key = dev_words(torch, kw, dev)  # resident on every rank (the device-timed value)
+    split = "none" if world == 1 else (pd.choose_split(n, m, world) if args.split == "auto" else args.split)
     res = {}
-    if split == "keys":
-        h = pa.Hasher(n, m, dev_words(torch, sw, dev))
-        key = dev_words(torch, kw, dev)
+    if world == 1:
+        h = pa.Hasher(n, m, seed_t)
         out = h.new_out()
         res["out"] = out
 
         def step():
             h.hash(key, out)
-    else:  # one key split across the ranks (paper_1805_02372_b200.dist)
-        from paper_1805_02372_b200 import dist as pd
-        seed_t = dev_words(torch, sw, dev)
+        sh = None
+    else:
         sh = pd.RowSplit(n, m, seed_t) if split == "rows" else pd.ColSplit(n, m, seed_t)
-        key = dev_words(torch, kw, dev) if split == "rows" else sh.key_block(kw, dev)
+        blk = key if split == "rows" else sh.key_block(kw, dev)
         h = sh.h
 
         def step():
-            res["out"] = sh(key)
+            res["out"] = sh(blk)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -239,235 +331,294 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     tot_ms = float(sum(ms))
-    # correctness spot check of the last output against the oracle (sampled rows)
     verified = None
     if rank == 0:
-        import oracle
-        rows = np.unique(np.concatenate([np.arange(64), np.arange(m - 64, m),
-                                         np.random.default_rng(1).integers(0, m, 256)]))
-        got = oracle.unpack(res["out"].cpu().numpy().view(np.uint32), m)[rows]
-        verified = bool(np.array_equal(got, oracle.toeplitz_rows(n, m, sw, kw, rows)))
+        verified = verify_rows(n, m, sw, kw, res["out"].cpu().numpy(), sampled_rows(m, 256))
 
-    # profiled pass: per-kernel CUDA-event times of the same K steps
-    pa.pa_profile_enable(h.handle, True)
-    pa.pa_profile_read(h.handle)
-    prof_ms = time_steps(torch, step, args.steps, flush)
-    kern = pa.pa_profile_read(h.handle)
-    pa.pa_profile_enable(h.handle, False)
+    # profiled pass: per-kernel CUDA-event times of the same K steps (rank 0's handle)
+    kern = {}
+    if h is not None:
+        pa.pa_profile_enable(h.handle, True)
+        pa.pa_profile_read(h.handle)
+        time_steps(torch, step, args.steps, flush)
+        kern = pa.pa_profile_read(h.handle)
+        pa.pa_profile_enable(h.handle, False)
 
     # end to end through the public API with host buffers: every step copies the key from
-    # pinned host memory and reads the output back (pa_hash_host_async = one CUDA graph of
-    # H2D + kernels + D2H, stream-ordered; the synchronous pa_hash_host is timed too)
+    # pinned host memory and reads the output back.  N = 1: pa_hash_host_async (one CUDA graph:
+    # pinned key -> copy kernel -> K0..K3 -> copy kernel -> pinned output).  N > 1: rank 0's
+    # pinned key H2D, broadcast (row split) / scatter (column split) to the ranks, the sharded
+    # hash with its collectives, y D2H on rank 0.
     out_h = torch.empty(pa.words32(m), dtype=torch.int32).pin_memory()
-    e2e_steps = max(3, min(args.steps, 100))
-    if split == "keys":
-        key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
+    key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    if world == 1:
         e2e_fn = lambda: h.hash_host_async(key_h, out_h)  # noqa: E731
-    else:  # this rank's key words H2D, the sharded hash with its collectives, y D2H
-        key_h = key.cpu().pin_memory()
+        h2d = 4 * key_h.numel()
+    else:
+        src_key = torch.zeros_like(key)
 
         def e2e_fn():
-            key.copy_(key_h, non_blocking=True)
-            step()
-            out_h.copy_(res["out"][: out_h.numel()], non_blocking=True)
+            if rank == 0:
+                src_key[: key_h.numel()].copy_(key_h, non_blocking=True)
+            if split == "rows":
+                y = sh(src_key, src=0)
+            else:
+                y = sh(sh.scatter_key(src_key if rank == 0 else None, src=0))
+            if rank == 0:
+                out_h.copy_(y[: out_h.numel()], non_blocking=True)
+        h2d = 4 * key_h.numel()
     for _ in range(3):
         e2e_fn()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e2e_ms = time_steps(torch, e2e_fn, e2e_steps, flush)
-    e2e_ok = bool(np.array_equal(out_h.numpy().view(np.uint32),
-                                 res["out"].cpu().numpy().view(np.uint32)[:out_h.numel()]))
-    e2e_sync_ms = (time_steps(torch, lambda: h.hash_host(key_h, out_h), max(3, min(args.steps, 30)), flush)
-                   if split == "keys" else e2e_ms)
+    e2e_ok = None
+    if rank == 0:
+        e2e_ok = bool(np.array_equal(out_h.numpy().view(np.uint32),
+                                     res["out"].cpu().numpy().view(np.uint32)[: out_h.numel()]))
 
-    # max over ranks
-    t = torch.tensor([tot_ms, float(np.mean(e2e_ms)), float(np.mean(e2e_sync_ms))], dtype=torch.float64,
-                     device=dev)
+    # N > 1: the other split and the cost model's choice, and C5 key dealing, same protocol
+    side = {}
+    if world > 1:
+        side = multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush, split, name)
+
+    t = torch.tensor([tot_ms, float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tot_ms, e2e_mean, e2e_sync_mean = float(t[0]), float(t[1]), float(t[2])
+    tot_ms, e2e_mean = float(t[0]), float(t[1])
 
     line = None
     if rank == 0:
         info = h.info
-        keys_per_step = world if split == "keys" else 1  # splits: one key across all ranks
-        value = n * keys_per_step * args.steps / (tot_ms * 1e-3) / 1e9
-        e2e_value = n * keys_per_step / (e2e_mean * 1e-3) / 1e9
-        # roofline of the dominant kernel
-        roof = None
-        per = {k: v[1] / max(1, v[0]) for k, v in kern.items()}
-        if per:
-            top = max(per, key=per.get)
-            peak, peak_src = peak_hbm()
-            if top == "k_toeplitz_bitpacked":
-                # ALU bound: 2 ALU ops (SHF + LOP3) per 32 bit-products, 64 lanes/clk/SM
-                bp = float(n) * m
-                achieved = bp / (per[top] * 1e-3) / 1e12
-                alu_peak = 1024 * 148 * (info.get("sm_max_mhz") or 1965) * 1e6 / 1e12
-                roof = {"kernel": top, "bound": "alu", "achieved": achieved, "peak": alu_peak,
-                        "unit": "Tbit-products/s", "frac": achieved / alu_peak, "traffic": None,
-                        "peak_source": "derived: 148 SMs x 64 ALU lanes/clk x 16 bit-products/op x 1.965 GHz"}
-            else:
-                b = alg_bytes(top, info)
-                achieved = b / (per[top] * 1e-3) / 1e9
-                traffic = ncu_traffic(name, top)
-                nk = ncu_kernel(name, top) or {}
-                roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": b,
-                        "avg_launch_us": per[top] * 1e3, "peak_source": peak_src,
-                        "fp64_pipe_frac_ncu": (nk.get("fp64_pipe_pct") or 0) / 100 or None,
-                        "issue_active_frac_ncu": (nk.get("issue_pct") or 0) / 100 or None,
-                        "note": "achieved = algorithmic HBM bytes / CUDA-event launch time vs the measured "
-                                "copy bandwidth.  The FFT passes are bound by the FP64 pipe and issue "
-                                "latency, not HBM (fp64_pipe_frac_ncu / issue_active_frac_ncu from the "
-                                "committed ncu capture, profiles/ncu_<config>.json); DESIGN.md Sec. 9"}
+        value = n * args.steps / (tot_ms * 1e-3) / 1e9
+        roof = roofline(kern, info, name)
+        parallelism = {
+            "none": "one key on 1 GPU (the G = 1 point of the configured 1/2/4/8 curve)",
+            "rows": f"one key, output rows split over {world} GPUs (configured): per-rank seed window at "
+                    "offset r0, NCCL all_gather_into_tensor",
+            "cols": f"one key, Eq. (4) key blocks over {world} GPUs: XOR reduce-scatter (all_to_all_single "
+                    "+ pa_xor_fold) + all_gather"}[split]
         line = {
             "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak" if split == "keys" else "strong", "vs_baseline": None,
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
             "dtype": "f64" if info["route"] == 1 else "u32",
             "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits (SURVEY 8(d) streams)",
-            "config": {"workload": workload_desc(name), "n": n, "m": m,
-                       "keys_per_rank": 1 if split == "keys" else 1.0 / world,
-                       "route": h.route, "transform_len": info["transform_len"], "n1": info["n1"],
-                       "n2": info["n2"], "cols_per_cta": info["cols_per_cta"],
-                       "parallelism": {
-                           "keys": f"independent keys x {world} GPU(s), no data-path collective",
-                           "rows": f"one key, output rows split over {world} GPU(s) (rank 0's share shown), "
-                                   "NCCL all_gather_into_tensor",
-                           "cols": f"one key, Eq. (4) key blocks over {world} GPU(s) (rank 0's share shown), "
-                                   "XOR reduce-scatter (all_to_all_single + pa_xor_fold) + all_gather"}[split],
-                       "l2": "flushed before every step (256 MiB memset, untimed)", "verified": verified},
+            "config": {"workload": workload_desc(name), "n": n, "m": m, "route": h.route,
+                       "transform_len": info["transform_len"], "n1": info["n1"], "n2": info["n2"],
+                       "cols_per_cta": info["cols_per_cta"], "split": split, "parallelism": parallelism,
+                       "l2": "flushed before every step (256 MiB memset, untimed); working set > L2",
+                       "verified_rows": verified},
             "roofline": roof,
             "kernels_us": {k: v[1] / max(1, v[0]) * 1e3 for k, v in kern.items()},
-            "profiled_ms_per_step": float(np.mean(prof_ms)),
-            "e2e": {"value": e2e_value, "unit": "Gbit/s", "h2d_bytes_per_step": 4 * key_h.numel(),
+            "e2e": {"value": n / (e2e_mean * 1e-3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 4 * pa.words32(m), "steps": e2e_steps, "verified": e2e_ok,
-                    "how": ("pa_hash_host_async per step (CUDA graph: pinned host key -> copy kernel over the mapped "
-                            "pages -> K0..K3 -> copy kernel to the pinned host output), CUDA events around "
-                            "each step, L2 flushed between")
-                    if split == "keys" else
-                    "per step: this rank's key words H2D from pinned memory, the sharded hash and its "
-                    "collectives, y D2H; CUDA events around each step, L2 flushed between",
-                    "sync_api_value": n * world / (e2e_sync_mean * 1e-3) / 1e9,
-                    "sync_api_how": "pa_hash_host (same, plus a stream synchronisation every step)"},
-            "gpu_launches": args.steps * (info["kernels_per_hash"] + (1 if split == "cols" and world > 1 else 0)),
+                    "how": "pa_hash_host_async per step (CUDA graph: pinned host key -> copy kernel -> K0..K3 "
+                           "-> copy kernel -> pinned host output), CUDA events around each step"
+                    if world == 1 else
+                    "rank 0: pinned key H2D, NCCL broadcast (rows) / scatter of key blocks (cols), sharded "
+                    "hash and merge collectives, y D2H; CUDA events, max over ranks"},
+            "gpu_launches": args.steps * (info["kernels_per_hash"] + (1 if split == "cols" else 0)),
             "clocks": clk.result(),
         }
-    if split == "keys":
-        h.close()
-    else:
+        if side:
+            line["multi_gpu"] = side
+    if sh is not None:
         sh.close()
+    else:
+        h.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return line
 
 
+def c5_keys(torch, name, count, dev, first=0):
+    """`count` distinct keys of C5 sub-config `name` (streams key(c, first..first+count-1)),
+    generated on the device with the pa_synth counter generator."""
+    c = syn.CONFIG_INDEX[name]
+    n = syn.CONFIGS[name]["n"]
+    return syn.random_bits_torch([syn.key_stream(c, k) for k in range(first, first + count)], n, dev)
+
+
+def time_batch(torch, h, keys, outs, flush, reps=2):
+    h.hash_batch(keys, outs)
+    torch.cuda.synchronize()
+    return float(np.mean(time_steps(torch, lambda: h.hash_batch(keys, outs), reps, flush)))
+
+
+def multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush, split, name):
+    """N > 1 side measurements: the other split of the same key, the cost model's pick, and C5
+    batches dealt across the ranks (each rank generates its own keys: pre-distributed)."""
+    out = {"choose_split": pd.choose_split(syn.CONFIGS[name]["n"], syn.CONFIGS[name]["m"], world)}
+    n, m, sw, kw = syn.config_inputs(name)
+    seed_t = dev_words(torch, sw, dev)
+    other = "cols" if split == "rows" else "rows"
+    sh = pd.RowSplit(n, m, seed_t) if other == "rows" else pd.ColSplit(n, m, seed_t)
+    blk = dev_words(torch, kw, dev) if other == "rows" else sh.key_block(kw, dev)
+    for _ in range(3):
+        y = sh(blk)
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps = max(5, min(args.steps, 30))
+    t = float(sum(time_steps(torch, lambda: sh(blk), steps, flush)))
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ok = None
+    if rank == 0:
+        ok = verify_rows(n, m, sw, kw, y.cpu().numpy(), sampled_rows(m, 64))
+    out[f"{other}_split"] = {"gbit_s": n * steps / (float(tt[0]) * 1e-3) / 1e9,
+                             "ms_per_hash": float(tt[0]) / steps, "verified_rows": ok}
+    sh.close()
+    for cname in ("C5a", "C5b", "C5c", "C5d"):
+        cn, cm, csw, _ = syn.config_inputs(cname)
+        idx = list(range(rank, C5_KEYS, world))
+        total = len(idx) * world
+        c = syn.CONFIG_INDEX[cname]
+        keys = syn.random_bits_torch([syn.key_stream(c, k) for k in idx], cn, dev)
+        kd = pd.KeyDeal(cn, cm, dev_words(torch, csw, dev))
+        outs = kd.h.new_out(len(idx))
+        kd(keys, outs)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = float(np.mean(time_steps(torch, lambda: kd(keys, outs), 2, flush)))
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        out[f"{cname}_dealt"] = {"keys": total, "keys_per_rank": len(idx),
+                                 "gbit_s": cn * total / (float(tt[0]) * 1e-3) / 1e9}
+        kd.close()
+        del keys, outs
+    return out
+
+
 def sweep(torch, pa, dev, steps=10):
-    """Side measurements (rank 0, N = 1): other BASELINE configs, same protocol."""
+    """Side measurements (rank 0, N = 1), same protocol: C1 latency and 2^16 distinct keys
+    batched (route b), C2 / C3 single keys, the C5 batches of 1024 distinct keys, fresh seeds, host-buffer batches.  Each transform entry carries its
+    whole-hash HBM fraction (SURVEY 8(d) model bytes / time / measured peak)."""
+    import oracle  # noqa: F401  (sampled-row checks below)
+    peak, _ = peak_hbm()
     res = {}
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    for name in ("C1", "C3", "C4"):
+    for name in ("C1", "C2", "C3"):
         n, m, sw, kw = syn.config_inputs(name)
         h = pa.Hasher(n, m, dev_words(torch, sw, dev))
         key = dev_words(torch, kw, dev)
         out = h.new_out()
         for _ in range(3):
             h.hash(key, out)
-        ms = time_steps(torch, lambda: h.hash(key, out), steps, flush)
+        ms = time_steps(torch, lambda: h.hash(key, out), max(steps, 20), flush)
         t = float(np.mean(ms))
-        res[name] = {"n": n, "m": m, "route": h.route, "ms_per_hash": t, "gbit_s": n / (t * 1e-3) / 1e9,
-                     "transform_len": h.info["transform_len"], "residual": h.residual()}
+        info = h.info
+        e = {"n": n, "m": m, "route": h.route, "ms_per_hash": t, "gbit_s": n / (t * 1e-3) / 1e9,
+             "transform_len": info["transform_len"], "residual": h.residual(),
+             "verified_rows": verify_rows(n, m, sw, kw, out.cpu().numpy(), sampled_rows(m))}
+        if info["route"] == 1:
+            hb = hash_bytes(n, m, info["n1"] * info["n2"])
+            e["hbm_frac_whole_hash"] = hb / (t * 1e-3) / 1e9 / peak
+        res[name] = e
         h.close()
-    # BASELINE configs[4] shape: independent keys against one seed through pa_hash_batch
-    for name, count in (("C5a", 256), ("C5c", 32)):
-        n, m, sw, kw = syn.config_inputs(name)
+    # C5 (BASELINE configs[4]): distinct keys against one seed through pa_hash_batch
+    for name in ("C5a", "C5b", "C5c", "C5d"):
+        n, m, sw, _ = syn.config_inputs(name)
+        count = C5_KEYS
         h = pa.Hasher(n, m, dev_words(torch, sw, dev))
-        kw32 = (n + 31) // 32
-        stride = (kw32 + 3) // 4 * 4
-        keys = torch.zeros((count, stride), dtype=torch.int32, device=dev)
-        keys[:, :kw32] = dev_words(torch, kw, dev)[:kw32]
+        keys = c5_keys(torch, name, count, dev)
         outs = h.new_out(count)
-        h.hash_batch(keys, outs)
-        ms = time_steps(torch, lambda: h.hash_batch(keys, outs), 3, flush)
-        t = float(np.mean(ms)) / count
-        res[name + "_batched"] = {"n": n, "m": m, "keys": count, "ms_per_key": t,
-                                  "gbit_s": n / (t * 1e-3) / 1e9, "transform_len": h.info["transform_len"]}
+        t = time_batch(torch, h, keys, outs, flush) / count
+        info = h.info
+        ok = True
+        for k in (0, count - 1):
+            kw = syn.random_bits(syn.key_stream(syn.CONFIG_INDEX[name], k), n)
+            ok &= verify_rows(n, m, sw, kw, outs[k].cpu().numpy(), sampled_rows(m, 32, seed=k))
+        res[name + "_batched"] = {"n": n, "m": m, "keys": count, "distinct_keys": True, "ms_per_key": t,
+                                  "gbit_s": n / (t * 1e-3) / 1e9, "transform_len": info["transform_len"],
+                                  "hbm_frac_whole_hash": hash_bytes(n, m, info["n1"] * info["n2"])
+                                  / (t * 1e-3) / 1e9 / peak, "verified_rows": ok}
         h.close()
-    # the same C5a batch end to end from pinned host memory (pa_hash_host_batch: one H2D, one
-    # batched hash, one D2H, synchronised)
-    n, m, sw, kw = syn.config_inputs("C5a")
-    count = 256
-    h = pa.Hasher(n, m, dev_words(torch, sw, dev))
-    kw32 = (n + 31) // 32
-    kh = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32)[:kw32].copy()).repeat(count, 1).pin_memory()
-    oh = torch.empty((count, pa.words32(m)), dtype=torch.int32).pin_memory()
-    h.hash_host_batch(kh, oh)
-    ms = time_steps(torch, lambda: h.hash_host_batch(kh, oh), 3, flush)
-    t = float(np.mean(ms)) / count
-    res["C5a_batched_e2e"] = {"n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
-                              "note": "pa_hash_host_batch: pinned host keys in, host outputs out"}
-    h.close()
-    # C1 throughput (SURVEY 8(d)): 2^16 keys against one seed, route (b) batched on the grid
-    n, m, sw, kw = syn.config_inputs("C1")
+        del keys, outs
+    # C1: one key's latency is launch-bound; throughput over 2^16 distinct keys (route b)
+    n, m, sw, _ = syn.config_inputs("C1")
     count = 1 << 16
     h = pa.Hasher(n, m, dev_words(torch, sw, dev))
-    kw32 = (n + 31) // 32
-    keys = dev_words(torch, kw, dev)[:kw32].repeat(count, 1).contiguous()
+    keys = c5_keys(torch, "C1", count, dev)
     outs = h.new_out(count)
-    h.hash_batch(keys, outs)
-    ms = time_steps(torch, lambda: h.hash_batch(keys, outs), 3, flush)
-    t = float(np.mean(ms)) / count
-    res["C1_batched"] = {"n": n, "m": m, "keys": count, "route": h.route, "us_per_key": t * 1e3,
-                         "gbit_s": n / (t * 1e-3) / 1e9}
+    t = time_batch(torch, h, keys, outs, flush, reps=3) / count
+    res["C1_batched"] = {"n": n, "m": m, "keys": count, "distinct_keys": True, "route": h.route,
+                         "us_per_key": t * 1e3, "gbit_s": n / (t * 1e-3) / 1e9}
+    h.close()
+    # C5a end to end from pinned host memory (pa_hash_host_batch: H2D / batched hash / D2H of
+    # neighbouring chunks overlapped), 1024 distinct keys
+    n, m, sw, _ = syn.config_inputs("C5a")
+    h = pa.Hasher(n, m, dev_words(torch, sw, dev))
+    kh = c5_keys(torch, "C5a", C5_KEYS, dev).cpu().pin_memory()
+    oh = torch.empty((C5_KEYS, pa.words32(m)), dtype=torch.int32).pin_memory()
+    h.hash_host_batch(kh, oh)
+    ms = time_steps(torch, lambda: h.hash_host_batch(kh, oh), 2, flush)
+    t = float(np.mean(ms)) / C5_KEYS
+    res["C5a_batched_e2e"] = {"n": n, "m": m, "keys": C5_KEYS, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
+                              "note": "pa_hash_host_batch: pinned host keys in, host outputs out"}
     h.close()
     # fresh seed per key (NEXT-2, P:90): seed transform + hash per key, C2 shape
     n, m, sw, kw = syn.config_inputs("C2")
     count = 64
-    seeds = torch.stack([dev_words(torch, syn.random_bits(syn.seed_stream(900 + k), n + m - 1), dev)
-                         for k in range(count)])
-    keys = torch.stack([dev_words(torch, kw, dev)] * count)
+    seeds = syn.random_bits_torch([syn.seed_stream(900 + k) for k in range(count)], n + m - 1, dev)
+    keys = syn.random_bits_torch([syn.key_stream(2, k) for k in range(count)], n, dev)
     h = pa.Hasher(n, m, seeds[0])
     outs = h.new_out(count)
     h.hash_fresh_batch(seeds, keys, outs)
     ms = time_steps(torch, lambda: h.hash_fresh_batch(seeds, keys, outs), 3, flush)
     t = float(np.mean(ms)) / count
     res["C2_fresh_seed"] = {"n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
-                            "note": "pa_hash_fresh_batch: a distinct seed per key; the chunk's seeds transformed "
-                                    "as one batch into per-key spectra, then its keys hashed as one batch"}
+                            "note": "pa_hash_fresh_batch: a distinct seed per key (seed transforms batched "
+                                    "into per-key spectra, then the keys hashed as one batch)"}
+    h.close()
+    # create time (SURVEY 8(d) timing protocol: pa_create timed separately): C4 seed transform
+    n, m, sw, _ = syn.config_inputs("C4")
+    seed_t = dev_words(torch, sw, dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h = pa.Hasher(n, m, seed_t)
+    torch.cuda.synchronize()
+    e0.record()
+    h.set_seed(seed_t)
+    e1.record()
+    torch.cuda.synchronize()
+    res["C4_set_seed_ms"] = e0.elapsed_time(e1)
     h.close()
     return res
 
 
-def cpu_oracle_baseline(name, budget_s=12.0, max_rows=None):
-    """The CPU oracle (as it stands) on the same workload, all host cores."""
+def cpu_oracle_baseline(name, budget_s=12.0):
+    """The CPU oracle (as it stands) on a bounded sample of the workload's rows (every row costs
+    the same: n/64 word products), all host cores and one core; extrapolated to a full hash."""
     import oracle
     n, m, sw, kw = syn.config_inputs(name)
-    cores = oracle.max_threads()
-    if max_rows is None:  # bound the sample: probe one row's cost, then fit ~budget_s / 4 per repeat
-        probe = np.arange(min(m, 1024), dtype=np.uint64)
+    cores = host_cores()
+
+    def rate(threads, budget):
+        probe = np.arange(min(m, 256), dtype=np.uint64)
         t0 = time.perf_counter()
-        oracle.toeplitz_rows(n, m, sw, kw, probe)
+        oracle.toeplitz_rows(n, m, sw, kw, probe, threads=threads)
         per_row = (time.perf_counter() - t0) / probe.size
-        max_rows = max(1024, int(budget_s / 4 / max(per_row, 1e-12)))
-    rows = np.arange(min(m, max_rows), dtype=np.uint64)
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        oracle.toeplitz_rows(n, m, sw, kw, rows)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or reps >= 50:
-            break
-    per_row = el / (reps * rows.size)
-    t_full = per_row * m
-    return {"value": n / t_full / 1e9, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
-            "sample": f"{name} rows [0,{rows.size}) of m={m} x {reps} repeats ({el:.1f} s, "
-                      f"word-level direct GF(2) product, OpenMP); value extrapolated per full hash"
-                      if rows.size < m else
-                      f"{name} full hash (all {m} rows) x {reps} repeats ({el:.1f} s, word-level direct "
-                      f"GF(2) product, OpenMP)",
-            "seconds_per_hash": t_full}
+        rows = np.arange(min(m, max(256, int(budget / 3 / max(per_row, 1e-12)))), dtype=np.uint64)
+        t0, reps = time.perf_counter(), 0
+        while True:
+            oracle.toeplitz_rows(n, m, sw, kw, rows, threads=threads)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget or reps >= 50:
+                break
+        return el / (reps * rows.size) * m, rows.size, reps, el
+    t_all, r_all, reps_all, el_all = rate(cores, budget_s)
+    t_one, r_one, reps_one, el_one = rate(1, budget_s * 0.6)
+    return {"value": n / t_all / 1e9, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
+            "sample": f"{name}: rows [0,{r_all}) of m={m} x {reps_all} repeats ({el_all:.1f} s, word-level direct "
+                      f"GF(2) product, OpenMP {cores} threads); every row costs the same, value extrapolated "
+                      f"to the full hash (x{m / r_all:.0f})",
+            "seconds_per_hash": t_all, "cpu_model": cpu_model(),
+            "one_core": {"value": n / t_one / 1e9, "cores": 1, "seconds_per_hash": t_one,
+                         "sample": f"rows [0,{r_one}) x {reps_one} ({el_one:.1f} s)"}}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -479,38 +630,89 @@ def run_reference(args):
     import oracle
     name = args.config
     n, m, sw, kw = syn.config_inputs(name)
-    cores = oracle.max_threads()
+    cores = host_cores()
     # size each step so the whole run takes ~1-2 minutes: estimate one row's cost
-    probe = np.arange(min(m, 2000), dtype=np.uint64)
+    probe = np.arange(min(m, 512), dtype=np.uint64)
     t0 = time.perf_counter()
-    oracle.toeplitz_rows(n, m, sw, kw, probe)
+    oracle.toeplitz_rows(n, m, sw, kw, probe, threads=cores)
     per_row = (time.perf_counter() - t0) / probe.size
     budget = 90.0 / max(1, args.steps + args.warmup)
     nrows = int(max(64, min(m, budget / max(per_row, 1e-9))))
     rows = np.arange(nrows, dtype=np.uint64)
     for _ in range(args.warmup):
-        oracle.toeplitz_rows(n, m, sw, kw, rows)
+        oracle.toeplitz_rows(n, m, sw, kw, rows, threads=cores)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.toeplitz_rows(n, m, sw, kw, rows)
+        oracle.toeplitz_rows(n, m, sw, kw, rows, threads=cores)
         ts.append(time.perf_counter() - t0)
     t_full = float(np.sum(ts)) / args.steps * (m / nrows)
     value = n / t_full / 1e9
-    sample = (f"{name}: rows [0,{nrows}) of m={m} per step (full hash extrapolated x{m / nrows:.2f}), "
-              f"word-level direct GF(2) oracle, OpenMP {cores} threads")
+    sample = (f"{name}: rows [0,{nrows}) of m={m} per step (full hash extrapolated x{m / nrows:.0f}; every row "
+              f"costs the same), word-level direct GF(2) oracle, OpenMP {cores} threads ({cpu_model()})")
     return {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "impl": "reference",
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u64",
+            "impl": "reference",
             "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits",
-            "config": {"workload": workload_desc(name), "n": n, "m": m, "keys_per_rank": 1},
+            "config": {"workload": workload_desc(name), "n": n, "m": m},
             "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# ----------------------------------------------------------------------------- CPU plumbing check
+def run_selftest_cpu(args):
+    """The multi-rank path without a GPU: gloo process group, the CPU oracle injected as each
+    rank's hash (paper_1805_02372_b200.dist factories) -- rank spawning, row split with key
+    broadcast, column split with key scatter + XOR merge, key dealing, cost model.  Prints a
+    check line (not a measurement)."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_1805_02372_b200 import dist as pd
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    n, m = 3001, 700
+    sw = syn.random_bits(syn.seed_stream(91), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(91, 0), n)
+
+    def ohash(nn, mm, seed_t, off, key_t):
+        s = pd.extract_bits(seed_t.numpy().view(np.uint32), off, nn + mm - 1)
+        k = pd.extract_bits(key_t.numpy().view(np.uint32), 0, nn)
+        return torch.from_numpy(oracle.toeplitz_words(nn, mm, s, k).view(np.int32)[: (mm + 31) // 32].copy())
+    seed_t = torch.from_numpy(sw.view(np.int32).copy())
+    pd.distribute_seed(seed_t)
+    key_t = torch.from_numpy(kw.view(np.int32).copy()) if rank == 0 else torch.zeros(
+        (kw.size * 2,), dtype=torch.int32)
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    ok = {}
+    for split in ("rows", "cols"):
+        _, y = pd.hash(n, m, seed_t, key_t, split=split, hash_fn=ohash, xor_fn=pd._xor_fold_host)
+        ok[split] = bool(np.array_equal(oracle.unpack(y.numpy().view(np.uint32), m), want))
+    flags = torch.tensor([int(ok["rows"]), int(ok["cols"])])
+    if world > 1:
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        dist.destroy_process_group()
+    if rank == 0:
+        return {"selftest": "cpu-gloo multi-rank plumbing (not a measurement)", "n_gpus": world,
+                "rows_split_ok": bool(flags[0]), "cols_split_ok": bool(flags[1]),
+                "choose_split_C4": pd.choose_split(10**8, 2 * 10**7, world)}
+    return None
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(respawn(args))
+    if args.selftest_cpu:
+        line = run_selftest_cpu(args)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
     if args.impl == "reference":
         line = run_reference(args)
         if line is not None:

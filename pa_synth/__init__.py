@@ -106,6 +106,42 @@ def as_u32(words64: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(words64).view(np.uint32)
 
 
+def _s64(u: int) -> int:
+    """A uint64 constant as the int64 with the same bits (torch has no uint64 arithmetic)."""
+    return u - (1 << 64) if u >= (1 << 63) else u
+
+
+def random_bits_torch(streams, nbits: int, device, words32: int | None = None):
+    """The same SplitMix64 words as random_bits(stream, nbits), generated where they are used
+    (e.g. on the GPU: 1024 C5d keys are 6.4 GB) with torch int64 ops (two's-complement
+    wrap-around multiply, logical shifts by masking).  streams: a list of stream ids.
+    Returns a (len(streams), W) int32 tensor, W = words32 or ceil(nbits/32) rounded up to a
+    multiple of 4 (16-byte rows), bits past nbits zero.  No method arithmetic here either."""
+    import torch
+    nw64 = (nbits + 63) // 64
+    nw32 = (nbits + 31) // 32
+    W = words32 if words32 is not None else (nw32 + 3) // 4 * 4
+    out = torch.zeros((len(streams), W), dtype=torch.int32, device=device)
+    k = torch.arange(1, nw64 + 1, dtype=torch.int64, device=device)
+    g, m1, m2 = _s64(int(GAMMA)), _s64(int(_M1)), _s64(int(_M2))
+    st = torch.tensor([_s64(int(x) & 0xFFFF_FFFF_FFFF_FFFF) for x in streams], dtype=torch.int64, device=device)
+
+    def lsr(z, s):  # logical shift right of int64 bits
+        return (z >> s) & ((1 << (64 - s)) - 1)
+    rows = max(1, (1 << 25) // max(1, nw64))  # streams per chunk (bounded temporaries)
+    for i in range(0, len(streams), rows):
+        z = (k * g).unsqueeze(0) + st[i:i + rows].unsqueeze(1)
+        z = (z ^ lsr(z, 30)) * m1
+        z = (z ^ lsr(z, 27)) * m2
+        z = z ^ lsr(z, 31)
+        w32 = z.view(torch.int32)[:, :nw32]
+        out[i:i + rows, :nw32] = w32
+    r = nbits % 32
+    if r:
+        out[:, nw32 - 1] &= (1 << r) - 1
+    return out
+
+
 def config_inputs(name: str, key_index: int = 0) -> tuple[int, int, np.ndarray, np.ndarray]:
     """(n, m, seed_words, key_words) for a named config, seeded per SURVEY 8(d)."""
     cfg = CONFIGS[name]

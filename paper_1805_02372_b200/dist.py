@@ -1,27 +1,33 @@
 """Multi-GPU partitioning of one Toeplitz hash (one process per GPU, torch.distributed).
 
-Three exact decompositions of y = T x (PAPER.md Eq. (1), P:48-64):
+Three exact decompositions of y = T x (PAPER.md Eq. (1), P:48-64; SURVEY 8(e)):
 
 * Output-row split (BASELINE.json configs[3]): rank g owns rows [r0, r1) and its
   own handle on the seed window s[r0 : r1 + n - 1] (pa_options.seed_bit_offset
-  = r0), hashes the whole key, and the m-bit result is assembled with one NCCL
-  all-gather (every rank ends with all of y).
+  = r0), hashes the whole key (broadcast from the source rank), and the m-bit
+  result is assembled with one NCCL all-gather (every rank ends with all of y).
 * Input-column split (the paper's Eq. (4) block division, with the
-  Eq. (7) modulo-2 merge): rank g owns key bits [c0, c1) and the seed
-  window s[n - c1 : n - c0 + m - 1]; partial m-bit hashes are XOR-reduced.  NCCL
-  has no XOR reduction (nccl.h: Sum/Prod/Max/Min/Avg), so the merge is a
-  reduce-scatter built from all_to_all_single + libpa's XOR-fold kernel, then an
-  all-gather (exact, order-free).
-* Independent keys (configs[4]): keys are dealt round-robin; no collective on
-  the data path.
+  Eq. (7) modulo-2 merge): rank g owns key bits [c0, c1) (scattered
+  from the source rank, or already resident: P:107) and the seed window
+  s[n - c1 : n - c0 + m - 1]; partial m-bit hashes are XOR-reduced.  NCCL has no
+  XOR reduction (nccl.h: Sum/Prod/Max/Min/Avg), so the merge is a reduce-scatter
+  built from all_to_all_single + libpa's XOR-fold kernel, then an all-gather.
+* Independent keys (configs[4]): keys are dealt round-robin, hashed in batches
+  (pa_hash_batch); no collective on the data path.
 
-The split arithmetic (`row_ranges`, `col_ranges`, window offsets, bit packing of
-shard keys) is host logic; all hashing runs in libpa on each rank's GPU.  With
-the gloo backend and CPU tensors the same driver runs in CI through an injected
-`hash_fn` (see tests/test_dist_cpu.py) -- never on the product path.
+`choose_split` is the cost model that picks the row or the column split for one
+key: per-GPU transform length (rows: n + m/G - 1, cols: n/G + m - 1) against the
+merge traffic (rows: one all-gather of m/8 bytes; cols: reduce-scatter +
+all-gather).  At C4 (n = 10^8, m = 2*10^7) it picks the column split for G >= 2.
+
+The split arithmetic (`row_ranges`, `col_ranges`, window offsets, key blocks) is
+host logic; all hashing runs in libpa on each rank's GPU.  With the gloo backend
+and CPU tensors the same classes run in CI through an injected hash factory (see
+tests/test_dist_cpu.py: the CPU oracle) -- never on the product path.
 """
 from __future__ import annotations
 
+import math
 from typing import Callable
 
 import numpy as np
@@ -29,6 +35,7 @@ import torch
 import torch.distributed as dist
 
 WORD = 32
+COL_ALIGN = 128  # key blocks start on 16-byte boundaries of the packed key (no bit shifting)
 
 
 def split_even(total: int, parts: int) -> list[tuple[int, int]]:
@@ -46,10 +53,7 @@ def row_ranges(m: int, world: int) -> list[tuple[int, int]]:
     """Output rows per rank, each a multiple of 32 except the last (word-aligned
     gather: every rank's slice starts on a uint32 boundary of y)."""
     words = (m + WORD - 1) // WORD
-    out = []
-    for a, b in split_even(words, world):
-        out.append((min(m, a * WORD), min(m, b * WORD)))
-    return out
+    return [(min(m, a * WORD), min(m, b * WORD)) for a, b in split_even(words, world)]
 
 
 def row_seed_offset(r0: int) -> int:
@@ -57,9 +61,11 @@ def row_seed_offset(r0: int) -> int:
     return r0
 
 
-def col_ranges(n: int, m: int, world: int) -> list[tuple[int, int]]:
-    """Key-bit blocks per rank (n_g may be < m: the handles use pa_options.allow_wide)."""
-    return split_even(n, world)
+def col_ranges(n: int, m: int, world: int, align: int = COL_ALIGN) -> list[tuple[int, int]]:
+    """Key-bit blocks per rank, starting at multiples of `align` bits (n_g may be < m: the
+    handles use pa_options.allow_wide; trailing ranks may be empty when n < world * align)."""
+    units = (n + align - 1) // align
+    return [(min(n, a * align), min(n, b * align)) for a, b in split_even(units, world)]
 
 
 def col_seed_offset(n: int, c0: int, c1: int) -> int:
@@ -81,53 +87,60 @@ def _words4(nbits: int) -> int:
     return (w + 3) // 4 * 4
 
 
-class _LibpaHash:
-    """hash_fn backed by libpa on this rank's GPU (the product path)."""
+def _world_rank(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
 
-    def __init__(self):
+
+# ---------------------------------------------------------------- cost model
+def choose_split(n: int, m: int, world: int, ns_per_point: float = 0.0196, link_gbs: float = 300.0,
+                 coll_us: float = 20.0) -> str:
+    """'rows' or 'cols' for one (n, m) key over `world` GPUs: modelled step time =
+    per-GPU transform (ns_per_point x real length, the measured C4 rate) + merge (bytes over
+    NVLink + a fixed latency per collective).  world == 1 -> 'rows' (no split)."""
+    if world <= 1:
+        return "rows"
+    ybytes = m / 8.0
+    t_rows = ns_per_point * (n + math.ceil(m / world) - 1) * 1e-3 + coll_us + ybytes / link_gbs * 1e-3
+    t_cols = (ns_per_point * (math.ceil(n / world) + m - 1) * 1e-3 + 2 * coll_us
+              + 2 * ybytes / link_gbs * 1e-3)
+    return "cols" if t_cols < t_rows else "rows"
+
+
+# ---------------------------------------------------------------- hash factories
+class LibpaFactory:
+    """Per-shard handles from libpa on this rank's GPU (the product path)."""
+
+    def __call__(self, n, m, seed_t, seed_off, allow_wide):
         from . import Hasher
-        self._Hasher = Hasher
-        self._cache = {}
-
-    def __call__(self, n, m, seed_t, seed_off, key_t):
-        k = (n, m, seed_t.data_ptr(), seed_off)
-        h = self._cache.get(k)
-        if h is None:
-            h = self._Hasher(n, m, seed_t, seed_bit_offset=seed_off, allow_wide=m > n)
-            self._cache[k] = h
-        return h.hash(key_t)
-
-    def close(self):
-        for h in self._cache.values():
-            h.close()
-        self._cache.clear()
+        return Hasher(n, m, seed_t, seed_bit_offset=seed_off, allow_wide=allow_wide)
 
 
-def hash_rows(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=None,
-              hash_fn: Callable | None = None) -> torch.Tensor:
-    """Output-row split: returns all ceil(m/32) words of y on every rank."""
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    ranges = row_ranges(m, world)
-    r0, r1 = ranges[rank]
-    hf = hash_fn or _LibpaHash()
-    span = (ranges[0][1] - ranges[0][0]) // WORD  # words per slice (all but the last equal)
-    span = max(span, max((b - a + WORD - 1) // WORD for a, b in ranges))
-    mine = torch.zeros(span, dtype=torch.int32, device=key_t.device)
-    if r1 > r0:
-        part = hf(n, r1 - r0, seed_t, row_seed_offset(r0), key_t)
-        w = (r1 - r0 + WORD - 1) // WORD
-        mine[:w] = part[:w]
-    gathered = torch.empty(world * span, dtype=torch.int32, device=key_t.device)
-    dist.all_gather_into_tensor(gathered, mine, group=group)
-    words = (m + WORD - 1) // WORD
-    out = torch.zeros(words, dtype=torch.int32, device=key_t.device)
-    for g, (a, b) in enumerate(ranges):
-        if b > a:
-            wa, wb = a // WORD, (b + WORD - 1) // WORD
-            out[wa:wb] = gathered[g * span: g * span + (wb - wa)]
-    if hash_fn is None:
-        hf.close()
-    return out
+class FnFactory:
+    """Wraps a plain hash_fn(n, m, seed_t, seed_off, key_t) -> words (test injection)."""
+
+    class _H:
+        def __init__(self, fn, n, m, seed_t, seed_off):
+            self.fn, self.n, self.m, self.seed_t, self.seed_off = fn, n, m, seed_t, seed_off
+
+        def hash(self, key_t):
+            return self.fn(self.n, self.m, self.seed_t, self.seed_off, key_t)
+
+        def close(self):
+            pass
+
+    def __init__(self, fn: Callable):
+        self.fn = fn
+
+    def __call__(self, n, m, seed_t, seed_off, allow_wide):
+        return FnFactory._H(self.fn, n, m, seed_t, seed_off)
+
+
+def _factory(factory=None, hash_fn=None):
+    if factory is not None:
+        return factory
+    return FnFactory(hash_fn) if hash_fn is not None else LibpaFactory()
 
 
 def _xor_fold_libpa(parts: torch.Tensor) -> torch.Tensor:
@@ -148,83 +161,39 @@ def _xor_fold_host(parts: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def hash_cols(n: int, m: int, seed_t: torch.Tensor, key_words: np.ndarray, group=None,
-              hash_fn: Callable | None = None, device=None, xor_fn: Callable | None = None) -> torch.Tensor:
-    """Input-column split with the Eq. (7) XOR merge; returns all ceil(m/32) words of y on
-    every rank.  key_words: the full key (host, LSB-first); each rank uploads its block.
-
-    Merge = XOR reduce-scatter + all-gather: the packed partial (words padded to a
-    multiple of 4*G) is cut into G slices, one all_to_all_single sends slice g to rank g,
-    rank g XOR-folds the G copies of its slice (libpa k_xor_fold), and one
-    all_gather_into_tensor assembles y -- 2 * m/8 bytes per rank on the wire."""
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    c0, c1 = col_ranges(n, m, world)[rank]
-    words = (m + WORD - 1) // WORD
-    dev = device if device is not None else seed_t.device
-    hf = hash_fn or _LibpaHash()
-    fold = xor_fn or (_xor_fold_libpa if dev.type == "cuda" else _xor_fold_host)
-    slice_w = ((words + world - 1) // world + 3) // 4 * 4
-    mine = torch.zeros(world * slice_w, dtype=torch.int32, device=dev)
-    if c1 > c0:
-        blk = extract_bits(key_words, c0, c1 - c0)
-        kt = torch.zeros(_words4(c1 - c0), dtype=torch.int32)
-        kt[:blk.size] = torch.from_numpy(blk.view(np.int32))
-        part = hf(c1 - c0, m, seed_t, col_seed_offset(n, c0, c1), kt.to(dev))
-        mine[:words] = part[:words]
-    recv = torch.empty_like(mine)
-    dist.all_to_all_single(recv, mine, group=group)
-    myslice = fold(recv.view(world, slice_w))
-    gathered = torch.empty(world * slice_w, dtype=torch.int32, device=dev)
-    dist.all_gather_into_tensor(gathered, myslice, group=group)
-    if hash_fn is None:
-        hf.close()
-    return gathered[:words].clone()
-
-
-def hash_keys(n: int, m: int, seed_t: torch.Tensor, keys: torch.Tensor, group=None,
-              hash_fn: Callable | None = None) -> tuple[list[int], torch.Tensor]:
-    """Independent keys: rank g hashes keys g, g+W, g+2W, ... of `keys` ((count, words)).
-    Returns (indices, outputs) for this rank; no data-path collective."""
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    idx = list(range(rank, keys.shape[0], world))
-    hf = hash_fn or _LibpaHash()
-    outs = torch.zeros((len(idx), _words4(m)), dtype=torch.int32, device=keys.device)
-    for i, k in enumerate(idx):
-        o = hf(n, m, seed_t, 0, keys[k].contiguous())
-        outs[i, :o.numel()] = o[: outs.shape[1]]
-    if hash_fn is None:
-        hf.close()
-    return idx, outs
+def distribute_seed(seed_t: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """Create-time seed distribution: the source rank's seed words are broadcast in place
+    (every shard window is a slice of them; the seed is bound once)."""
+    w, _ = _world_rank(group)
+    if w > 1:
+        dist.broadcast(seed_t, src, group=group)
+    return seed_t
 
 
 # ---------------------------------------------------------------- persistent sharded hashers
-def _world_rank(group):
-    if dist.is_available() and dist.is_initialized():
-        return dist.get_world_size(group), dist.get_rank(group)
-    return 1, 0
-
-
 class RowSplit:
     """Output-row split of one (n, m) hash (BASELINE configs[3], "output rows sharded with NCCL
     gather"): this rank owns rows row_ranges(m, W)[rank] and keeps a handle on the seed window
     at offset r0 (n + m_g - 1 bits, P:88-92 per row block); each call hashes the full key
-    (device words, every rank holds it) and one all_gather_into_tensor assembles y.  Per-rank
-    transform >= n + m/W - 1: it barely shrinks."""
+    (device words; with src set it is first broadcast from rank src) and one
+    all_gather_into_tensor assembles y.  Per-rank transform >= n + m/W - 1."""
 
-    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None):
-        from . import Hasher
+    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None, factory=None, hash_fn=None):
         self.n, self.m, self.group = n, m, group
         self.world, self.rank = _world_rank(group)
         self.ranges = row_ranges(m, self.world)
         r0, r1 = self.ranges[self.rank]
         self.span = max((b - a + WORD - 1) // WORD for a, b in self.ranges)
-        self.h = Hasher(n, r1 - r0, seed_t, seed_bit_offset=row_seed_offset(r0), allow_wide=True) if r1 > r0 else None
+        fac = _factory(factory, hash_fn)
+        self.h = fac(n, r1 - r0, seed_t, row_seed_offset(r0), True) if r1 > r0 else None
         dev = seed_t.device
         self.mine = torch.zeros(self.span, dtype=torch.int32, device=dev)
         self.gathered = torch.empty(self.world * self.span, dtype=torch.int32, device=dev)
         self.out = torch.zeros((m + WORD - 1) // WORD, dtype=torch.int32, device=dev)
 
-    def __call__(self, key_t: torch.Tensor) -> torch.Tensor:
+    def __call__(self, key_t: torch.Tensor, src: int | None = None) -> torch.Tensor:
+        if src is not None and self.world > 1:
+            dist.broadcast(key_t, src, group=self.group)  # every rank hashes the whole key
         if self.h is not None:
             part = self.h.hash(key_t)
             w = min(self.span, part.numel())
@@ -245,34 +214,59 @@ class RowSplit:
 
 class ColSplit:
     """Input-column split (the paper's Eq. (4) key blocks, with the Eq. (7) modulo-2
-    merge): this rank owns key bits col_ranges(n, m, W)[rank] -- the layout when each
-    GPU already holds its own decoded key segment -- and keeps a handle on the seed
-    window at offset n - c1.  Each call hashes this rank's key block (device words, see
-    key_block) and merges: XOR reduce-scatter (one all_to_all_single + libpa's pa_xor_fold; NCCL
-    has no XOR op) then one all_gather_into_tensor.  Per-rank transform >= n/W + m - 1."""
+    merge): this rank owns key bits col_ranges(n, m, W)[rank] (128-bit aligned) -- the
+    layout when each GPU already holds its own decoded key segment, or scattered from a
+    source rank each step (scatter_key) -- and keeps a handle on the seed window at offset
+    n - c1.  Each call hashes this rank's key block and merges: XOR reduce-scatter (one
+    all_to_all_single + an XOR fold; NCCL has no XOR op) then one all_gather_into_tensor.
+    Per-rank transform >= n/W + m - 1."""
 
-    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None):
-        from . import Hasher
+    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None, factory=None, hash_fn=None,
+                 xor_fn: Callable | None = None):
         self.n, self.m, self.group = n, m, group
         self.world, self.rank = _world_rank(group)
-        self.c0, self.c1 = col_ranges(n, m, self.world)[self.rank]
+        self.ranges = col_ranges(n, m, self.world)
+        self.c0, self.c1 = self.ranges[self.rank]
         ng = self.c1 - self.c0
-        self.h = Hasher(ng, m, seed_t, seed_bit_offset=col_seed_offset(n, self.c0, self.c1),
-                        allow_wide=m > ng) if ng > 0 else None
+        fac = _factory(factory, hash_fn)
+        self.h = fac(ng, m, seed_t, col_seed_offset(n, self.c0, self.c1), m > ng) if ng > 0 else None
         dev = seed_t.device
+        self.device = dev
+        self.fold = xor_fn or (_xor_fold_libpa if dev.type == "cuda" else _xor_fold_host)
         self.words = (m + WORD - 1) // WORD
         self.slice_w = ((self.words + self.world - 1) // self.world + 3) // 4 * 4
         self.mine = torch.zeros(self.world * self.slice_w, dtype=torch.int32, device=dev)
         self.recv = torch.empty_like(self.mine)
         self.gathered = torch.empty(self.world * self.slice_w, dtype=torch.int32, device=dev)
+        # key scatter: equal chunks of blk_w words (the widest block), block g at word c0_g / 32
+        self.blk_w = max(_words4(b - a) for a, b in self.ranges)
+        self.blk = torch.zeros(self.blk_w, dtype=torch.int32, device=dev)
 
     def key_block(self, key_words: np.ndarray, device) -> torch.Tensor:
-        """This rank's key bits [c0, c1) as word-aligned device words (host-side extraction)."""
+        """This rank's key bits [c0, c1) as device words (host-side extraction)."""
         ng = self.c1 - self.c0
         blk = extract_bits(key_words, self.c0, ng)
-        kt = torch.zeros(_words4(ng), dtype=torch.int32)
+        kt = torch.zeros(max(4, _words4(ng)), dtype=torch.int32)
         kt[:blk.size] = torch.from_numpy(blk.view(np.int32))
         return kt.to(device)
+
+    def scatter_key(self, key_t: torch.Tensor | None, src: int = 0) -> torch.Tensor:
+        """Per-step key distribution for the column split: rank src holds the whole key (device
+        words, >= ceil(n/32)); every rank receives its block (blocks start on 128-bit
+        boundaries, so a block is a word slice; bits past c1 are ignored by the handle)."""
+        if self.world == 1:
+            return key_t
+        chunks = None
+        if self.rank == src:
+            chunks = []
+            for a, b in self.ranges:
+                c = torch.zeros(self.blk_w, dtype=torch.int32, device=self.device)
+                if b > a:
+                    wa, wb = a // WORD, min(key_t.numel(), (b + WORD - 1) // WORD)
+                    c[: wb - wa] = key_t[wa:wb]
+                chunks.append(c)
+        dist.scatter(self.blk, chunks, src=src, group=self.group)
+        return self.blk
 
     def __call__(self, key_block_t: torch.Tensor) -> torch.Tensor:
         if self.h is not None:
@@ -281,10 +275,89 @@ class ColSplit:
         if self.world == 1:
             return self.mine[: self.words]
         dist.all_to_all_single(self.recv, self.mine, group=self.group)
-        myslice = _xor_fold_libpa(self.recv.view(self.world, self.slice_w))
+        myslice = self.fold(self.recv.view(self.world, self.slice_w))
         dist.all_gather_into_tensor(self.gathered, myslice, group=self.group)
         return self.gathered[: self.words]
 
     def close(self):
         if self.h is not None:
             self.h.close()
+
+
+class KeyDeal:
+    """Independent keys (BASELINE configs[4]): this rank hashes keys rank, rank + W, ... of a
+    batch in one pa_hash_batch (shared seed spectrum per GPU); no data-path collective."""
+
+    def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None, factory=None, hash_fn=None):
+        self.n, self.m = n, m
+        self.world, self.rank = _world_rank(group)
+        self.h = _factory(factory, hash_fn)(n, m, seed_t, 0, False)
+
+    def indices(self, count: int) -> list[int]:
+        return list(range(self.rank, count, self.world))
+
+    def __call__(self, keys: torch.Tensor, outs: torch.Tensor | None = None) -> torch.Tensor:
+        """keys: this rank's keys, (count_mine, words) -- already dealt."""
+        if hasattr(self.h, "hash_batch"):
+            return self.h.hash_batch(keys, outs)
+        res = torch.zeros((keys.shape[0], _words4(self.m)), dtype=torch.int32, device=keys.device)
+        for i in range(keys.shape[0]):
+            o = self.h.hash(keys[i].contiguous())
+            res[i, :min(o.numel(), res.shape[1])] = o[: res.shape[1]]
+        return res
+
+    def close(self):
+        self.h.close()
+
+
+# ---------------------------------------------------------------- one-shot entry points
+def hash_rows(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=None,
+              hash_fn: Callable | None = None, factory=None, src: int | None = None) -> torch.Tensor:
+    """Output-row split: returns all ceil(m/32) words of y on every rank."""
+    sh = RowSplit(n, m, seed_t, group, factory, hash_fn)
+    try:
+        return sh(key_t, src).clone()
+    finally:
+        sh.close()
+
+
+def hash_cols(n: int, m: int, seed_t: torch.Tensor, key_words: np.ndarray | None, group=None,
+              hash_fn: Callable | None = None, device=None, xor_fn: Callable | None = None, factory=None,
+              key_t: torch.Tensor | None = None, src: int | None = None) -> torch.Tensor:
+    """Input-column split with the Eq. (7) XOR merge; returns all ceil(m/32) words of y on
+    every rank.  The key block comes from key_words (the full key on the host, each rank
+    extracts its block) or, with src set, is scattered from rank src's device key_t."""
+    dev = device if device is not None else seed_t.device
+    sh = ColSplit(n, m, seed_t, group, factory, hash_fn, xor_fn)
+    try:
+        blk = sh.scatter_key(key_t, src) if src is not None else sh.key_block(key_words, dev)
+        return sh(blk).clone()
+    finally:
+        sh.close()
+
+
+def hash_keys(n: int, m: int, seed_t: torch.Tensor, keys: torch.Tensor, group=None,
+              hash_fn: Callable | None = None, factory=None) -> tuple[list[int], torch.Tensor]:
+    """Independent keys: rank g hashes keys g, g+W, g+2W, ... of `keys` ((count, words)) as one
+    batch.  Returns (indices, outputs) for this rank; no data-path collective."""
+    kd = KeyDeal(n, m, seed_t, group, factory, hash_fn)
+    try:
+        idx = kd.indices(keys.shape[0])
+        if not idx:
+            return idx, torch.zeros((0, _words4(m)), dtype=torch.int32, device=keys.device)
+        return idx, kd(keys[idx].contiguous())
+    finally:
+        kd.close()
+
+
+def hash(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=None, split: str = "auto",
+         src: int = 0, factory=None, hash_fn: Callable | None = None, xor_fn: Callable | None = None):
+    """One key over all ranks of `group`, the split chosen by choose_split (or forced):
+    rank src holds the key (device words); returns (split, y words) on every rank."""
+    world, _ = _world_rank(group)
+    if split == "auto":
+        split = choose_split(n, m, world)
+    if split == "rows":
+        return split, hash_rows(n, m, seed_t, key_t, group, hash_fn, factory, src=src)
+    return split, hash_cols(n, m, seed_t, None, group, hash_fn, key_t.device, xor_fn, factory,
+                            key_t=key_t, src=src)
