@@ -68,6 +68,18 @@ typedef enum pa_route {
     PA_ROUTE_BITPACKED = 2
 } pa_route;
 
+/* Arithmetic of route (a)'s transform (SURVEY 8(b) "Create").  FP64 is the one built: an
+ * FP64 complex transform with a proven < 0.5 rounding bound.  The
+ * number-theoretic transforms are not built -- an NTT over a 32-bit prime costs ~190 integer
+ * operations per real point and does not beat FP64 on B200 -- and are
+ * rejected with PA_ERR_UNSUPPORTED naming the field. */
+typedef enum pa_arith {
+    PA_ARITH_AUTO = 0,
+    PA_ARITH_FP64 = 1,
+    PA_ARITH_NTT32 = 2,
+    PA_ARITH_NTT64 = 3
+} pa_arith;
+
 #define PA_RESIDUAL_LIMIT 0.25
 
 typedef struct pa_options {
@@ -89,7 +101,13 @@ typedef struct pa_options {
                                  128-bit block's transform (>= 128 + m - 1) exceeds it.  Ignored
                                  by route (b).  With 0, pa_create splits by itself when n + m is
                                  beyond one transform (~3.3e8 bits; pa_plan reports the blocks) */
-    uint32_t reserved[3];     /* must be zero */
+    int32_t arith;            /* pa_arith: AUTO or FP64 (route (a)); NTT32 / NTT64 -> PA_ERR_UNSUPPORTED */
+    int32_t device;           /* CUDA device of the handle: -1 (pa_options_init's default) = the
+                                 caller's current device at create; >= 0 = that device.  Every
+                                 later call on the handle runs on it (the library switches to it
+                                 for the call and back); seed, keys, outputs and workspace must
+                                 live there and `stream` must belong to it */
+    uint32_t reserved[1];     /* must be zero */
 } pa_options;
 
 /* Runtime facts about a handle (all lengths in bits or elements). */
@@ -107,7 +125,8 @@ typedef struct pa_info {
                                  cols_per_cta, or half of it when that fits two CTAs per SM */
 } pa_info;
 
-/* Fill *opt with defaults (route AUTO, offset 0, library batch width, no split). */
+/* Fill *opt with defaults (route AUTO, arith AUTO, device -1 = current, offset 0, library
+ * batch width, no split). */
 pa_status pa_options_init(pa_options *opt);
 
 /* Create a hashing context for n-bit keys and m-bit outputs with the
@@ -187,7 +206,8 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
 pa_status pa_hash_host(pa_handle h, const uint32_t *key_host, uint32_t *out_host, void *stream);
 
 /* pa_hash_host without the final synchronisation: the copies and kernels are
- * enqueued on `stream` (as one CUDA graph) and *out_host is valid once the stream
+ * enqueued on `stream` (as one CUDA graph, re-captured when the handle's work buffers have
+ * moved or a host buffer's mapping changed) and *out_host is valid once the stream
  * reaches this point.  Lets a caller stream keys through a handle: successive calls
  * on the same stream serialise on the GPU but not on the host.  key_host must stay
  * unchanged and out_host unread until then. */
@@ -198,7 +218,9 @@ pa_status pa_hash_host_async(pa_handle h, const uint32_t *key_host, uint32_t *ou
  * k*out_stride_words.  Keys move in chunks through two device staging slots: chunk i+1's
  * host->device copy and chunk i-1's device->host copy (copy engines, on a stream of the handle)
  * overlap chunk i's hash on `stream`.  Synchronises `stream` before returning.  Strides in uint32 words (>= ceil(n/32) and
- * ceil(m/32)).  Staging grows on demand (a workspace handle: PA_ERR_NOMEM beyond count = 1). */
+ * ceil(m/32)).  Staging grows on demand; a workspace handle (pa_create_ws) allocates nothing
+ * more and hashes the keys one at a time through its own pa_hash_host staging instead.  On an
+ * error the copies already enqueued are drained before returning. */
 pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t key_stride_words,
                              uint32_t *outs_host, uint64_t out_stride_words, uint32_t count, void *stream);
 

@@ -103,6 +103,44 @@ void dev_free(pa_ctx *h, void *p)
     if (p && !h->arena) cudaFree(p);
 }
 
+void reap(pa_ctx *h, bool wait)
+{
+    int k = 0;
+    for (int i = 0; i < h->ngrave; ++i) {
+        if (wait) cudaEventSynchronize(h->grave_ev[i]);
+        if (wait || cudaEventQuery(h->grave_ev[i]) == cudaSuccess) {
+            cudaFree(h->grave[i]);
+            cudaEventDestroy(h->grave_ev[i]);
+        } else {
+            h->grave[k] = h->grave[i];
+            h->grave_ev[k++] = h->grave_ev[i];
+        }
+    }
+    cudaGetLastError();  // a not-ready query is not an error
+    h->ngrave = k;
+}
+
+void defer_free(pa_ctx *h, void *p, cudaStream_t s)
+{
+    if (!p || h->arena) return;
+    reap(h, false);
+    if (h->ngrave == pa_ctx::kGrave) {  // full: wait for the oldest
+        cudaEventSynchronize(h->grave_ev[0]);
+        reap(h, false);
+    }
+    cudaEvent_t ev = nullptr;
+    if (h->ngrave == pa_ctx::kGrave || cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, s) != cudaSuccess) {
+        if (ev) cudaEventDestroy(ev);
+        cudaGetLastError();
+        cudaStreamSynchronize(s);
+        cudaFree(p);
+        return;
+    }
+    h->grave[h->ngrave] = p;
+    h->grave_ev[h->ngrave++] = ev;
+}
+
 static cudaEvent_t prof_event(Profiler &P)
 {
     if (P.npool > 0) return P.pool[--P.npool];
@@ -171,6 +209,23 @@ static void prof_free(Profiler &P)
 
 using namespace pa;
 
+namespace {
+// Every call on a handle runs on the handle's device (pa_options.device): switch for the call
+// and back (a no-op when it is already current).
+struct DeviceGuard {
+    int prev = -1;
+    bool sw = false;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) sw = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard()
+    {
+        if (sw) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
 extern "C" {
 
 static void drop_host_graph(pa_ctx *h);
@@ -201,6 +256,8 @@ pa_status pa_options_init(pa_options *opt)
     memset(opt, 0, sizeof *opt);
     opt->struct_size = sizeof *opt;
     opt->route = PA_ROUTE_AUTO;
+    opt->arith = PA_ARITH_AUTO;
+    opt->device = -1;
     return PA_OK;
 }
 
@@ -212,6 +269,7 @@ static void destroy_ctx(pa_ctx *h)
     delete[] h->sub_c0;
     prof_free(h->prof);
     drop_host_graph(h);
+    reap(h, true);
     ra_destroy(h);
     rb_destroy(h);
     dev_free(h, h->stage_blk);
@@ -267,7 +325,20 @@ static pa_status parse_options(const pa_options *opt, uint64_t n, uint64_t m, pa
         set_error("opt->batch_keys = %u exceeds 4096", o->batch_keys);
         return PA_ERR_INVALID_ARG;
     }
-    for (int i = 0; i < 3; ++i)
+    if (o->arith == PA_ARITH_NTT32 || o->arith == PA_ARITH_NTT64) {
+        set_error("opt->arith = %d: the number-theoretic transforms are not built (FP64 is the route-(a) "
+                  "arithmetic; use PA_ARITH_AUTO or PA_ARITH_FP64)", o->arith);
+        return PA_ERR_UNSUPPORTED;
+    }
+    if (o->arith != PA_ARITH_AUTO && o->arith != PA_ARITH_FP64) {
+        set_error("opt->arith = %d is not a pa_arith", o->arith);
+        return PA_ERR_INVALID_ARG;
+    }
+    if (o->device < -1) {
+        set_error("opt->device = %d: use -1 (current device) or a CUDA device ordinal", o->device);
+        return PA_ERR_INVALID_ARG;
+    }
+    for (int i = 0; i < 1; ++i)
         if (o->reserved[i]) {
             set_error("opt->reserved[%d] = %u must be 0", i, o->reserved[i]);
             return PA_ERR_INVALID_ARG;
@@ -375,9 +446,18 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
     pa_options o;
     pa_status st = parse_options(opt, n, m, &o);
     if (st != PA_OK) return st;
-    int dev = 0;
+    int dev = 0, ndev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (o.device >= 0) {
+        if ((e = cudaGetDeviceCount(&ndev)) != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+        if (o.device >= ndev) {
+            set_error("opt->device = %d, but %d CUDA device(s) are visible", o.device, ndev);
+            return PA_ERR_INVALID_ARG;
+        }
+        dev = o.device;
+    }
+    DeviceGuard dg(dev);
     if ((st = check_dev_ptr(seed_bits, "seed_bits", dev)) != PA_OK) return st;
     if (workspace) {
         if ((st = check_dev_ptr(workspace, "workspace", dev)) != PA_OK) return st;
@@ -533,6 +613,7 @@ pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream)
         set_error("handle is NULL");
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     pa_status st = check_dev_ptr(seed_bits, "seed_bits", h->device);
     if (st != PA_OK) return st;
     return seed_impl(h, seed_bits, (cudaStream_t)stream);
@@ -590,6 +671,7 @@ static pa_status hash_impl(pa_handle h, const uint32_t *key, uint32_t *out, uint
         set_error("handle is NULL");
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     if (validate) {
         pa_status st;
         // the output is zeroed before (or while) the key is read: they must not share memory
@@ -653,6 +735,7 @@ pa_status pa_hash_batch(pa_handle h, const uint32_t *keys, uint64_t key_stride_w
         set_error("handle is NULL");
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     pa_status st;
     if ((st = check_strides(h, key_stride_words, out_stride_words)) != PA_OK) return st;
     if (count == 0) return PA_OK;
@@ -677,6 +760,7 @@ pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_
         set_error("handle is NULL");
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     pa_status st;
     if ((st = check_strides(h, key_stride_words, out_stride_words)) != PA_OK) return st;
     if (seed_stride_words < (h->off + h->L + 31) / 32 || (seed_stride_words & 3)) {
@@ -688,6 +772,14 @@ pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_
     if ((st = check_dev_ptr(seeds, "seeds", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(keys, "keys", h->device)) != PA_OK) return st;
     if ((st = check_dev_ptr(outs, "outs", h->device)) != PA_OK) return st;
+    // K1 zeroes the outputs while keys and seeds are being read: no sharing with them
+    const uint64_t out_bytes = ((uint64_t)(count - 1) * out_stride_words + (h->m + 31) / 32) * 4;
+    if (overlaps(keys, ((uint64_t)(count - 1) * key_stride_words + (h->n + 31) / 32) * 4, outs, out_bytes) ||
+        overlaps(seeds, ((uint64_t)(count - 1) * seed_stride_words + (h->off + h->L + 31) / 32) * 4, outs,
+                 out_bytes)) {
+        set_error("pa_hash_fresh_batch: outs overlaps keys or seeds");
+        return PA_ERR_INVALID_ARG;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     if (h->route == PA_ROUTE_TRANSFORM && !h->nsub) {  // batched seed transforms + batched hashes
         st = ra_fresh_batch(h, seeds, seed_stride_words, keys, key_stride_words, outs, out_stride_words, count,
@@ -726,7 +818,7 @@ __global__ void k_host_copy(const uint32_t *__restrict__ src, uint32_t *__restri
 static uint64_t host_copy_max_bytes()
 {
     static const uint64_t v = [] {
-        const char *e = getenv("PA_HOST_COPY_MAX");  // developer override: 0 = always the copy engines
+        const char *e = dev_env("PA_HOST_COPY_MAX");  // developer override: 0 = always the copy engines
         return e ? (uint64_t)strtoull(e, nullptr, 0) : ~(uint64_t)0;
     }();
     return v;
@@ -779,6 +871,15 @@ static cudaError_t set_copy_node(cudaGraphExec_t ex, cudaGraphNode_t node, const
     return cudaGraphExecKernelNodeSetParams(ex, node, &p);
 }
 
+// generation of every work buffer a pa_hash_host graph may have captured (bumped by each
+// reallocation, route_a.cu carve_work): a graph captured under another generation is stale
+static uint64_t work_gen(const pa_ctx *h)
+{
+    uint64_t g = h->a.wgen;
+    for (uint32_t i = 0; h->sub && i < h->nsub; ++i) g += work_gen(h->sub[i]);
+    return g;
+}
+
 static void drop_host_graph(pa_ctx *h)
 {
     if (h->host_exec) cudaGraphExecDestroy(h->host_exec);
@@ -789,6 +890,8 @@ static void drop_host_graph(pa_ctx *h)
     h->host_copy = 0;
     h->g_key_host = nullptr;
     h->g_out_host = nullptr;
+    h->g_key_dev = nullptr;
+    h->g_out_dev = nullptr;
 }
 
 // Capture H2D + the hash kernels + D2H once; later calls patch the two memcpy
@@ -854,6 +957,9 @@ static pa_status build_host_graph(pa_ctx *h, const uint32_t *key_host, uint32_t 
     h->host_copy = mode;
     h->g_key_host = key_host;
     h->g_out_host = out_host;
+    h->g_key_dev = mode == 2 ? mapped_ptr(key_host) : nullptr;
+    h->g_out_dev = mode == 2 ? mapped_ptr(out_host) : nullptr;
+    h->g_wgen = work_gen(h);
     return PA_OK;
 }
 
@@ -865,6 +971,7 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
                   (const void *)key_host, (void *)out_host);
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     cudaStream_t s = (cudaStream_t)stream;
     size_t kb = ((h->n + 31) / 32) * 4, ob = ((h->m + 31) / 32) * 4;
     cudaError_t e;
@@ -874,8 +981,17 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
         h->stage_key = (uint32_t *)h->stage_blk;
         h->stage_out = (uint32_t *)(h->stage_blk + al256(kb));
     }
-    const bool moved = key_host != h->g_key_host || out_host != h->g_out_host;
-    const int mode = h->host_exec && !moved ? h->host_copy : pick_host_copy(h, key_host, out_host);
+    // a graph captured before the work buffers moved (a larger batch / fresh-seed batch since)
+    // holds stale kernel arguments: capture again
+    if (h->host_exec && work_gen(h) != h->g_wgen) drop_host_graph(h);
+    // copy kernels address the host buffers through their mapped device pointers: re-derive them
+    // every call (a freed pinned buffer's address may come back pageable or mapped elsewhere)
+    const void *kdev = mapped_ptr(key_host);
+    void *odev = mapped_ptr(out_host);
+    if (h->host_exec && h->host_copy == 2 && (!kdev || !odev)) drop_host_graph(h);
+    const bool moved = key_host != h->g_key_host || out_host != h->g_out_host || kdev != h->g_key_dev ||
+                       odev != h->g_out_dev;
+    const int mode = h->host_exec && !moved ? h->host_copy : !kdev || !odev ? 0 : pick_host_copy(h, key_host, out_host);
     if (h->prof.on || mode == 0) {  // per-launch profiling events need the plain launches
         if ((e = cudaMemcpyAsync(h->stage_key, key_host, kb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
             return cuda_fail(e, "pa_hash_host H2D");
@@ -889,21 +1005,21 @@ static pa_status hash_host_impl(pa_handle h, const uint32_t *key_host, uint32_t 
             pa_status st = build_host_graph(h, key_host, out_host, kb, ob, mode);
             if (st != PA_OK) return st;
         }
-        if (key_host != h->g_key_host) {
-            e = mode == 2 ? set_copy_node(h->host_exec, h->h2d_node, (const uint32_t *)mapped_ptr(key_host),
-                                          h->stage_key, kb / 4)
+        if (key_host != h->g_key_host || (mode == 2 && kdev != h->g_key_dev)) {
+            e = mode == 2 ? set_copy_node(h->host_exec, h->h2d_node, (const uint32_t *)kdev, h->stage_key, kb / 4)
                           : cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->h2d_node, h->stage_key, key_host,
                                                                kb, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return cuda_fail(e, "pa_hash_host graph update (key)");
             h->g_key_host = key_host;
+            h->g_key_dev = mode == 2 ? kdev : nullptr;
         }
-        if (out_host != h->g_out_host) {
-            e = mode == 2 ? set_copy_node(h->host_exec, h->d2h_node, h->stage_out,
-                                          (uint32_t *)mapped_ptr(out_host), ob / 4)
+        if (out_host != h->g_out_host || (mode == 2 && odev != h->g_out_dev)) {
+            e = mode == 2 ? set_copy_node(h->host_exec, h->d2h_node, h->stage_out, (uint32_t *)odev, ob / 4)
                           : cudaGraphExecMemcpyNodeSetParams1D(h->host_exec, h->d2h_node, out_host, h->stage_out,
                                                                ob, cudaMemcpyDeviceToHost);
             if (e != cudaSuccess) return cuda_fail(e, "pa_hash_host graph update (out)");
             h->g_out_host = out_host;
+            h->g_out_dev = mode == 2 ? odev : nullptr;
         }
         if ((e = cudaGraphLaunch(h->host_exec, s)) != cudaSuccess) return cuda_fail(e, "pa_hash_host graph launch");
     }
@@ -918,6 +1034,7 @@ pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t ke
         set_error("pa_hash_host_batch: NULL argument");
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     const uint64_t kw = (h->n + 31) / 32, ow = (h->m + 31) / 32;
     if (key_stride_words < kw || out_stride_words < ow) {
         set_error("pa_hash_host_batch: key_stride_words = %llu (need >= %llu), out_stride_words = %llu (need >= "
@@ -971,6 +1088,13 @@ pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t ke
     if (chunk > 1 && batch_grows(h, chunk)) drop_host_graph(h);  // work buffers are about to move
     cudaStream_t cs = h->cstream;
     cudaEvent_t *h2d = h->pev, *comp = h->pev + 2, start = h->pev[4];
+    // an error mid-pipeline: copies into the caller's host buffers may be in flight on the copy
+    // stream -- let them finish before returning, so the caller may free / reuse the buffers
+    auto fail = [&](pa_status st) {
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(s);
+        return st;
+    };
     auto kslot = [&](uint32_t i) { return (uint32_t *)h->bstage + (i % nslot) * slot_words; };
     auto oslot = [&](uint32_t i) { return kslot(i) + (size_t)chunk * kw4; };
     auto keys_of = [&](uint32_t i) { return count - i * chunk < chunk ? count - i * chunk : chunk; };
@@ -981,24 +1105,24 @@ pa_status pa_hash_host_batch(pa_handle h, const uint32_t *keys_host, uint64_t ke
     const uint32_t nch = (count + chunk - 1) / chunk;
     cudaEventRecord(start, s);  // earlier work on `stream` may still use the staging / work buffers
     cudaStreamWaitEvent(cs, start, 0);
-    if ((e = h2d_chunk(0)) != cudaSuccess) return cuda_fail(e, "pa_hash_host_batch H2D");
+    if ((e = h2d_chunk(0)) != cudaSuccess) return fail(cuda_fail(e, "pa_hash_host_batch H2D"));
     cudaEventRecord(h2d[0], cs);
     for (uint32_t i = 0; i < nch; ++i) {
         const uint32_t sl = i % nslot;
         if (i + 1 < nch) {  // next chunk's keys, once chunk i-1 (same slot) has consumed its own
             if (i >= 1) cudaStreamWaitEvent(cs, comp[(i + 1) % nslot], 0);
-            if ((e = h2d_chunk(i + 1)) != cudaSuccess) return cuda_fail(e, "pa_hash_host_batch H2D");
+            if ((e = h2d_chunk(i + 1)) != cudaSuccess) return fail(cuda_fail(e, "pa_hash_host_batch H2D"));
             cudaEventRecord(h2d[(i + 1) % nslot], cs);
         }
         // chunk i-2's outputs left this slot before chunk i's keys arrived (copy stream order)
         cudaStreamWaitEvent(s, h2d[sl], 0);
         pa_status st = batch_impl(h, kslot(i), kw4, oslot(i), ow4, keys_of(i), ow, s);
-        if (st != PA_OK) return st;
+        if (st != PA_OK) return fail(st);
         cudaEventRecord(comp[sl], s);
         cudaStreamWaitEvent(cs, comp[sl], 0);
         if ((e = cudaMemcpy2DAsync(outs_host + (size_t)i * chunk * out_stride_words, out_stride_words * 4, oslot(i),
                                    ow4 * 4, ow * 4, keys_of(i), cudaMemcpyDeviceToHost, cs)) != cudaSuccess)
-            return cuda_fail(e, "pa_hash_host_batch D2H");
+            return fail(cuda_fail(e, "pa_hash_host_batch D2H"));
     }
     cudaEventRecord(start, cs);
     cudaStreamWaitEvent(s, start, 0);
@@ -1022,6 +1146,7 @@ pa_status pa_residual(pa_handle h, double *max_residual, void *stream)
         set_error("pa_residual: NULL argument");
         return PA_ERR_INVALID_ARG;
     }
+    DeviceGuard dg(h->device);
     *max_residual = 0.0;
     if (h->route != PA_ROUTE_TRANSFORM) return PA_OK;
     cudaStream_t s = (cudaStream_t)stream;

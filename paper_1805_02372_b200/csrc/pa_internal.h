@@ -4,11 +4,21 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/pa.h"
 #include "fft_core.cuh"
 
 namespace pa {
+
+// Developer overrides (plan / kernel-variant experiments, tools/dev/) exist only in a PA_DEV
+// build (PA_DEV=1 python paper_1805_02372_b200/build.py); the product library ignores the
+// environment.
+#ifdef PA_DEV
+inline const char *dev_env(const char *k) { return getenv(k); }
+#else
+inline const char *dev_env(const char *) { return nullptr; }
+#endif
 
 // ---------------------------------------------------------------- route (a)
 // FP64 negacyclic ("right-angle") convolution of length N = 2M real points
@@ -31,6 +41,9 @@ struct Geometry {
     uint32_t pf2;           // K2: L2 prefetch distance in rows (0 = off)
     uint32_t lr;            // K2 -> K3 array: rows in blocks of 2^lr (route_a.cu wrow / wcol)
     bool k3t;               // K3 as the persistent TMEM-staged k3t_inv_columns (opt-in)
+    uint32_t k1p_kmax;      // K1 as the persistent TMEM write-behind k1p_fwd_columns: last-stage
+                            // butterflies per thread (1 or 2); 0 = plain k1_fwd_columns
+    uint32_t smem1p;        // K1P dynamic shared bytes (K1's + a second key-bit buffer)
     int k2shape;            // K2 as k2_rows_t<R0, R1> (1: 16,16  2: 5,8  3: 3,8  4: 7,4), 0: k2_rows
     int k13;                // K1/K3 instantiation (route_a.cu kK13), 0: general
 };
@@ -56,6 +69,7 @@ struct RouteA {
     unsigned long long *resid = nullptr; // max |v - rint v| (as double bits)
     uint32_t *kb = nullptr;    // K0 output: per-column-group bit streams of the input
     uint32_t cap = 0;          // keys the work buffers (buf, kb) hold
+    uint64_t wgen = 0;         // bumped whenever the work buffers move (cached host graphs check it)
     bool shared_w = false;     // work block borrowed from the first column block (not owned)
     double2 *fspec = nullptr;  // pa_hash_fresh_batch: one spectrum per key of a chunk
     uint32_t fcap = 0;         // keys fspec holds
@@ -133,6 +147,15 @@ struct pa_ctx {
     int host_copy = 0;  // how the graph moves the key / output: 1 copy engines, 2 copy kernels (mapped pages)
     const void *g_key_host = nullptr;
     void *g_out_host = nullptr;
+    const void *g_key_dev = nullptr;  // mapped device addresses the graph's copy kernels use
+    void *g_out_dev = nullptr;
+    uint64_t g_wgen = 0;              // work-buffer generation the graph was captured with
+    // replaced device blocks, freed once the stream that last used them passes an event
+    // (stream-ordered reallocation instead of a device-wide synchronisation)
+    static constexpr int kGrave = 8;
+    void *grave[kGrave] = {};
+    cudaEvent_t grave_ev[kGrave] = {};
+    int ngrave = 0;
 };
 
 namespace pa {
@@ -169,6 +192,9 @@ size_t rb_bytes(uint64_t n, uint64_t m);
 // device memory from the handle's arena or cudaMalloc (dev_free is a no-op for arena memory)
 pa_status dev_alloc(pa_ctx *h, void **p, size_t bytes, const char *what);
 void dev_free(pa_ctx *h, void *p);
+// free p (cudaMalloc'ed) after the work enqueued on s so far; reap frees what has passed
+void defer_free(pa_ctx *h, void *p, cudaStream_t s);
+void reap(pa_ctx *h, bool wait);
 
 void set_error(const char *fmt, ...);
 // bracket one kernel launch with profiling events (no-ops unless enabled)

@@ -503,6 +503,207 @@ k1_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geome
     TRACE_END(1);
 }
 
+// ------------------------------------------------------------------ TMEM helpers
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void cta_sync_tmem()  // barrier ordering tcgen05 traffic across warps
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ K1P (TMEM write-behind K1)
+// K1 for one-CTA-per-SM tiles of a multi-wave grid (C4, C5c/d): every non-persistent K1 CTA
+// ends with a burst of N2 x C scattered 32-byte row-piece stores (the last DIF stage writing
+// HBM; ~14 k of ~43 k cycles per tile at C4) that nothing overlaps, because shared memory
+// holds one tile.  Tensor memory (256 KB per SM, idle in this pass) holds the finished tile
+// instead: K1P is persistent (one CTA per SM, tables loaded once, the next tile's key bits
+// prefetched with cp.async), its last DIF stage writes each butterfly's 16 outputs to the
+// thread's own TMEM lane (tcgen05.st), and during the NEXT tile's stages every thread drains
+// its own columns back out (tcgen05.ld -> 16-byte stores), so the stores stream under the
+// FP64 stages.  A thread reads only what it wrote (its lane, its columns): no cross-thread
+// TMEM hazard, only tcgen05.wait::st/ld ordering within the thread.
+// TMEM layout: warp w owns lane quarter w & 3; thread (w, l) -> lane 32 (w & 3) + l, butterfly
+// k of the thread (q = tid + k * 512) -> columns [64 ((w >> 2) kmax + k), + 64): complex r at
+// words 4r..4r+3 (re lo, re hi, im lo, im hi).
+constexpr uint32_t kK1pWarpsPerQuarter = PA_TMAX / 32 / 4;  // 4 at 512 threads
+
+__device__ __forceinline__ uint32_t k1p_col(uint32_t k, uint32_t kmax)
+{
+    return (((threadIdx.x >> 5) >> 2) * kmax + k) * 64u;
+}
+
+// last DIF stage (radix 16, Ls = 1: no twiddles) of the tile in shared memory -> TMEM
+__device__ __forceinline__ void k1p_last_stage(const double2 *sm, const StageDesc &sd, uint32_t logC, uint32_t tm,
+                                               uint32_t kmax)
+{
+    const uint32_t nb = sd.nb << logC, cm = (1u << logC) - 1;
+    const uint32_t lane_base = tm + ((32u * ((threadIdx.x >> 5) & 3)) << 16);
+    uint32_t k = 0;
+    for (uint32_t qb = threadIdx.x & ~31u; qb < nb; qb += blockDim.x, ++k) {  // warp-uniform trip count
+        const uint32_t q = qb + (threadIdx.x & 31);
+        double2 v[16];
+        if (q < nb) {
+            const uint32_t c = q & cm, g = q >> logC;
+            const uint32_t base = ((g * 16u) << logC) + c;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = sm[pidx(base + (r << logC))];
+            Dft<16, false>::run(v);
+        } else {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t w[32];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double2 d = v[8 * h + i];
+                w[4 * i] = __double2loint(d.x);
+                w[4 * i + 1] = __double2hiint(d.x);
+                w[4 * i + 2] = __double2loint(d.y);
+                w[4 * i + 3] = __double2hiint(d.y);
+            }
+            tm_st32(lane_base + k1p_col(k, kmax) + 32u * h, w);
+        }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// drain chunks [ch0, ch1) of the previous tile (chunk = 8 outputs of one butterfly: k = ch / 2,
+// half = ch & 1) from TMEM to its rows: output r of butterfly (c, g) is work-array row 16 g + r
+__device__ __forceinline__ void k1p_drain(double2 *__restrict__ dst, uint32_t N1, uint32_t nb, uint32_t logC,
+                                          uint32_t tm, uint32_t kmax, uint32_t ch0, uint32_t ch1)
+{
+    const uint32_t cm = (1u << logC) - 1;
+    const uint32_t lane_base = tm + ((32u * ((threadIdx.x >> 5) & 3)) << 16);
+    for (uint32_t ch = ch0; ch < ch1; ++ch) {
+        const uint32_t k = ch >> 1, h = ch & 1;
+        const uint32_t qb = (threadIdx.x & ~31u) + k * blockDim.x;
+        if (k >= kmax || qb >= nb) break;  // warp-uniform
+        uint32_t w[32];
+        tm_ld32(lane_base + k1p_col(k, kmax) + 32u * h, w);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const uint32_t q = qb + (threadIdx.x & 31);
+        if (q < nb) {
+            const uint32_t c = q & cm, g = q >> logC;
+            double2 *p = dst + (uint64_t)(16u * g + 8u * h) * N1 + c;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                p[(uint64_t)i * N1] = make_double2(__hiloint2double(w[4 * i + 1], w[4 * i]),
+                                                   __hiloint2double(w[4 * i + 3], w[4 * i + 2]));
+        }
+    }
+}
+
+template <int RA, int RB, int RC>
+__global__ void __launch_bounds__(PA_TMAX, 1)
+k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
+                uint32_t *__restrict__ zero_out, uint64_t zero_words, uint64_t out_stride, uint32_t count)
+{
+    extern __shared__ double2 sm[];
+    __shared__ uint32_t tm_base;
+    const uint32_t logC = g.logC, C = 1u << logC;
+    double2 *wlo = sm + g.tile1, *whi = wlo + 64, *thlo = whi + g.f2.nhi + g.f2.ntw, *thhi = thlo + 64;
+    uint32_t *rowbits0 = reinterpret_cast<uint32_t *>(thhi + g.f2.nhi);
+    double2 *tb = reinterpret_cast<double2 *>(rowbits0 + g.kbw);
+    uint32_t *rowbits1 = reinterpret_cast<uint32_t *>(tb + g.ntb);
+    constexpr bool kBits = RA >= 2 && RA <= 4;
+    const uint32_t ngroups = g.N1 / C, ntiles = ngroups * count;
+    const int S = g.f2.S;
+    const StageDesc &last = g.f2.st[S - 1];
+    const uint32_t nb_last = last.nb << logC, kmax = g.k1p_kmax;
+    const uint32_t nchunks = 2 * kmax;  // per thread and tile (some may be empty)
+    load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
+    load_tables_async(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
+    if (kBits)
+        for (uint32_t i = threadIdx.x; i < g.ntb; i += blockDim.x) cp_async16(tb + i, T.tb + i);
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tm_base)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    grid_dep_wait();  // K0's bit streams
+    if (zero_out) {   // K3 XORs this hash's output bits in
+        for (uint32_t key = 0; key < count; ++key)
+            for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < zero_words;
+                 i += (uint64_t)gridDim.x * blockDim.x)
+                zero_out[key * out_stride + i] = 0u;
+    }
+    auto fetch_bits = [&](uint32_t t, uint32_t *dst) {
+        const uint32_t *src = kb + (uint64_t)t * g.kbw;  // tile t = key * ngroups + group
+        for (uint32_t i = 4 * threadIdx.x; i < g.kbw; i += 4 * blockDim.x) cp_async16(dst + i, src + i);
+    };
+    if (blockIdx.x < ntiles) fetch_bits(blockIdx.x, rowbits0);
+    cta_sync_tmem();
+    const uint32_t tm = tm_base;
+    double2 *prev = nullptr;  // previous tile's column group (key's work array + a0), drained below
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const uint32_t key = t / ngroups, a0 = (t % ngroups) * C;
+        uint32_t *rowbits = (it & 1) ? rowbits1 : rowbits0;
+        cp_async_wait_all();
+        __syncthreads();  // this tile's bits (and the tables) landed; the last tile's smem reads done
+        if (t + gridDim.x < ntiles) fetch_bits(t + gridDim.x, (it & 1) ? rowbits0 : rowbits1);
+        // spread the previous tile's drain over this tile's S stage passes
+        uint32_t ch = 0;
+        auto drain_step = [&](int i) {
+            if (!prev) return;
+            const uint32_t upto = (nchunks * (uint32_t)(i + 1) + S - 1) / S;
+            k1p_drain(prev, g.N1, nb_last, logC, tm, kmax, ch, upto);
+            ch = upto;
+        };
+        int s0 = 0;
+        drain_step(0);
+        if (kBits && g.ntb) {
+            k1_first_stage_bits<kBits ? RA : 2>(sm, g.f2.st[0], logC, rowbits, tb, thlo, thhi, wlo, whi);
+            s0 = 1;
+        } else {
+            const uint32_t twoC = 2 * C, epw = 32 / twoC, tot = g.N2 << logC;
+            for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
+                const uint32_t b = e >> logC, c = e & (C - 1);
+                const uint32_t rb = rowbits[b / epw] >> ((b % epw) * twoC);
+                const double xr = (double)((rb >> c) & 1u), xi = (double)((rb >> (C + c)) & 1u);
+                const double2 th = twiddle(thlo, thhi, b);
+                sm[pidx(e)] = make_double2(xr * th.x - xi * th.y, xr * th.y + xi * th.x);
+            }
+        }
+        __syncthreads();
+        for (int i = s0; i < S - 1; ++i) {
+            if (i > 0) drain_step(i);
+            stage_t<false, MODE_PLAIN, RA, RB, RC>(sm, g.f2, i, logC, wlo, whi);
+            __syncthreads();
+        }
+        drain_step(S - 1);  // everything of the previous tile is out of TMEM now
+        k1p_last_stage(sm, last, logC, tm, kmax);
+        prev = buf + (uint64_t)key * g.M + a0;
+    }
+    grid_dep_launch();  // K2 may start its prologue
+    if (prev) k1p_drain(prev, g.N1, nb_last, logC, tm, kmax, 0, nchunks);
+    cta_sync_tmem();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
 // ------------------------------------------------------------------ K2
 // Fused last DIF stage (Ls = 1, no twiddles) * spectrum * first DIT stage.  The
 // spectrum row is stored [r][g] (element g*R + r at sp[r * nb + g]) so that the
@@ -891,34 +1092,6 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
 // [8 i, 8 i + 8) = the row's two complex values (4 words each).
 constexpr uint32_t kK3tCompute = 384;  // compute threads (12 warps); 4 loader warps follow
 
-__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&r)[32])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
-__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&r)[32])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void cta_sync_tmem()  // barrier ordering tcgen05 traffic across warps
-{
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
 // loader warps: tile t of the batch into TMEM (8 rows = 16 x 16 B loads in flight per batch)
 __device__ __forceinline__ void k3t_load_tile(const double2 *__restrict__ buf, const Geometry &g, uint32_t t,
                                               uint32_t ngroups, uint32_t tm)
@@ -1039,20 +1212,19 @@ using K1Fn = void (*)(const uint32_t *, double2 *, Geometry, RouteTables, uint32
                       const uint32_t *, uint64_t, uint64_t);
 using K3Fn = void (*)(const double2 *, Geometry, RouteTables, uint64_t, uint64_t, uint32_t *, unsigned long long *,
                       uint64_t);
+using K1pFn = void (*)(const uint32_t *, double2 *, Geometry, RouteTables, uint32_t *, uint64_t, uint64_t, uint32_t);
 struct K13 {
     int a, b, c;
     K1Fn k1;
     K3Fn k3;
+    K1pFn k1p;
 };
+#define PA_K13(A, B, C) {A, B, C, k1_fwd_columns<A, B, C>, k3_inv_columns<A, B, C>, k1p_fwd_columns<A, B, C>}
 static const K13 kK13[] = {
-    {0, 0, 0, k1_fwd_columns<0, 0, 0>, k3_inv_columns<0, 0, 0>},
-    {2, 5, 0, k1_fwd_columns<2, 5, 0>, k3_inv_columns<2, 5, 0>},
-    {3, 4, 7, k1_fwd_columns<3, 4, 7>, k3_inv_columns<3, 4, 7>},
-    {3, 8, 0, k1_fwd_columns<3, 8, 0>, k3_inv_columns<3, 8, 0>},
-    {3, 3, 0, k1_fwd_columns<3, 3, 0>, k3_inv_columns<3, 3, 0>},
-    {7, 4, 0, k1_fwd_columns<7, 4, 0>, k3_inv_columns<7, 4, 0>},
-    {3, 7, 8, k1_fwd_columns<3, 7, 8>, k3_inv_columns<3, 7, 8>},
+    PA_K13(0, 0, 0), PA_K13(2, 5, 0), PA_K13(3, 4, 7), PA_K13(3, 8, 0), PA_K13(3, 3, 0), PA_K13(7, 4, 0),
+    PA_K13(3, 7, 8),
 };
+#undef PA_K13
 
 static int k13_shape(const FftPlan &p)
 {
@@ -1082,7 +1254,7 @@ std::vector<uint32_t> smooth_numbers(uint32_t limit)
 
 static bool asc_off()  // developer override PA_K13_ASC=0: K1/K3 plans in the default radix order
 {
-    const char *e = getenv("PA_K13_ASC");
+    const char *e = dev_env("PA_K13_ASC");
     return e && atoi(e) == 0;
 }
 
@@ -1222,7 +1394,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         }
     }
     // developer override for plan experiments: PA_FORCE_PLAN="N1,N2,C"
-    if (const char *fp = getenv("PA_FORCE_PLAN")) {
+    if (const char *fp = dev_env("PA_FORCE_PLAN")) {
         unsigned f1 = 0, f2 = 0, fc = 0;
         FftPlan q1, q2;
         if (sscanf(fp, "%u,%u,%u", &f1, &f2, &fc) == 3 && (uint64_t)f1 * f2 >= Mmin && fc >= 1 &&
@@ -1246,7 +1418,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     uint32_t logC = 0;
     while ((1u << logC) < g->C) ++logC;
     g->logC = logC;
-    const char *r1 = getenv("PA_FORCE_RMAX1");  // developer override: row-plan radix cap
+    const char *r1 = dev_env("PA_FORCE_RMAX1");  // developer override: row-plan radix cap
     make_plan(g->N1, &g->f1, r1 ? (uint32_t)atoi(r1) : 16);
     // K1/K3: the radices in ascending order when that puts a radix-2 or -3 stage first (K1 then
     // reads the key bits through an 8- or 24-entry table, k_bits_table).  Same-box: C2 [2, 5, 16]
@@ -1269,7 +1441,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // K2: L2 prefetch of the row pf2 rows ahead when one CTA per SM runs > 2 waves (C4, C5d); it
     // measured slower at two CTAs per SM
     {
-        const char *e = getenv("PA_PF");
+        const char *e = dev_env("PA_PF");
         // distance in rows: 56 (a third of a wave; same-box sweep C4 / C5d: 8 -> 1040 us at C5d,
         // 37-74 -> 2405-2410 / 1010-1012 us, 148 -> 2424 / 1019, 296 -> 2494 / 1070, off -> 2529 /
         // 1067).  Developer override PA_PF=0 (off) or PA_PF=d
@@ -1278,9 +1450,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     }
     // K1/K2/K3 specialised for the common plan shapes (developer override PA_K2_T=0 / PA_K13_T=0)
     {
-        const char *e = getenv("PA_K2_T");
+        const char *e = dev_env("PA_K2_T");
         g->k2shape = (!e || atoi(e) != 0) ? k2_shape(g->f1) : 0;
-        const char *e13 = getenv("PA_K13_T");
+        const char *e13 = dev_env("PA_K13_T");
         g->k13 = (!e13 || atoi(e13) != 0) ? k13_shape(g->f2) : 0;
     }
     // K1's first stage straight from the key bits through a 2^R0 x R0 table (radix R0 <= 4 of a
@@ -1290,7 +1462,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     {
         // K0 tile (developer overrides PA_K0_RB / PA_K0_CB).  Larger tiles (fewer CTAs) measured
         // slower: C3 64 x 256 / 64 x 512 / 64 x 1024 -> K0 9.7-13.8 / 20.2 us vs 10.3 us at 16 x 256
-        const char *er = getenv("PA_K0_RB"), *ec = getenv("PA_K0_CB");
+        const char *er = dev_env("PA_K0_RB"), *ec = dev_env("PA_K0_CB");
         g->k0rb = er ? (uint32_t)atoi(er) : g->N2 >= 2048 ? 64u : 16u;
         g->k0cb = ec ? (uint32_t)atoi(ec) : g->N1 >= 8192 ? 1024u : 256u;
         if (g->k0rb % 16 || g->k0rb > kK0Rows || g->k0rb == 0) g->k0rb = 16;
@@ -1298,7 +1470,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     }
     g->ntb = 0;
     {
-        const char *e = getenv("PA_K1_BITS");
+        const char *e = dev_env("PA_K1_BITS");
         const uint32_t R0 = g->f2.S ? g->f2.st[0].R : 16u;
         if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 2 && R0 <= 4) {
             const uint32_t ntb = (1u << R0) * R0, s1 = g->smem1 + ntb * 16;
@@ -1312,7 +1484,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // 4-column groups.  Bit-exact, but K2's stores become 32-byte pieces: C4 K3 725 -> 627, K2
     // 1119 -> 1208 us (net 0), C5d -1.8%, so row-major stays the default
     {
-        const char *e = getenv("PA_LR");
+        const char *e = dev_env("PA_LR");
         const uint32_t lr = g->C == 2 ? 2u : g->C == 4 ? 1u : 0u;
         g->lr = e && atoi(e) == 1 && g->N2 % (1u << lr) == 0 ? lr : 0u;
     }
@@ -1320,12 +1492,18 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // 723 -> 1019 us): its loader warps keep ~2 k row pieces in flight against K3's 12 k
     // cp.async (registers bound them; shared memory has no room for staging), see DESIGN.md
     {
-        const char *e = getenv("PA_K3T");
+        const char *e = dev_env("PA_K3T");
         g->k3t = e && atoi(e) == 1 && g->C == 2 && g->t1 == PA_TMAX && g->N2 <= 8192 &&
                  g->N1 / g->C > 2 * 148u && g->smem1 + 1024 <= kSmemLimit;
     }
-    if (const char *e = getenv("PA_FORCE_T1")) g->t1 = (uint32_t)atoi(e);  // developer overrides
-    if (const char *e = getenv("PA_FORCE_T2")) g->t2 = (uint32_t)atoi(e);
+    // developer overrides of the thread counts: accepted only as multiples of 32 (k3_epilogue's
+    // ballot runs need whole warps, and warps a multiple of C) within [64, PA_TMAX]
+    auto threads_ok = [](const char *e) {
+        const int v = e ? atoi(e) : 0;
+        return v >= 64 && v <= PA_TMAX && v % 32 == 0;
+    };
+    if (const char *e = dev_env("PA_FORCE_T1"); threads_ok(e)) g->t1 = (uint32_t)atoi(e);
+    if (const char *e = dev_env("PA_FORCE_T2"); threads_ok(e)) g->t2 = (uint32_t)atoi(e);
     // K3's column groups: half of K1's when K1's tile allows one CTA per SM and the half tile
     // two -- a second CTA's loads overlap the first one's stages, worth more than the longer
     // 16-byte row pieces (C4: K3 721 -> 630 us; K1 itself measured slower at C = 1, 778 -> 919
@@ -1334,19 +1512,33 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     {
         // K1's last stage stores straight to global from C = 2 up (32-byte row pieces; same-box
         // C4 2481 -> 2459 us, C5c 336.9 -> 333.8, C5d 1030 -> 1026); developer override
-        const char *e = getenv("PA_K1_GOUT_MINC");
+        const char *e = dev_env("PA_K1_GOUT_MINC");
         g->k1gout = e ? (uint32_t)atoi(e) : 2u;
     }
     // K2: L2 prefetch of the CTA's own spectrum row at its start, under the forward stages, when
     // one CTA runs per SM (C4 2453 -> 2421 us, C5d -0.7%; at two CTAs per SM it measured slower,
     // C3 187 -> 193 us).  Developer override PA_PFS=0/1
     {
-        const char *e = getenv("PA_PFS");
+        const char *e = dev_env("PA_PFS");
         g->pfs = e ? (uint32_t)atoi(e) : g->t2 == PA_TMAX ? 1u : 0u;
+    }
+    // K1P (persistent K1, finished tiles written behind through TMEM, k1p_fwd_columns): one CTA of
+    // 512 threads per SM, a multi-wave grid, a shape-specialised plan ending in radix 16 whose
+    // last-stage outputs fit the 512 TMEM columns (<= 2 butterflies per thread), and K0's bit
+    // streams (not the C = 16 direct gather).  Developer override PA_K1P=0.
+    g->k1p_kmax = 0;
+    g->smem1p = g->smem1 + g->kbw * 4;
+    {
+        const char *e = dev_env("PA_K1P");
+        const uint32_t nbl = g->f2.S ? (g->f2.st[g->f2.S - 1].nb << g->logC) : 0;
+        const uint32_t kmax = (nbl + PA_TMAX - 1) / PA_TMAX;
+        if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 3 && g->f2.st[g->f2.S - 1].R == 16 && g->t1 == PA_TMAX &&
+            g->C < 16 && kmax >= 1 && kmax <= 2 && g->smem1p + 64 <= kSmemLimit && g->N1 / g->C >= 2 * 148u)
+            g->k1p_kmax = kmax;
     }
     g->C3 = g->C;
     {
-        const char *e = getenv("PA_K3_HALF");
+        const char *e = dev_env("PA_K3_HALF");
         if ((!e || atoi(e) != 0) && g->lr == 0 && !g->k3t && g->C >= 2 && 2 * g->smem1 > kSmemLimit &&
             2 * smem_k13(g->N2, g->C / 2, g->f2) <= kSmemLimit)
             g->C3 = g->C / 2;
@@ -1399,6 +1591,7 @@ static void carve_work(RouteA &a, char *blk, uint32_t cap)
     a.kb = reinterpret_cast<uint32_t *>(blk + b);
     a.buf2 = a.g.lr ? reinterpret_cast<double2 *>(blk + b + al256((size_t)cap * kb_bytes(a.g))) : a.buf;
     a.cap = cap;
+    ++a.wgen;
 }
 
 // K1 reads the key itself (no K0) when its column groups are at least `min C` wide:
@@ -1406,7 +1599,7 @@ static void carve_work(RouteA &a, char *blk, uint32_t cap)
 static bool k1_direct(const Geometry &g)
 {
     static const uint32_t cmin = [] {
-        const char *e = getenv("PA_K1_DIRECT_MINC");  // developer override (0 = never)
+        const char *e = dev_env("PA_K1_DIRECT_MINC");  // developer override (0 = never)
         return e ? (uint32_t)atoi(e) : 16u;  // C = 8 measured slower (C3 K1 66 -> 80 us)
     }();
     return cmin && g.C >= cmin;
@@ -1485,6 +1678,8 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     for (const K13 &f : kK13)
         if ((e = cudaFuncSetAttribute(f.k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
                 cudaSuccess ||
+            (e = cudaFuncSetAttribute(f.k1p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit - 64)) !=
+                cudaSuccess ||
             (e = cudaFuncSetAttribute(f.k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
                 cudaSuccess)
             return cuda_fail(e, "route (a) cudaFuncSetAttribute");
@@ -1531,7 +1726,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // Work buffers for `count` keys in flight (grown on demand, kept for the next call).
 // A caller workspace is never grown: pa_hash_batch chunks by its capacity.
-static pa_status ra_reserve(pa_ctx *h, uint32_t count)
+static pa_status ra_reserve(pa_ctx *h, uint32_t count, cudaStream_t s)
 {
     RouteA &a = h->a;
     if (count <= a.cap) return PA_OK;
@@ -1549,10 +1744,9 @@ static pa_status ra_reserve(pa_ctx *h, uint32_t count)
                   (unsigned long long)bytes, cudaGetErrorString(e));
         return PA_ERR_NOMEM;
     }
-    // the old buffers may still be in use by enqueued work
-    cudaDeviceSynchronize();
+    // the old buffers may still be in use by work enqueued on s: freed once s passes this point
     h->ws_bytes += bytes - ra_work_bytes(a.g, a.cap);
-    cudaFree(a.wblk);
+    defer_free(h, a.wblk, s);
     carve_work(a, nb, count);
     return PA_OK;
 }
@@ -1573,7 +1767,7 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
                         uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s,
                         const double2 *spec, uint64_t spec_stride)
 {
-    pa_status st = ra_reserve(h, count);
+    pa_status st = ra_reserve(h, count, s);
     if (st != PA_OK) return st;
     RouteA &a = h->a;
     const Geometry &g = a.g;
@@ -1585,8 +1779,14 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         prof_end(h, s);
     }
     prof_begin(h, 0, s);
-    launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
-               out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
+    if (g.k1p_kmax && !direct) {
+        const uint32_t tiles = (g.N1 / g.C) * count;
+        launch_pdl(kK13[g.k13].k1p, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1p, s,
+                   (const uint32_t *)a.kb, a.buf, g, a.T, outs, zero_words, out_stride, count);
+    } else {
+        launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
+                   out_stride, direct ? keys : (const uint32_t *)nullptr, key_stride, h->n);
+    }
     prof_end(h, s);
     prof_begin(h, 1, s);
     {
@@ -1637,11 +1837,10 @@ pa_status ra_fresh_batch(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride,
     const size_t spec_bytes = (size_t)g.M * sizeof(double2);
     if (h->arena || h->parent || chunk < 2 || (size_t)chunk * spec_bytes > (size_t(4) << 30))
         return PA_ERR_UNSUPPORTED;
-    pa_status st = ra_reserve(h, chunk);
+    pa_status st = ra_reserve(h, chunk, s);
     if (st != PA_OK) return st;
     if (a.fcap < chunk) {
-        cudaStreamSynchronize(s);  // the old spectra may still be read by enqueued hashes
-        dev_free(h, a.fspec);
+        defer_free(h, a.fspec, s);  // the old spectra may still be read by enqueued hashes
         h->ws_bytes -= (size_t)a.fcap * spec_bytes;
         a.fspec = nullptr;
         a.fcap = 0;

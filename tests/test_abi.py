@@ -78,6 +78,7 @@ def test_struct_layouts_match_header(tmp_path, struct):
     if struct == "pa_options":
         o = L.pa_options_init()
         assert o.struct_size == size and o.route == 0 and o.batch_keys == 0 and o.max_transform_len == 0
+        assert o.arith == 0 and o.device == -1
 
 
 def test_invalid_lengths_rejected_before_device_work():
@@ -169,10 +170,26 @@ def test_option_and_pointer_errors_before_device_work():
         pa.workspace_size(100, 10, batch_keys=5000)
     assert e.value.status == pa.PA_ERR_INVALID_ARG and "batch_keys" in pa.pa_last_error()
     o = pa.make_options()
-    o.reserved[1] = 7
+    o.reserved[0] = 7
     with pytest.raises(pa.PaError) as e:
         pa.pa_workspace_size(100, 10, o)
-    assert e.value.status == pa.PA_ERR_INVALID_ARG and "reserved[1]" in pa.pa_last_error()
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "reserved[0]" in pa.pa_last_error()
+    # SURVEY 8(b) pa_options.arith: FP64 is the built arithmetic, the NTTs are refused by name
+    for a, ok in ((pa.PA_ARITH_AUTO, True), (pa.PA_ARITH_FP64, True), (pa.PA_ARITH_NTT32, False),
+                  (pa.PA_ARITH_NTT64, False), (9, False)):
+        o = pa.make_options(route="transform")
+        o.arith = a
+        if ok:
+            assert pa.pa_workspace_size(100_000, 10_000, o) > 0
+        else:
+            with pytest.raises(pa.PaError) as e:
+                pa.pa_workspace_size(100_000, 10_000, o)
+            assert "arith" in pa.pa_last_error()
+    o = pa.make_options()
+    o.device = -2
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_workspace_size(100, 10, o)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "device" in pa.pa_last_error()
     with pytest.raises(pa.PaError) as e:
         pa.pa_create_ws(100, 10, 0, None, 0, 1 << 20, 0)
     assert e.value.status == pa.PA_ERR_INVALID_ARG and "workspace" in pa.pa_last_error()
@@ -196,3 +213,24 @@ def test_plan_splits_keys_beyond_one_transform():
     assert p["column_blocks"] > 1 and p["transform_len"] < 10**9 + 10**8
     p = pa.pa_plan(10**10, 10**7)
     assert p["column_blocks"] >= 28 and p["workspace_bytes"] < 180 * 2**30
+
+
+def test_product_library_ignores_developer_overrides():
+    """PA_* plan / variant overrides exist only in the PA_DEV build (libpa_dev.so): the product
+    libpa.so plans the same with and without them; the developer build follows them."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\nimport paper_1805_02372_b200 as pa\n"
+            "p = pa.pa_plan(10**7, 10**6); print(p['n1'], p['n2'], p['cols_per_cta'])\n" % ROOT)
+    force = {"PA_FORCE_PLAN": "4096,3600,2", "PA_K13_ASC": "0", "PA_FORCE_T1": "100"}
+    base = {k: v for k, v in os.environ.items() if k != "PA_LIB"}
+
+    def plan(env):
+        r = subprocess.run([sys.executable, "-c", code], env={**base, **env}, capture_output=True, text=True,
+                           timeout=300, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return r.stdout.strip()
+    assert plan({}) == plan(force) != "4096 3600 2"
+    dev = os.path.join(ROOT, "paper_1805_02372_b200", "libpa_dev.so")
+    if os.path.exists(dev):
+        assert plan({**force, "PA_LIB": dev}) == "4096 3600 2"

@@ -691,25 +691,6 @@ def test_auto_split_gigabit_key():
     assert bad.size == 0, f"{bad.size} wrong bits, first {bad[:8]}"
 
 
-@pytest.mark.parametrize("name", ["C4", "C5d"])
-def test_tmem_staged_k3_opt_in(name, monkeypatch):
-    """The opt-in TMEM-staged K3 (PA_K3T=1: persistent CTAs, loader warps ld.global ->
-    tcgen05.st, compute warps tcgen05.ld -> shared memory) is bit-exact at the sizes it serves:
-    sampled rows vs the oracle plus the full unit-key closed form."""
-    monkeypatch.setenv("PA_K3T", "1")
-    n, m, sw, kw = syn.config_inputs(name)
-    with pa.Hasher(n, m, to_dev(sw)) as h:
-        got = from_dev(h.hash(to_dev(kw)), m)
-        j = n // 3
-        unit = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
-        torch.cuda.synchronize()
-        assert h.residual() < 1e-3
-    rows = sample_rows(m, 5)
-    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
-    s01 = oracle.unpack(sw, n + m - 1)
-    assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m])
-
-
 def test_key_and_output_must_not_overlap():
     n, m = 1_000_003, 250_000
     with pa.Hasher(n, m, to_dev(syn.random_bits(syn.seed_stream(99), n + m - 1))) as h:
@@ -744,57 +725,6 @@ def test_random_shapes_fuzz(n, m):
     if n * m <= 2e9:
         got_b, _ = check(n, m, sw, kw, "bitpacked", full=False)
         assert np.array_equal(got, got_b)
-
-
-@pytest.mark.parametrize("n,m", [(100_000_000, 20_000_000), (16_777_233, 1_677_723), (300_007, 60_001)])
-def test_row_block_layout_opt_in(n, m, monkeypatch):
-    """Opt-in blocked work-array layout (PA_LR=1: R x C blocks of a column group contiguous)
-    through K1/K2/K3 (and the seed path): bit-exact vs the oracle on sampled rows and the
-    full unit-key closed form, with and without the TMEM-staged K3."""
-    monkeypatch.setenv("PA_LR", "1")
-    sw = syn.random_bits(syn.seed_stream(101), n + m - 1)
-    kw = syn.random_bits(syn.key_stream(101, 0), n)
-    s01 = oracle.unpack(sw, n + m - 1)
-    rows = sample_rows(m, 9)
-    for k3t in ("0", "1"):
-        monkeypatch.setenv("PA_K3T", k3t)
-        with pa.Hasher(n, m, to_dev(sw), route="transform") as h:
-            got = from_dev(h.hash(to_dev(kw)), m)
-            j = (2 * n) // 3
-            unit = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
-            torch.cuda.synchronize()
-            assert h.residual() < 1e-3
-        assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows)), k3t
-        assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m]), k3t
-
-
-@pytest.mark.parametrize("n,m,plan", [(10_000_000, 1_000_000, "4096,1792,4"), (3_000_000, 300_000, "1024,3600,2"),
-                                       (2_000_003, 400_000, "1536,4096,2")])
-def test_k3_half_column_groups(n, m, plan, monkeypatch):
-    """K3 on half of K1's column groups (Geometry::C3, taken when K1's tile allows one CTA per SM
-    and the half tile two): forced plans that trigger it at moderate sizes, bit-exact against
-    the oracle (sampled rows), the full unit-key closed form, and PA_K3_HALF=0 (K3 on K1's
-    groups) giving the same output."""
-    monkeypatch.setenv("PA_FORCE_PLAN", plan)
-    sw = syn.random_bits(syn.seed_stream(121), n + m - 1)
-    kw = syn.random_bits(syn.key_stream(121, 0), n)
-    s01 = oracle.unpack(sw, n + m - 1)
-    outs = []
-    for half in ("1", "0"):
-        monkeypatch.setenv("PA_K3_HALF", half)
-        with pa.Hasher(n, m, to_dev(sw), route="transform") as h:
-            assert "%d,%d,%d" % (h.info["n1"], h.info["n2"], h.info["cols_per_cta"]) == plan
-            assert h.info["k3_cols_per_cta"] == h.info["cols_per_cta"] // (2 if half == "1" else 1)
-            got = from_dev(h.hash(to_dev(kw)), m)
-            j = n // 2 + 1
-            unit = from_dev(h.hash(to_dev(syn.unit_bits(n, j))), m)
-            torch.cuda.synchronize()
-            assert h.residual() < 1e-3
-        assert np.array_equal(unit, s01[n - 1 - j:n - 1 - j + m]), half
-        outs.append(got)
-    assert np.array_equal(outs[0], outs[1])
-    rows = sample_rows(m, 12)
-    assert np.array_equal(outs[0][rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
 
 
 def test_no_device_memory_leak_across_handles():
@@ -965,3 +895,75 @@ def test_hash_host_batch(n, m, count, kwargs):
         assert np.array_equal(oracle.unpack(got[k], m), want), k
         assert not oracle.unpack(got[k][: pa.words32(m)], 32 * pa.words32(m))[m:].any()
     assert (oh[:, pa.words32(m):] == -1).all()
+
+
+def test_host_graph_recaptured_after_work_buffers_move():
+    """pa_hash_host caches a CUDA graph holding the work-buffer pointers.  A fresh-seed batch
+    (count >= 2) regrows those buffers (stream-ordered, the old block freed once the stream
+    passes it); the next pa_hash_host on the same host buffers must re-capture, not replay stale
+    pointers.  Every output is checked against the oracle."""
+    n, m = 1_000_003, 250_000
+    sw = syn.random_bits(syn.seed_stream(131), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(131, 0), n)
+    key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
+    out_h = torch.zeros(pa.words32(m), dtype=torch.int32).pin_memory()
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    count = 4
+    seeds = syn.random_bits_torch([syn.seed_stream(140 + k) for k in range(count)], n + m - 1, DEV)
+    keys = syn.random_bits_torch([syn.key_stream(141, k) for k in range(count)], n, DEV)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        h.hash_host(key_h, out_h)
+        assert np.array_equal(oracle.unpack(out_h.numpy().view(np.uint32), m), want)
+        outs = h.hash_fresh_batch(seeds, keys)
+        h.set_seed(to_dev(sw))
+        out_h.zero_()
+        h.hash_host(key_h, out_h)
+        assert np.array_equal(oracle.unpack(out_h.numpy().view(np.uint32), m), want)
+        for k in (0, count - 1):
+            s_k = syn.random_bits(syn.seed_stream(140 + k), n + m - 1)
+            k_k = syn.random_bits(syn.key_stream(141, k), n)
+            rows = sample_rows(m, k, 256)
+            assert np.array_equal(from_dev(outs[k], m)[rows], oracle.toeplitz_rows(n, m, s_k, k_k, rows))
+        # a larger plain batch moves them again
+        big = h.hash_batch(syn.random_bits_torch([syn.key_stream(142, k) for k in range(8)], n, DEV))
+        out_h.zero_()
+        h.hash_host_async(key_h, out_h)
+        torch.cuda.synchronize()
+        assert np.array_equal(oracle.unpack(out_h.numpy().view(np.uint32), m), want)
+        k7 = syn.random_bits(syn.key_stream(142, 7), n)
+        rows = sample_rows(m, 7, 256)
+        assert np.array_equal(from_dev(big[7], m)[rows], oracle.toeplitz_rows(n, m, sw, k7, rows))
+
+
+def test_fresh_batch_rejects_overlapping_outputs():
+    n, m = 100_003, 20_000
+    with pa.Hasher(n, m, to_dev(syn.random_bits(syn.seed_stream(150), n + m - 1))) as h:
+        W = (pa.words32(n + m) + 3) // 4 * 4
+        buf = torch.zeros((4, W), dtype=torch.int32, device=DEV)
+        for outs_p in (buf[0, 8:].data_ptr(), buf[2, 8:].data_ptr()):  # inside the seed / the key
+            with pytest.raises(pa.PaError) as e:
+                pa.pa_hash_fresh_batch(h.handle, buf[0].data_ptr(), W, buf[2].data_ptr(), W, outs_p, W, 1, 0)
+            assert e.value.status == pa.PA_ERR_INVALID_ARG and "overlap" in pa.pa_last_error()
+
+
+def test_explicit_device_option():
+    """pa_options.device: an explicit ordinal binds the handle to that device and
+    later calls run there; an ordinal past the visible devices is rejected."""
+    n, m = 4096, 1024
+    sw = syn.random_bits(syn.seed_stream(151), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(151, 0), n)
+    seed_t, key_t = to_dev(sw), to_dev(kw)
+    o = pa.make_options(route="transform", device=0)
+    h = pa.pa_create_ex(n, m, seed_t.data_ptr(), o, 0)
+    try:
+        assert pa.pa_get_info(h)["device"] == 0
+        out = torch.zeros(pa.words32(m) + 3, dtype=torch.int32, device=DEV)
+        pa.pa_hash(h, key_t.data_ptr(), out.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(from_dev(out, m), oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m))
+    finally:
+        pa.pa_destroy(h)
+    o.device = torch.cuda.device_count()
+    with pytest.raises(pa.PaError) as e:
+        pa.pa_create_ex(n, m, seed_t.data_ptr(), o, 0)
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "device" in pa.pa_last_error()
