@@ -546,8 +546,6 @@ __device__ __forceinline__ void cta_sync_tmem()  // barrier ordering tcgen05 tra
 // TMEM layout: warp w owns lane quarter w & 3; thread (w, l) -> lane 32 (w & 3) + l, butterfly
 // k of the thread (q = tid + k * 512) -> columns [64 ((w >> 2) kmax + k), + 64): complex r at
 // words 4r..4r+3 (re lo, re hi, im lo, im hi).
-constexpr uint32_t kK1pWarpsPerQuarter = PA_TMAX / 32 / 4;  // 4 at 512 threads
-
 __device__ __forceinline__ uint32_t k1p_col(uint32_t k, uint32_t kmax)
 {
     return (((threadIdx.x >> 5) >> 2) * kmax + k) * 64u;
@@ -1530,10 +1528,14 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     g->smem1p = g->smem1 + g->kbw * 4;
     {
         const char *e = dev_env("PA_K1P");
+        const char *et = dev_env("PA_K1P_T");  // developer override of K1P's threads (multiple of 128)
+        const int tv = et ? atoi(et) : 0;
+        g->k1p_t = tv >= 256 && tv <= PA_TMAX && tv % 128 == 0 ? (uint32_t)tv : PA_TMAX;
         const uint32_t nbl = g->f2.S ? (g->f2.st[g->f2.S - 1].nb << g->logC) : 0;
-        const uint32_t kmax = (nbl + PA_TMAX - 1) / PA_TMAX;
+        const uint32_t kmax = (nbl + g->k1p_t - 1) / g->k1p_t;
         if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 3 && g->f2.st[g->f2.S - 1].R == 16 && g->t1 == PA_TMAX &&
-            g->C < 16 && kmax >= 1 && kmax <= 2 && g->smem1p + 64 <= kSmemLimit && g->N1 / g->C >= 2 * 148u)
+            g->C < 16 && kmax >= 1 && (g->k1p_t / 128) * kmax * 64 <= 512 && g->smem1p + 64 <= kSmemLimit &&
+            g->N1 / g->C >= 2 * 148u)
             g->k1p_kmax = kmax;
     }
     g->C3 = g->C;
@@ -1781,7 +1783,7 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
     prof_begin(h, 0, s);
     if (g.k1p_kmax && !direct) {
         const uint32_t tiles = (g.N1 / g.C) * count;
-        launch_pdl(kK13[g.k13].k1p, dim3(tiles < 148 ? tiles : 148), dim3(PA_TMAX), g.smem1p, s,
+        launch_pdl(kK13[g.k13].k1p, dim3(tiles < 148 ? tiles : 148), dim3(g.k1p_t), g.smem1p, s,
                    (const uint32_t *)a.kb, a.buf, g, a.T, outs, zero_words, out_stride, count);
     } else {
         launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,

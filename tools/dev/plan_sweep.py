@@ -1,0 +1,60 @@
+"""Same-box sweep of forced plans (PA_FORCE_PLAN="N1,N2,C") for one config -- developer build.
+
+    PA_LIB=$PWD/paper_1805_02372_b200/libpa_dev.so python tools/dev/plan_sweep.py C4 10240,6144,2 8192,7680,1 ...
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import pa_synth as syn  # noqa: E402
+import paper_1805_02372_b200 as pa  # noqa: E402
+
+
+def words(w):
+    w = np.ascontiguousarray(w).view(np.int32)
+    w = np.concatenate([w, np.zeros((-w.size) % 4, np.int32)])
+    return torch.from_numpy(w.copy()).cuda()
+
+
+name = sys.argv[1]
+n, m, sw, kw = syn.config_inputs(name)
+seed, key = words(sw), words(kw)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ref = None
+for plan in ["default"] + sys.argv[2:]:
+    if plan == "default":
+        os.environ.pop("PA_FORCE_PLAN", None)
+    else:
+        os.environ["PA_FORCE_PLAN"] = plan
+    h = pa.Hasher(n, m, seed, route="transform")
+    out = h.new_out()
+    for _ in range(3):
+        h.hash(key, out)
+    ts = []
+    for _ in range(15):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h.hash(key, out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    pa.pa_profile_enable(h.handle, True)
+    pa.pa_profile_read(h.handle)
+    for _ in range(5):
+        flush.zero_()
+        h.hash(key, out)
+    kern = pa.pa_profile_read(h.handle)
+    got = out.cpu().numpy()
+    if ref is None:
+        ref = got
+    ok = np.array_equal(got[: (m + 31) // 32], ref[: (m + 31) // 32])
+    ks = " ".join(f"{k.split('_')[0]}={v[1] / v[0] * 1e3:.1f}" for k, v in kern.items())
+    i = h.info
+    print(f"{plan:18s} -> {i['n1']}x{i['n2']} C={i['cols_per_cta']} C3={i['k3_cols_per_cta']}: "
+          f"{np.median(ts) * 1e3:8.1f} us [{ks}] same={ok}", flush=True)
+    h.close()
