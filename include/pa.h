@@ -257,15 +257,27 @@ pa_status pa_profile_enable(pa_handle h, int enable);
 pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32_t *count);
 
 /* Length-compatible hashing for keys whose single transform would be too long
- * (Sec. 3, Fig. 1, Eq. (4)-(7)): T is cut into row blocks and
- * key (column) blocks with n_b + m_b - 1 <= max_block_bits (0 = the largest block
- * one handle supports); every block is a Toeplitz hash on the seed window at
- * offset r0 + n - c1, and each row block's output is the XOR of its column
- * blocks (Eq. (7)).  seed_bits: n+m-1 bits, key_bits: n bits, out_bits:
- * ceil(m/32) words, all device.  Creates a temporary handle per block and
- * synchronises `stream` before returning. */
+ * (Sec. 3, Fig. 1, Eq. (4)-(7)): T is cut into row blocks of mb rows and
+ * key (column) blocks of nb bits, nb + mb - 1 <= max_block_bits (0 = the largest block one
+ * handle plans), nb and mb multiples of 32; block (r0, c0) is a Toeplitz hash on the seed window
+ * at bit r0 + n - c0 - nb (zero-padded before s[0]; the last key block's bits past n and the
+ * last row block's rows past m are padding), and each row block's output is the XOR of its
+ * column blocks (Eq. (7)).  One handle of the block shape serves every block (pa_set_seed per
+ * block).  seed_bits: n+m-1 bits, key_bits: n bits, out_bits: ceil(m/32) words, all device;
+ * out bits >= m are written 0.  Synchronises `stream` before returning. */
 pa_status pa_hash_blocked(uint64_t n, uint64_t m, const uint32_t *seed_bits, const uint32_t *key_bits,
                           uint32_t *out_bits, uint64_t max_block_bits, void *stream);
+
+/* pa_hash_blocked with the seed, key and output in HOST memory (pinned recommended): keys of
+ * 10^9-10^10 bits need not fit the device.  Each block's key and seed words move
+ * host->device on a copy stream into one of two staging slots while the previous block is
+ * hashed, and every finished row block's output moves device->host the same way.
+ * device_budget_bytes > 0 caps the device memory the call uses (block handle + staging): the
+ * block length is the largest within it (PA_ERR_NOMEM if even a 64-bit block does not fit);
+ * 0 = no cap (max_block_bits or the planner's limit).  Synchronises `stream` before returning. */
+pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t *seed_host, const uint32_t *key_host,
+                               uint32_t *out_host, uint64_t max_block_bits, uint64_t device_budget_bytes,
+                               void *stream);
 
 /* Modulo-2 addition of partial hashes (Eq. (7)): dst[w] = XOR over
  * g < count of src[g * src_stride_words + w], w < words.  Device pointers,

@@ -23,7 +23,7 @@ from ._lib import (PA_ARITH_AUTO, PA_ARITH_FP64, PA_ARITH_NTT32, PA_ARITH_NTT64,
                    PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISION,  # noqa: F401
                    PA_ERR_UNSUPPORTED, PA_OK, PA_RESIDUAL_LIMIT, PA_ROUTE_AUTO, PA_ROUTE_BITPACKED,
                    PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
-                   pa_get_info, pa_hash, pa_hash_batch, pa_hash_blocked, pa_hash_host, pa_hash_host_async, pa_hash_u64, pa_last_error,
+                   pa_get_info, pa_hash, pa_hash_batch, pa_hash_blocked, pa_hash_blocked_host, pa_hash_host, pa_hash_host_async, pa_hash_u64, pa_last_error,
                    pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_set_seed, pa_xor_fold, pa_residual, pa_status_string,
                    pa_version, pa_workspace_size, pa_create_ws, pa_hash_fresh_batch, pa_seed_from_paper_eq1,
                    pa_hash_host_batch)

@@ -33,7 +33,7 @@ PA_RESIDUAL_LIMIT = 0.25
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
             "pa_hash_host", "pa_create_u64", "pa_hash_u64", "pa_residual", "pa_get_info",
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
-            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked",
+            "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked", "pa_hash_blocked_host",
             "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1",
             "pa_hash_host_batch"]
 
@@ -83,6 +83,7 @@ _sig = {
     "pa_hash_host_async": (_st, [_H, _p, _p, _p]),
     "pa_hash_host_batch": (_st, [_H, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
     "pa_hash_blocked": (_st, [_u64, _u64, _p, _p, _p, _u64, _p]),
+    "pa_hash_blocked_host": (_st, [_u64, _u64, _p, _p, _p, _u64, _u64, _p]),
     "pa_create_u64": (_st, [ctypes.POINTER(_H), _u64, _u64, _p, _p]),
     "pa_hash_u64": (_st, [_H, _p, _p, _p]),
     "pa_residual": (_st, [_H, ctypes.POINTER(ctypes.c_double), _p]),
@@ -218,6 +219,12 @@ def pa_xor_fold(dst_ptr: int, src_ptr: int, words: int, count: int, src_stride_w
 def pa_hash_blocked(n: int, m: int, seed_ptr: int, key_ptr: int, out_ptr: int, max_block_bits: int = 0,
                     stream: int = 0) -> None:
     _check(_lib.pa_hash_blocked(n, m, seed_ptr, key_ptr, out_ptr, max_block_bits, stream))
+
+
+def pa_hash_blocked_host(n: int, m: int, seed_host_ptr: int, key_host_ptr: int, out_host_ptr: int,
+                         max_block_bits: int = 0, device_budget_bytes: int = 0, stream: int = 0) -> None:
+    _check(_lib.pa_hash_blocked_host(n, m, seed_host_ptr, key_host_ptr, out_host_ptr, max_block_bits,
+                                     device_budget_bytes, stream))
 
 
 def pa_workspace_size(n: int, m: int, opt: pa_options | None = None) -> int:

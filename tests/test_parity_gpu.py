@@ -967,3 +967,75 @@ def test_explicit_device_option():
     with pytest.raises(pa.PaError) as e:
         pa.pa_create_ex(n, m, seed_t.data_ptr(), o, 0)
     assert e.value.status == pa.PA_ERR_INVALID_ARG and "device" in pa.pa_last_error()
+
+
+@pytest.mark.parametrize("n,m,maxb,pinned", [(20_000, 7_000, 5_000, True), (50_001, 20_000, 16_384, False),
+                                             (3001, 3000, 700, True), (100_000, 10_000, 0, True),
+                                             (1_000_003, 250_000, 300_001, True)])
+def test_length_compatible_blocked_host(n, m, maxb, pinned):
+    """pa_hash_blocked_host: seed, key and output in host memory (pinned or
+    pageable), row x column blocks streamed through two staging slots, Eq. (7) XOR merge -- the
+    full output equals the oracle's, and nothing is written past ceil(m/32) words."""
+    sw = syn.random_bits(syn.seed_stream(93 + n), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(93, n), n)
+    seed_h = torch.from_numpy(np.ascontiguousarray(sw).view(np.int32).copy())
+    key_h = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy())
+    out_h = torch.full((pa.words32(m) + 3,), -1, dtype=torch.int32)
+    if pinned:
+        seed_h, key_h, out_h = seed_h.pin_memory(), key_h.pin_memory(), out_h.pin_memory()
+    pa.pa_hash_blocked_host(n, m, seed_h.data_ptr(), key_h.data_ptr(), out_h.data_ptr(), maxb, 0, 0)
+    want = oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m)
+    allb = oracle.unpack(out_h.numpy()[: pa.words32(m)].view(np.uint32), 32 * pa.words32(m))
+    assert np.array_equal(allb[:m], want)
+    assert not allb[m:].any()
+    assert (out_h.numpy()[pa.words32(m):] == -1).all()
+
+
+def test_blocked_host_4gbit_under_16gib_budget():
+    """NEXT-3 at the paper's scale: n = 4*10^9 key bits and the seed stay in pinned
+    host memory; pa_hash_blocked_host streams them through a 16 GiB device budget (peak device
+    use sampled with NVML).  Random key: 64 sampled rows vs the oracle.  All-ones key: every
+    output bit against the closed form y[i] = parity(s[i .. i+n-1]) (y[i+1] = y[i] ^ s[i] ^
+    s[i+n]), computed from the seed alone."""
+    import threading
+    import pynvml
+    n, m = 4 * 10**9, 10**7
+    budget = 16 * 2**30
+    sw = syn.random_bits(syn.seed_stream(160), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(160, 0), n)
+    seed_h = torch.from_numpy(sw.view(np.int32)).pin_memory()
+    key_h = torch.from_numpy(kw.view(np.int32)).pin_memory()
+    out_h = torch.zeros(pa.words32(m), dtype=torch.int32).pin_memory()
+    pynvml.nvmlInit()
+    hnd = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    base = pynvml.nvmlDeviceGetMemoryInfo(hnd).used
+    peak = [base]
+    stop = threading.Event()
+
+    def sample():
+        while not stop.is_set():
+            peak[0] = max(peak[0], pynvml.nvmlDeviceGetMemoryInfo(hnd).used)
+            stop.wait(0.0005)
+    th = threading.Thread(target=sample)
+    th.start()
+    try:
+        pa.pa_hash_blocked_host(n, m, seed_h.data_ptr(), key_h.data_ptr(), out_h.data_ptr(), 0, budget, 0)
+        got = oracle.unpack(out_h.numpy().view(np.uint32), m)
+        ones_h = torch.from_numpy(syn.ones_bits(n).view(np.int32)).pin_memory()
+        pa.pa_hash_blocked_host(n, m, seed_h.data_ptr(), ones_h.data_ptr(), out_h.data_ptr(), 0, budget, 0)
+        got_ones = oracle.unpack(out_h.numpy().view(np.uint32), m)
+    finally:
+        stop.set()
+        th.join()
+    assert peak[0] - base <= budget, f"peak device memory {(peak[0] - base) / 2**30:.2f} GiB"
+    rows = sample_rows(m, 160, k=32)[:64]
+    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+    assert n % 64 == 0  # parity of s[0..n): the popcount parity of the XOR of its words
+    y0 = bin(int(np.bitwise_xor.reduce(sw[: n // 64]))).count("1") & 1
+    lo = np.unpackbits(sw[: (m + 63) // 64].view(np.uint8), bitorder="little")
+    hi = np.unpackbits(sw[n // 64: (n + m + 63) // 64].view(np.uint8), bitorder="little")
+    d = np.bitwise_xor(lo[: m - 1], hi[: m - 1])
+    want = np.concatenate([[y0], np.bitwise_xor.accumulate(d) ^ y0]).astype(np.uint8)
+    assert np.array_equal(got_ones, want)
