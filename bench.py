@@ -472,6 +472,22 @@ def multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush, split, na
     out[f"{other}_split"] = {"gbit_s": n * steps / (float(tt[0]) * 1e-3) / 1e9,
                              "ms_per_hash": float(tt[0]) / steps, "verified_rows": ok}
     sh.close()
+    # the column split with the fused Eq. (7) merge (NEXT-1): partials folded straight from the
+    # peers' memory (pa_xor_fold_peers over CUDA IPC mappings) + one all-gather
+    sh = pd.ColSplit(n, m, seed_t, fused=True)
+    blk = sh.key_block(kw, dev)
+    for _ in range(3):
+        y = sh(blk)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = float(sum(time_steps(torch, lambda: sh(blk), steps, flush)))
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ok = verify_rows(n, m, sw, kw, y.cpu().numpy(), sampled_rows(m, 64)) if rank == 0 else None
+    out["cols_fused_split"] = {"gbit_s": n * steps / (float(tt[0]) * 1e-3) / 1e9,
+                               "ms_per_hash": float(tt[0]) / steps, "verified_rows": ok,
+                               "merge": "pa_xor_fold_peers over CUDA-IPC-mapped peer partials + all_gather"}
+    sh.close()
     for cname in ("C5a", "C5b", "C5c", "C5d"):
         cn, cm, csw, _ = syn.config_inputs(cname)
         idx = list(range(rank, C5_KEYS, world))

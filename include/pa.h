@@ -286,6 +286,28 @@ pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t *seed_host
 pa_status pa_xor_fold(uint32_t *dst, const uint32_t *src, uint64_t words, uint32_t count,
                       uint64_t src_stride_words, void *stream);
 
+/* The Eq. (7) merge over peer memory (multi-GPU input-column split): dst[w] =
+ * XOR over g < count of srcs[g][first_word + w], w < words.  srcs is a DEVICE array of count
+ * device pointers -- this rank's partial and the peers' partials mapped through pa_peer_open
+ * (NVLink / NVSwitch loads); dst 16-byte aligned, first_word a multiple of 4.  The caller orders
+ * it after every rank's hash (e.g. a one-element NCCL all-reduce as a stream barrier). */
+pa_status pa_xor_fold_peers(uint32_t *dst, const uint32_t *const *srcs, uint32_t count, uint64_t first_word,
+                            uint64_t words, void *stream);
+
+/* Peer-mappable device memory for pa_xor_fold_peers: pa_peer_alloc returns a whole cudaMalloc
+ * allocation on the current device (free with pa_peer_free); pa_peer_export fills a 64-byte
+ * handle (CUDA IPC) another process passes to pa_peer_open, which maps the allocation into its
+ * address space (lazy peer access; unmap with pa_peer_close).  A process cannot open its own
+ * handle -- use the pointer directly. */
+typedef struct pa_peer_handle {
+    unsigned char bytes[64];
+} pa_peer_handle;
+pa_status pa_peer_alloc(uint64_t bytes, void **dev_ptr);
+pa_status pa_peer_free(void *dev_ptr);
+pa_status pa_peer_export(const void *dev_ptr, pa_peer_handle *handle);
+pa_status pa_peer_open(const pa_peer_handle *handle, void **dev_ptr);
+pa_status pa_peer_close(void *dev_ptr);
+
 /* Stream-ordered release of everything the handle owns.  Safe on NULL. */
 void pa_destroy(pa_handle h);
 

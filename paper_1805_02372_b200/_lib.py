@@ -35,13 +35,18 @@ EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_
             "pa_destroy", "pa_last_error", "pa_status_string", "pa_version", "pa_profile_enable",
             "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked", "pa_hash_blocked_host",
             "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1",
-            "pa_hash_host_batch"]
+            "pa_hash_host_batch", "pa_xor_fold_peers", "pa_peer_alloc", "pa_peer_free", "pa_peer_export",
+            "pa_peer_open", "pa_peer_close"]
 
 
 class PaError(RuntimeError):
     def __init__(self, status: int, message: str):
         self.status = status
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+
+
+class pa_peer_handle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 64)]
 
 
 class pa_options(ctypes.Structure):
@@ -100,6 +105,12 @@ _sig = {
     "pa_hash_fresh_batch": (_st, [_H, _p, _u64, _p, _u64, _p, _u64, ctypes.c_uint32, _p]),
     "pa_seed_from_paper_eq1": (_st, [_p, _p, _u64, _u64, _p]),
     "pa_xor_fold": (_st, [_p, _p, _u64, ctypes.c_uint32, _u64, _p]),
+    "pa_xor_fold_peers": (_st, [_p, _p, ctypes.c_uint32, _u64, _u64, _p]),
+    "pa_peer_alloc": (_st, [_u64, ctypes.POINTER(_p)]),
+    "pa_peer_free": (_st, [_p]),
+    "pa_peer_export": (_st, [_p, ctypes.POINTER(pa_peer_handle)]),
+    "pa_peer_open": (_st, [ctypes.POINTER(pa_peer_handle), ctypes.POINTER(_p)]),
+    "pa_peer_close": (_st, [_p]),
     "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
                               ctypes.POINTER(ctypes.c_uint32)]),
 }
@@ -256,3 +267,36 @@ def pa_hash_host_batch(h: int, keys_host_ptr: int, key_stride_words: int, outs_h
                        out_stride_words: int, count: int, stream: int = 0) -> None:
     _check(_lib.pa_hash_host_batch(h, keys_host_ptr, key_stride_words, outs_host_ptr, out_stride_words, count,
                                    stream))
+
+
+def pa_xor_fold_peers(dst_ptr: int, srcs_dev_ptr: int, count: int, first_word: int, words: int,
+                      stream: int = 0) -> None:
+    _check(_lib.pa_xor_fold_peers(dst_ptr, srcs_dev_ptr, count, first_word, words, stream))
+
+
+def pa_peer_alloc(nbytes: int) -> int:
+    p = _p()
+    _check(_lib.pa_peer_alloc(nbytes, ctypes.byref(p)))
+    return int(p.value)
+
+
+def pa_peer_free(ptr: int) -> None:
+    _check(_lib.pa_peer_free(ptr))
+
+
+def pa_peer_export(ptr: int) -> bytes:
+    h = pa_peer_handle()
+    _check(_lib.pa_peer_export(ptr, ctypes.byref(h)))
+    return bytes(h.bytes)
+
+
+def pa_peer_open(handle: bytes) -> int:
+    h = pa_peer_handle()
+    ctypes.memmove(h.bytes, handle, 64)
+    p = _p()
+    _check(_lib.pa_peer_open(ctypes.byref(h), ctypes.byref(p)))
+    return int(p.value)
+
+
+def pa_peer_close(ptr: int) -> None:
+    _check(_lib.pa_peer_close(ptr))

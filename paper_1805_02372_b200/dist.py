@@ -11,7 +11,10 @@ Three exact decompositions of y = T x (Eq. (1)):
   from the source rank, or already resident: P:107) and the seed window
   s[n - c1 : n - c0 + m - 1]; partial m-bit hashes are XOR-reduced.  NCCL has no
   XOR reduction (nccl.h: Sum/Prod/Max/Min/Avg), so the merge is a reduce-scatter
-  built from all_to_all_single + libpa's XOR-fold kernel, then an all-gather.
+  built from all_to_all_single + libpa's XOR-fold kernel, then an all-gather -- or,
+  fused (ColSplit(fused=True)), K3 leaves each partial in a
+  peer-mappable buffer and one kernel (pa_xor_fold_peers) folds this rank's slice
+  of every partial straight from the peers' memory over NVLink, then an all-gather.
 * Independent keys (configs[4]): keys are dealt round-robin, hashed in batches
   (pa_hash_batch); no collective on the data path.
 
@@ -222,8 +225,9 @@ class ColSplit:
     Per-rank transform >= n/W + m - 1."""
 
     def __init__(self, n: int, m: int, seed_t: torch.Tensor, group=None, factory=None, hash_fn=None,
-                 xor_fn: Callable | None = None):
+                 xor_fn: Callable | None = None, fused: bool = False):
         self.n, self.m, self.group = n, m, group
+        self.fused = fused
         self.world, self.rank = _world_rank(group)
         self.ranges = col_ranges(n, m, self.world)
         self.c0, self.c1 = self.ranges[self.rank]
@@ -241,6 +245,55 @@ class ColSplit:
         # key scatter: equal chunks of blk_w words (the widest block), block g at word c0_g / 32
         self.blk_w = max(_words4(b - a) for a, b in self.ranges)
         self.blk = torch.zeros(self.blk_w, dtype=torch.int32, device=dev)
+        self._opened, self.part_ptr = [], None
+        if fused:
+            self._setup_peers(dev)
+
+    def _setup_peers(self, dev):
+        """Fused merge: this rank's partial lives in a peer-mappable buffer
+        (pa_peer_alloc); the buffers' IPC handles are exchanged once (all_gather_object) and the
+        peers' partials mapped (pa_peer_open), so the Eq. (7) fold reads them over NVLink."""
+        from . import pa_peer_alloc, pa_peer_export, pa_peer_open
+        if self.h is None or not hasattr(self.h, "handle"):
+            raise ValueError("the fused column split needs libpa handles on CUDA devices")
+        self.part_ptr = pa_peer_alloc(4 * self.world * self.slice_w)
+        handles = [None] * self.world
+        mine = pa_peer_export(self.part_ptr)
+        if self.world > 1:
+            dist.all_gather_object(handles, mine, group=self.group)
+        else:
+            handles = [mine]
+        ptrs = []
+        for g, hd in enumerate(handles):
+            if g == self.rank:
+                ptrs.append(self.part_ptr)
+            else:
+                p = pa_peer_open(hd)
+                self._opened.append(p)
+                ptrs.append(p)
+        self.ptrs_dev = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        self.myslice = torch.zeros(self.slice_w, dtype=torch.int32, device=dev)
+        self.tick = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.valid = max(0, min(self.slice_w, self.words - self.rank * self.slice_w))
+
+    def _fused_call(self, key_block_t: torch.Tensor) -> torch.Tensor:
+        """K3 leaves this rank's partial in its peer-visible buffer; one stream-ordered barrier
+        (a one-element NCCL all-reduce); pa_xor_fold_peers folds this rank's slice of all G
+        partials straight from the peers' memory (the reduce-scatter and the XOR in one kernel);
+        one all-gather of the slices.  The all-gather also orders the next step's hash (which
+        rewrites the partial) after every peer's fold."""
+        from . import _lib
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.pa_hash(self.h.handle, key_block_t.data_ptr(), self.part_ptr, st)
+        if self.world > 1:
+            dist.all_reduce(self.tick, group=self.group)
+        if self.valid:
+            _lib.pa_xor_fold_peers(self.myslice.data_ptr(), self.ptrs_dev.data_ptr(), self.world,
+                                   self.rank * self.slice_w, self.valid, st)
+        if self.world == 1:
+            return self.myslice[: self.words]
+        dist.all_gather_into_tensor(self.gathered, self.myslice, group=self.group)
+        return self.gathered[: self.words]
 
     def key_block(self, key_words: np.ndarray, device) -> torch.Tensor:
         """This rank's key bits [c0, c1) as device words (host-side extraction)."""
@@ -269,6 +322,8 @@ class ColSplit:
         return self.blk
 
     def __call__(self, key_block_t: torch.Tensor) -> torch.Tensor:
+        if self.fused:
+            return self._fused_call(key_block_t)
         if self.h is not None:
             part = self.h.hash(key_block_t)
             self.mine[: self.words] = part[: self.words]
@@ -280,6 +335,15 @@ class ColSplit:
         return self.gathered[: self.words]
 
     def close(self):
+        if self._opened or self.part_ptr:
+            from . import pa_peer_close, pa_peer_free
+            torch.cuda.synchronize(self.device)
+            if self.world > 1:
+                dist.barrier(group=self.group)  # no peer still reads this rank's partial
+            for p in self._opened:
+                pa_peer_close(p)
+            pa_peer_free(self.part_ptr)
+            self._opened, self.part_ptr = [], None
         if self.h is not None:
             self.h.close()
 
@@ -351,7 +415,8 @@ def hash_keys(n: int, m: int, seed_t: torch.Tensor, keys: torch.Tensor, group=No
 
 
 def hash(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=None, split: str = "auto",
-         src: int = 0, factory=None, hash_fn: Callable | None = None, xor_fn: Callable | None = None):
+         src: int = 0, factory=None, hash_fn: Callable | None = None, xor_fn: Callable | None = None,
+         fused: bool = False):
     """One key over all ranks of `group`, the split chosen by choose_split (or forced):
     rank src holds the key (device words); returns (split, y words) on every rank."""
     world, _ = _world_rank(group)
@@ -359,5 +424,11 @@ def hash(n: int, m: int, seed_t: torch.Tensor, key_t: torch.Tensor, group=None, 
         split = choose_split(n, m, world)
     if split == "rows":
         return split, hash_rows(n, m, seed_t, key_t, group, hash_fn, factory, src=src)
+    if fused:
+        sh = ColSplit(n, m, seed_t, group, factory, hash_fn, xor_fn, fused=True)
+        try:
+            return split, sh(sh.scatter_key(key_t, src)).clone()
+        finally:
+            sh.close()
     return split, hash_cols(n, m, seed_t, None, group, hash_fn, key_t.device, xor_fn, factory,
                             key_t=key_t, src=src)

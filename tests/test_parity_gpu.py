@@ -334,8 +334,46 @@ def test_dist_driver_single_rank_nccl():
             torch.cuda.synchronize()
             assert np.array_equal(from_dev(y, m), want), cls.__name__
             sh.close()
+        # fused Eq. (7) merge (NEXT-1): K3's partial in a peer-mappable buffer, folded by
+        # pa_xor_fold_peers through the device pointer table, for several steps and shapes
+        for nn, mm in ((n, m), (4096 * 3 + 17, 5_000), (1_000_003, 250_000)):
+            s2 = syn.random_bits(syn.seed_stream(73), nn + mm - 1)
+            k2 = [syn.random_bits(syn.key_stream(73, k), nn) for k in range(3)]
+            sh = pd.ColSplit(nn, mm, to_dev(s2), fused=True)
+            for kk in k2:
+                y = sh(sh.key_block(kk, DEV))
+                torch.cuda.synchronize()
+                assert np.array_equal(from_dev(y, mm), oracle.unpack(oracle.toeplitz_words(nn, mm, s2, kk), mm))
+            sh.close()
+        # the one-shot auto entry point: key on the source rank, cost-model split
+        split, y = pd.hash(n, m, seed_t, to_dev(kw))
+        torch.cuda.synchronize()
+        assert split == "rows" and np.array_equal(from_dev(y, m), want)
     finally:
         dist.destroy_process_group()
+
+
+def test_xor_fold_peers_pointer_table():
+    """pa_xor_fold_peers over a device table of pointers (here all local): dst = XOR of the
+    slices [first, first + words) of every source, ragged lengths and offsets."""
+    rng = np.random.default_rng(5)
+    for G, words, first in ((1, 7, 0), (3, 1000, 4), (8, 4097, 12), (5, 3, 8)):
+        srcs = [torch.from_numpy(rng.integers(-2**31, 2**31, first + words + 5, dtype=np.int64).astype(np.int32))
+                .to(DEV) for _ in range(G)]
+        table = torch.tensor([t.data_ptr() for t in srcs], dtype=torch.int64, device=DEV)
+        dst = torch.full((words + 4,), -1, dtype=torch.int32, device=DEV)
+        pa.pa_xor_fold_peers(dst.data_ptr(), table.data_ptr(), G, first, words, 0)
+        torch.cuda.synchronize()
+        want = np.zeros(words, np.int32)
+        for t in srcs:
+            want ^= t.cpu().numpy()[first:first + words]
+        assert np.array_equal(dst.cpu().numpy()[:words], want)
+        assert (dst.cpu().numpy()[words:] == -1).all()
+    ptr = pa.pa_peer_alloc(4096)
+    try:
+        assert len(pa.pa_peer_export(ptr)) == 64
+    finally:
+        pa.pa_peer_free(ptr)
 
 
 def test_host_async_graph_repoints_buffers():
