@@ -639,10 +639,14 @@ def sweep(torch, pa, dev, steps=10):
     sh_, kh_ = torch.from_numpy(sw.view(np.int32)).pin_memory(), torch.from_numpy(kw.view(np.int32)).pin_memory()
     oh_ = torch.zeros(pa.words32(m), dtype=torch.int32).pin_memory()
     budget = 16 << 30
-    pa.pa_hash_blocked_host(n, m, sh_.data_ptr(), kh_.data_ptr(), oh_.data_ptr(), 0, budget, 0)
-    t0 = time.perf_counter()
-    pa.pa_hash_blocked_host(n, m, sh_.data_ptr(), kh_.data_ptr(), oh_.data_ptr(), 0, budget, 0)
-    t = time.perf_counter() - t0
+    ts = []
+    for i in range(6):  # the first calls pay one-time costs (pinned-page mappings, the block handle)
+        t0 = time.perf_counter()
+        pa.pa_hash_blocked_host(n, m, sh_.data_ptr(), kh_.data_ptr(), oh_.data_ptr(), 0, budget, 0)
+        if i >= 3:
+            ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    pa.pa_hash_blocked_release()
     res["NEXT3_host_1e9"] = {"n": n, "m": m, "s_per_hash": t, "gbit_s": n / t / 1e9, "device_budget_gib": 16,
                              "verified_rows": verify_rows(n, m, sw, kw, oh_.numpy(), sampled_rows(m, 16)),
                              "note": "pa_hash_blocked_host: key and seed in pinned host memory, row x column blocks "

@@ -36,7 +36,7 @@ EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_
             "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked", "pa_hash_blocked_host",
             "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1",
             "pa_hash_host_batch", "pa_xor_fold_peers", "pa_peer_alloc", "pa_peer_free", "pa_peer_export",
-            "pa_peer_open", "pa_peer_close"]
+            "pa_peer_open", "pa_peer_close", "pa_hash_blocked_release"]
 
 
 class PaError(RuntimeError):
@@ -111,6 +111,7 @@ _sig = {
     "pa_peer_export": (_st, [_p, ctypes.POINTER(pa_peer_handle)]),
     "pa_peer_open": (_st, [ctypes.POINTER(pa_peer_handle), ctypes.POINTER(_p)]),
     "pa_peer_close": (_st, [_p]),
+    "pa_hash_blocked_release": (None, []),
     "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
                               ctypes.POINTER(ctypes.c_uint32)]),
 }
@@ -300,3 +301,7 @@ def pa_peer_open(handle: bytes) -> int:
 
 def pa_peer_close(ptr: int) -> None:
     _check(_lib.pa_peer_close(ptr))
+
+
+def pa_hash_blocked_release() -> None:
+    _lib.pa_hash_blocked_release()

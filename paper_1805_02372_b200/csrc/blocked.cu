@@ -23,6 +23,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "bits.cuh"
 #include "pa_internal.h"
@@ -78,6 +79,16 @@ struct Staging {
 }  // namespace pa
 
 using namespace pa;
+
+// The block handle is kept between calls of the same block shape on the same device (creating a
+// multi-GB handle and freeing it costs more than hashing a block); pa_hash_blocked_release frees
+// it.  Calls are serialised on this cache.
+static std::mutex g_bmutex;
+static struct BlockCache {
+    pa_handle h = nullptr;
+    uint64_t nb = 0, mb = 0, off = 0;
+    int device = -1;
+} g_bcache;
 
 // The block loop shared by the device- and host-resident entry points.
 static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits, const uint32_t *key_bits,
@@ -137,7 +148,17 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
     uint32_t *tpart = blk + 2 * (st.sw + st.kw), *tacc[2] = {tpart + ow, tpart + 2 * ow};
     cudaStream_t cs = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_free[2] = {}, ev_acc[2] = {}, ev_out[2] = {};
+    std::lock_guard<std::mutex> lock(g_bmutex);
+    int dev = 0;
+    cudaGetDevice(&dev);
     pa_handle hb = nullptr;
+    if (g_bcache.h && g_bcache.nb == nb && g_bcache.mb == mb && g_bcache.off == off && g_bcache.device == dev) {
+        hb = g_bcache.h;
+    } else if (g_bcache.h) {
+        pa_destroy(g_bcache.h);
+        g_bcache = BlockCache{};
+    }
+    const bool fresh = hb == nullptr;
     pa_status res = PA_OK;
     auto fail = [&](pa_status r) {
         if (res == PA_OK) res = r;
@@ -205,6 +226,11 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
                 o.seed_bit_offset = off;
                 o.allow_wide = 1;
                 if (fail(pa_create_ex(&hb, nb, mb, st.seed[i], &o, s)) != PA_OK) break;
+                g_bcache.h = hb;
+                g_bcache.nb = nb;
+                g_bcache.mb = mb;
+                g_bcache.off = off;
+                g_bcache.device = dev;
             } else if (fail(pa_set_seed(hb, st.seed[i], s)) != PA_OK) {
                 break;
             }
@@ -243,7 +269,11 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
         cudaStreamDestroy(cs);
     }
     cudaStreamSynchronize(s);
-    pa_destroy(hb);
+    if (res != PA_OK && g_bcache.h) {  // a failed call does not leave a handle in an unknown state
+        pa_destroy(g_bcache.h);
+        g_bcache = BlockCache{};
+    }
+    (void)fresh;
     for (int i = 0; i < 2; ++i)
         for (cudaEvent_t ev : {ev_in[i], ev_free[i], ev_acc[i], ev_out[i]})
             if (ev) cudaEventDestroy(ev);
@@ -253,14 +283,23 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
 
 // default block limit: the whole product if one handle can plan it, else the longest
 // transform the planner accepts (binary search over n' + m' - 1)
+// default block limit: the longest blocks whose (nb, mb) shape route (a) plans as ONE transform
+// (a block that itself needed the in-handle Eq. (4) split would transform its seed windows twice)
+static bool one_plan(uint64_t n, uint64_t m, uint64_t lim)
+{
+    uint64_t nb, mb;
+    if (!block_shape(n, m, lim, &nb, &mb)) return false;
+    Geometry g;
+    char err[256];
+    return ra_plan(nb, mb, &g, err, sizeof err, 0) == PA_OK;
+}
 static uint64_t default_limit(uint64_t n, uint64_t m)
 {
-    pa_info info;
-    if (pa_plan(n, m, &info) == PA_OK && info.column_blocks <= 1) return n + m - 1;
+    if (one_plan(n, m, n + m - 1)) return n + m - 1;
     uint64_t lo = 64, hi = n + m - 1;
     while (lo + 1 < hi) {
         const uint64_t mid = lo + (hi - lo) / 2;
-        if (pa_plan(mid, 1, &info) == PA_OK && info.column_blocks <= 1) lo = mid;
+        if (one_plan(n, m, mid)) lo = mid;
         else hi = mid;
     }
     return lo;
@@ -300,4 +339,16 @@ extern "C" pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t
     }
     return blocked_impl(n, m, seed_host, key_host, out_host, lim, true, device_budget_bytes, (cudaStream_t)stream,
                         "pa_hash_blocked_host");
+}
+
+extern "C" void pa_hash_blocked_release(void)
+{
+    std::lock_guard<std::mutex> lock(g_bmutex);
+    if (g_bcache.h) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        pa_destroy(g_bcache.h);  // switches to the handle's device itself
+        cudaSetDevice(prev);
+    }
+    g_bcache = BlockCache{};
 }

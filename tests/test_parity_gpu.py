@@ -906,6 +906,7 @@ def test_gigabit_under_2gib_budget_and_plan_consistency():
     with pa.Hasher(n2, m2, seed2) as h:
         outs.append(from_dev(h.hash(key2), m2))
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    pa.pa_hash_blocked_release()
 
 
 @pytest.mark.parametrize("n,m,count,kwargs", [(1_048_576, 104_857, 64, {}), (4096, 1024, 500, {}),
@@ -1067,6 +1068,7 @@ def test_blocked_host_4gbit_under_16gib_budget():
     finally:
         stop.set()
         th.join()
+    pa.pa_hash_blocked_release()
     assert peak[0] - base <= budget, f"peak device memory {(peak[0] - base) / 2**30:.2f} GiB"
     rows = sample_rows(m, 160, k=32)[:64]
     assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
