@@ -845,8 +845,11 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 #ifndef K2T_STAGE
 #define K2T_STAGE stage_inl
 #endif
+#ifndef PA_K2MAX
+#define PA_K2MAX PA_TMAX  // developer experiments: K2's launch bound (PA_FORCE_T2 up to it)
+#endif
 template <int R0, int R1, int NS>
-__global__ void __launch_bounds__(PA_TMAX, PA_MINB)
+__global__ void __launch_bounds__(PA_K2MAX, PA_MINB)
 k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T,
           uint64_t spec_stride)
 {
@@ -1498,7 +1501,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     // ballot runs need whole warps, and warps a multiple of C) within [64, PA_TMAX]
     auto threads_ok = [](const char *e) {
         const int v = e ? atoi(e) : 0;
-        return v >= 64 && v <= PA_TMAX && v % 32 == 0;
+        return v >= 64 && v <= (PA_K2MAX > PA_TMAX ? PA_K2MAX : PA_TMAX) && v % 32 == 0;
     };
     if (const char *e = dev_env("PA_FORCE_T1"); threads_ok(e)) g->t1 = (uint32_t)atoi(e);
     if (const char *e = dev_env("PA_FORCE_T2"); threads_ok(e)) g->t2 = (uint32_t)atoi(e);

@@ -27,6 +27,11 @@ WANT = {
     "launch__occupancy_limit_shared_mem": "occ_limit_smem",
     "launch__block_size": "block",
     "launch__grid_size": "grid",
+    "smsp__inst_executed.sum": "warp_inst",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum": "thread_dfma",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "thread_dmul",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum": "thread_dadd",
+    "smsp__warps_active.avg.per_cycle_active": "warps_per_smsp",
     "smsp__average_warp_latency_issue_stalled_barrier": "stall_barrier",
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio": "stall_long_sb",
     "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio": "stall_barrier",
