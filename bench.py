@@ -60,6 +60,9 @@ def parse_args():
                     help="N > 1: how the key is split (rows = configured; auto = dist.choose_split)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the other-config side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline")
+    ap.add_argument("--side-smoke", action="store_true",
+                    help="N = 1: also run the N > 1 side measurements (splits, fused merge, key dealing) "
+                         "over a one-rank NCCL group -- a code-path check, not a scaling number")
     ap.add_argument("--selftest-cpu", action="store_true",
                     help="multi-rank plumbing check on CPU (gloo, oracle as the per-rank hash)")
     return ap.parse_args()
@@ -296,6 +299,10 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif args.side_smoke:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(free_port()))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     name = args.config
     n, m, sw, kw = syn.config_inputs(name)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -403,8 +410,9 @@ def run_ours(args):
 
     # N > 1: the other split and the cost model's choice, and C5 key dealing, same protocol
     side = {}
-    if world > 1:
-        side = multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush, split, name)
+    if world > 1 or args.side_smoke:
+        side = multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush,
+                              split if world > 1 else "cols", name)
 
     t = torch.tensor([tot_ms, float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
@@ -458,7 +466,7 @@ def run_ours(args):
         sh.close()
     else:
         h.close()
-    if world > 1:
+    if world > 1 or args.side_smoke:
         dist.barrier()
         dist.destroy_process_group()
     return line
