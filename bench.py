@@ -436,11 +436,14 @@ def run_ours(args):
             "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
             "dtype": "f64" if info["route"] == 1 else "u32",
             "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits (SURVEY 8(d) streams)",
-            "config": {"workload": workload_desc(name), "n": n, "m": m, "route": h.route,
-                       "transform_len": info["transform_len"], "n1": info["n1"], "n2": info["n2"],
-                       "cols_per_cta": info["cols_per_cta"], "split": split, "parallelism": parallelism,
-                       "l2": "flushed before every step (256 MiB memset, untimed); working set > L2",
-                       "verified_rows": verified},
+            # config: the same keys as the reference arm's line (the workload); how it ran is in
+            # "plan" / "parallelism"
+            "config": {"workload": workload_desc(name), "n": n, "m": m},
+            "plan": {"route": h.route, "transform_len": info["transform_len"], "n1": info["n1"], "n2": info["n2"],
+                     "cols_per_cta": info["cols_per_cta"], "split": split,
+                     "l2": "flushed before every step (256 MiB memset, untimed); working set > L2",
+                     "verified_rows": verified},
+            "parallelism": parallelism,
             "roofline": roof,
             "kernels_us": {k: v[1] / max(1, v[0]) * 1e3 for k, v in kern.items()},
             "e2e": {"value": stream_e2e["value"] if stream_e2e else n / (e2e_mean * 1e-3) / 1e9,
