@@ -145,3 +145,43 @@ def test_k3_half_column_groups(n, m, plan, tmp_path):
                   {"PA_FORCE_PLAN": plan, "PA_K3_HALF": half})
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def body_k1p_off(n, m, count, out):
+    """Hash `count` keys with K1P disabled (PA_K1P=0: the non-persistent K1) and save them."""
+    import numpy as np
+
+    import pa_synth as syn
+    np_, oracle, pa, to_dev, from_dev, sample_rows = _helpers()
+    sw = syn.random_bits(syn.seed_stream(171), n + m - 1)
+    keys = syn.random_bits_torch([syn.key_stream(171, k) for k in range(count)], n, "cuda")
+    with pa.Hasher(n, m, to_dev(sw), route="transform") as h:
+        outs = h.hash_batch(keys)
+        torch.cuda.synchronize()
+        np.save(out, outs.cpu().numpy())
+
+
+@pytest.mark.parametrize("count", [1, 3])
+def test_k1p_matches_plain_k1(count, tmp_path):
+    """K1P (persistent K1, TMEM write-behind; the product path at C4) performs the same FP64
+    operations in the same order as the plain K1, so the hashes are identical bit for bit -- one
+    key and a batch whose tiles span keys; plus sampled rows of the last key vs the oracle."""
+    import numpy as np
+
+    import oracle
+    import paper_1805_02372_b200 as pa
+    import pa_synth as syn
+    n, m = 100_000_000, 20_000_000
+    sw = syn.random_bits(syn.seed_stream(171), n + m - 1)
+    seed = torch.from_numpy(np.ascontiguousarray(sw).view(np.int32).copy()).cuda()
+    keys = syn.random_bits_torch([syn.key_stream(171, k) for k in range(count)], n, "cuda")
+    with pa.Hasher(n, m, seed, route="transform") as h:
+        assert h.info["cols_per_cta"] == 2  # the C4 plan K1P serves
+        outs = h.hash_batch(keys).cpu().numpy()
+    f = str(tmp_path / "plain.npy")
+    run_child("body_k1p_off", {"n": n, "m": m, "count": count, "out": f}, {"PA_K1P": "0"})
+    assert np.array_equal(outs, np.load(f))
+    kk = syn.random_bits(syn.key_stream(171, count - 1), n)
+    rows = np.unique(np.random.default_rng(7).integers(0, m, 128))
+    got = oracle.unpack(outs[count - 1].view(np.uint32), m)
+    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kk, rows))
