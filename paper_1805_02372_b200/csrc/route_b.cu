@@ -13,6 +13,7 @@
 // broadcast load, and CTAs along y take disjoint key-word chunks whose partial
 // parities are merged with atomicXor (order-independent, hence deterministic).
 #include <algorithm>
+#include <atomic>
 
 #include "bits.cuh"
 #include "bulk.cuh"
@@ -225,10 +226,14 @@ pa_status rb_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         e = count == 1 ? cudaMemsetAsync(outs, 0, zero_words * 4, s)
                        : cudaMemset2DAsync(outs, out_stride * 4, 0, zero_words * 4, count, s);
     if (e != cudaSuccess) return cuda_fail(e, "route (b) output memset");
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_toeplitz_bitpacked, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        attr = true;
+    // the shared-memory attribute is per device (a process may drive several): set once per device
+    static std::atomic<uint64_t> attr_done{0};
+    const uint64_t bit = h->device < 64 ? 1ull << h->device : 0;
+    if (!bit || !(attr_done.load() & bit)) {
+        if ((e = cudaFuncSetAttribute(k_toeplitz_bitpacked, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)) !=
+            cudaSuccess)
+            return cuda_fail(e, "route (b) cudaFuncSetAttribute");
+        attr_done.fetch_or(bit);
     }
     prof_begin(h, 3, s);
     for (uint32_t k0 = 0; k0 < count; k0 += 65535) {
