@@ -1370,7 +1370,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
                 for (int i = 0; i < p.S; ++i) w += p.st[i].R >= 8 ? 1.0 : 1.25;
                 return w;
             };
-            const double pass13 = p2.S + 2.0, pass2 = 2.0 * wsum(p1) + 1.0;
+            // radix weights for the column plan as well (round 2: n = 10^6, m = 10^5 took 2048 x 280
+            // = [7, 5, 8] columns at 44.0 us over 4096 x 144 = [3, 3, 16] at 33.8 us)
+            const double pass13 = wsum(p2) + 2.0, pass2 = 2.0 * wsum(p1) + 1.0;
             const double cfac = C == 1 ? 1.5 : C == 2 ? 1.0 : 0.95;  // short HBM runs (K1/K3)
             const uint32_t occ13 = std::min<uint32_t>(2, kSmemLimit / s13);
             const uint32_t occ2 = std::min<uint32_t>(2, kSmemLimit / smem_k2(N1, p1));
@@ -1382,7 +1384,13 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             // two CTAs per SM overlap one tile's HBM phases with the other's compute (measured:
             // C3 at C = 4, 2 per SM, 192 us vs C = 8, 1 per SM, 206 us -- same waves)
             const double ov13 = occ13 >= 2 ? 0.92 : 1.0, ov2 = occ2 >= 2 ? 0.92 : 1.0;
-            double cost = 2 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C)) + ktime(pass2, ov2, occ2, (double)N2);
+            // the shape-specialised kernels (k2_rows_t, the kK13 instantiations) run faster than the
+            // general ones: prefer plans that have them
+            FftPlan p2a;
+            const bool spec13 = k13_shape(p2) || (make_plan(N2, &p2a, 16, true) && k13_shape(p2a));
+            const double f2 = k2_shape(p1) ? 0.9 : 1.0, f13 = spec13 ? 0.95 : 1.0;
+            double cost = 2 * f13 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C)) +
+                          f2 * ktime(pass2, ov2, occ2, (double)N2);
             if (cost < best) {
                 best = cost;
                 found = true;

@@ -21,7 +21,11 @@ def words(w):
 
 
 name = sys.argv[1]
-n, m, sw, kw = syn.config_inputs(name)
+if "," in name:  # "n,m": an arbitrary shape
+    n, m = (int(v) for v in name.split(","))
+    sw, kw = syn.random_bits(syn.seed_stream(70), n + m - 1), syn.random_bits(syn.key_stream(70, 1), n)
+else:
+    n, m, sw, kw = syn.config_inputs(name)
 seed, key = words(sw), words(kw)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ref = None
