@@ -1328,6 +1328,18 @@ static uint32_t smem_k13(uint32_t N2, uint32_t C, const FftPlan &p2)
 }
 static uint32_t smem_k2(uint32_t N1, const FftPlan &p1) { return tile_bytes(N1) + (2 * (64 + p1.nhi) + p1.ntw) * 16; }
 
+#ifdef PA_DEV
+// developer build: every candidate plan the cost model scored (pa_dev_plan_candidates)
+struct PlanCand {
+    double cost;
+    uint32_t N1, N2, C;
+};
+constexpr int kMaxCand = 4096;
+static thread_local PlanCand g_cand[kMaxCand];
+static thread_local int g_ncand = 0;
+static thread_local bool g_cand_on = false;
+#endif
+
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len)
 {
     const uint64_t L = n + m - 1;
@@ -1389,8 +1401,16 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             FftPlan p2a;
             const bool spec13 = k13_shape(p2) || (make_plan(N2, &p2a, 16, true) && k13_shape(p2a));
             const double f2 = k2_shape(p1) ? 0.9 : 1.0, f13 = spec13 ? 0.95 : 1.0;
-            double cost = 2 * f13 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C)) +
-                          f2 * ktime(pass2, ov2, occ2, (double)N2);
+            // K1 runs as the persistent TMEM write-behind K1P on one-CTA-per-SM multi-wave plans
+            // (C4: K1 735 -> 670 us; the calibration sweep, tools/dev/plan_calib.py, found the
+            // model preferring two-CTA C = 2 plans over faster K1P C = 4 ones without this)
+            const bool k1p = spec13 && occ13 == 1 && C < 16 && N1 / C >= 2 * 148u && p2.S >= 3 &&
+                             p2.st[p2.S - 1].R == 16;
+            const double t13 = f13 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C));
+            double cost = t13 * (k1p ? 0.91 : 1.0) + t13 + f2 * ktime(pass2, ov2, occ2, (double)N2);
+#ifdef PA_DEV
+            if (g_cand_on && g_ncand < kMaxCand) g_cand[g_ncand++] = {cost, N1, N2, C};
+#endif
             if (cost < best) {
                 best = cost;
                 found = true;
@@ -1905,3 +1925,28 @@ void ra_destroy(pa_ctx *h)
 }
 
 }  // namespace pa
+
+#ifdef PA_DEV
+// Developer build only: the cost model's candidates for (n, m), cheapest first (cost in
+// seconds, N1, N2, C), for plan-calibration sweeps (tools/dev/plan_calib.py).
+extern "C" int pa_dev_plan_candidates(uint64_t n, uint64_t m, double *cost, uint32_t *n1, uint32_t *n2, uint32_t *c,
+                                      int max)
+{
+    using namespace pa;
+    Geometry g;
+    char err[256];
+    g_ncand = 0;
+    g_cand_on = true;
+    ra_plan(n, m, &g, err, sizeof err, 0);
+    g_cand_on = false;
+    std::sort(g_cand, g_cand + g_ncand, [](const PlanCand &a, const PlanCand &b) { return a.cost < b.cost; });
+    const int k = g_ncand < max ? g_ncand : max;
+    for (int i = 0; i < k; ++i) {
+        cost[i] = g_cand[i].cost;
+        n1[i] = g_cand[i].N1;
+        n2[i] = g_cand[i].N2;
+        c[i] = g_cand[i].C;
+    }
+    return k;
+}
+#endif

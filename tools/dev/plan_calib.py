@@ -1,0 +1,78 @@
+"""Plan calibration sweep (developer build): for seeded random (n, m), measure the cost model's
+top-K candidate plans (pa_dev_plan_candidates) with PA_FORCE_PLAN and print model cost vs measured
+time as JSON lines.
+
+    PA_LIB=$PWD/paper_1805_02372_b200/libpa_dev.so python tools/dev/plan_calib.py [count] [K] [seed]
+"""
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import pa_synth as syn  # noqa: E402
+import paper_1805_02372_b200 as pa  # noqa: E402
+from paper_1805_02372_b200 import _lib  # noqa: E402
+
+count = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+rng = np.random.default_rng(int(sys.argv[3]) if len(sys.argv) > 3 else 1805)
+f = _lib._lib.pa_dev_plan_candidates
+f.restype = ctypes.c_int
+f.argtypes = [ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 4 + [ctypes.c_int]
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+
+def words(w):
+    w = np.ascontiguousarray(w).view(np.int32)
+    w = np.concatenate([w, np.zeros((-w.size) % 4, np.int32)])
+    return torch.from_numpy(w.copy()).cuda()
+
+
+for _ in range(count):
+    n = int(np.exp(rng.uniform(np.log(1e6), np.log(1e8))))
+    m = int(n * float(rng.choice([0.1, 0.2, 0.25])))
+    cost = (ctypes.c_double * 4096)()
+    n1, n2, c = (ctypes.c_uint32 * 4096)(), (ctypes.c_uint32 * 4096)(), (ctypes.c_uint32 * 4096)()
+    k = f(n, m, cost, n1, n2, c, 4096)
+    seen, cands = set(), []
+    for i in range(k):
+        key = (n1[i], n2[i], c[i])
+        if key not in seen:
+            seen.add(key)
+            cands.append((cost[i], *key))
+        if len(cands) >= K:
+            break
+    sw, kw = syn.random_bits(syn.seed_stream(80), n + m - 1), syn.random_bits(syn.key_stream(80, 0), n)
+    seed, key_t = words(sw), words(kw)
+    res = []
+    ref = None
+    for cst, a, b, cc in cands:
+        os.environ["PA_FORCE_PLAN"] = f"{a},{b},{cc}"
+        try:
+            h = pa.Hasher(n, m, seed, route="transform")
+        except pa.PaError:
+            continue
+        out = h.new_out()
+        for _ in range(3):
+            h.hash(key_t, out)
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            h.hash(key_t, out)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        o = out.cpu().numpy()[: (m + 31) // 32]
+        same = True if ref is None else bool(np.array_equal(o, ref))
+        ref = o if ref is None else ref
+        res.append({"plan": [a, b, cc], "model_us": cst * 1e6, "meas_us": float(np.median(ts)) * 1e3, "same": same})
+        h.close()
+    os.environ.pop("PA_FORCE_PLAN", None)
+    print(json.dumps({"n": n, "m": m, "cands": res}), flush=True)

@@ -20,6 +20,11 @@ def words(w):
     return torch.from_numpy(w.copy()).cuda()
 
 
+batch = 1
+if "--batch" in sys.argv:  # distinct keys per timed call (pa_hash_batch)
+    i = sys.argv.index("--batch")
+    batch = int(sys.argv[i + 1])
+    del sys.argv[i:i + 2]
 name = sys.argv[1]
 if "," in name:  # "n,m": an arbitrary shape
     n, m = (int(v) for v in name.split(","))
@@ -36,14 +41,20 @@ for plan in ["default"] + sys.argv[2:]:
         os.environ["PA_FORCE_PLAN"] = plan
     h = pa.Hasher(n, m, seed, route="transform")
     out = h.new_out()
+    if batch > 1:
+        keys = syn.random_bits_torch([syn.key_stream(81, k) for k in range(batch)], n, "cuda")
+        outs = h.new_out(batch)
+        hash_once = lambda: h.hash_batch(keys, outs)  # noqa: E731
+    else:
+        hash_once = lambda: h.hash(key, out)  # noqa: E731
     for _ in range(3):
-        h.hash(key, out)
+        hash_once()
     ts = []
     for _ in range(15):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        h.hash(key, out)
+        hash_once()
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -51,7 +62,7 @@ for plan in ["default"] + sys.argv[2:]:
     pa.pa_profile_read(h.handle)
     for _ in range(5):
         flush.zero_()
-        h.hash(key, out)
+        hash_once()
     kern = pa.pa_profile_read(h.handle)
     got = out.cpu().numpy()
     if ref is None:
@@ -60,5 +71,5 @@ for plan in ["default"] + sys.argv[2:]:
     ks = " ".join(f"{k.split('_')[0]}={v[1] / v[0] * 1e3:.1f}" for k, v in kern.items())
     i = h.info
     print(f"{plan:18s} -> {i['n1']}x{i['n2']} C={i['cols_per_cta']} C3={i['k3_cols_per_cta']}: "
-          f"{np.median(ts) * 1e3:8.1f} us [{ks}] same={ok}", flush=True)
+          f"{np.median(ts) * 1e3 / batch:8.1f} us/key [{ks}] same={ok}", flush=True)
     h.close()
