@@ -1333,6 +1333,7 @@ static uint32_t smem_k2(uint32_t N1, const FftPlan &p1) { return tile_bytes(N1) 
 struct PlanCand {
     double cost;
     uint32_t N1, N2, C;
+    double f[9];  // thr13, lat13, thr2, lat2, spec13, spec2, k1p, occ13, occ2 (calibration features)
 };
 constexpr int kMaxCand = 4096;
 static thread_local PlanCand g_cand[kMaxCand];
@@ -1406,10 +1407,22 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             // model preferring two-CTA C = 2 plans over faster K1P C = 4 ones without this)
             const bool k1p = spec13 && occ13 == 1 && C < 16 && N1 / C >= 2 * 148u && p2.S >= 3 &&
                              p2.st[p2.S - 1].R == 16;
+            // (a grid refit of the throughput scales on 70 random single-key lengths x 12 plans,
+            // tools/dev/plan_refit.py, cut the mean regret 2.9% -> 1.6% there but lost on held-out
+            // shapes and batches -- C5b batched 46.0 -> 48.2 us/key, n = 5e7, m = 1e7 1137 -> 1233
+            // us -- so the calibrated throughput terms stay as they are)
             const double t13 = f13 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C));
             double cost = t13 * (k1p ? 0.91 : 1.0) + t13 + f2 * ktime(pass2, ov2, occ2, (double)N2);
 #ifdef PA_DEV
-            if (g_cand_on && g_ncand < kMaxCand) g_cand[g_ncand++] = {cost, N1, N2, C};
+            if (g_cand_on && g_ncand < kMaxCand) {
+                const double th13 = M * pass13 * 0.62 * cfac * ov13 / sm_rate;
+                const double la13 = std::ceil((double)(N1 / C) / (148.0 * occ13)) * pass13 * 1.3e-6;
+                const double th2 = M * pass2 * 0.62 * ov2 / sm_rate;
+                const double la2 = std::ceil((double)N2 / (148.0 * occ2)) * pass2 * 1.3e-6;
+                g_cand[g_ncand++] = {cost, N1, N2, C, {th13, la13, th2, la2, spec13 ? 1.0 : 0.0,
+                                                       k2_shape(p1) ? 1.0 : 0.0, k1p ? 1.0 : 0.0,
+                                                       (double)occ13, (double)occ2}};
+            }
 #endif
             if (cost < best) {
                 best = cost;
@@ -1946,6 +1959,29 @@ extern "C" int pa_dev_plan_candidates(uint64_t n, uint64_t m, double *cost, uint
         n1[i] = g_cand[i].N1;
         n2[i] = g_cand[i].N2;
         c[i] = g_cand[i].C;
+    }
+    return k;
+}
+// the same candidates with the cost model's features, 13 doubles each:
+// cost, N1, N2, C, thr13, lat13, thr2, lat2, spec13, spec2, k1p, occ13, occ2
+extern "C" int pa_dev_plan_features(uint64_t n, uint64_t m, double *out, int max)
+{
+    using namespace pa;
+    Geometry g;
+    char err[256];
+    g_ncand = 0;
+    g_cand_on = true;
+    ra_plan(n, m, &g, err, sizeof err, 0);
+    g_cand_on = false;
+    std::sort(g_cand, g_cand + g_ncand, [](const PlanCand &a, const PlanCand &b) { return a.cost < b.cost; });
+    const int k = g_ncand < max ? g_ncand : max;
+    for (int i = 0; i < k; ++i) {
+        double *o = out + 13 * i;
+        o[0] = g_cand[i].cost;
+        o[1] = g_cand[i].N1;
+        o[2] = g_cand[i].N2;
+        o[3] = g_cand[i].C;
+        for (int j = 0; j < 9; ++j) o[4 + j] = g_cand[i].f[j];
     }
     return k;
 }

@@ -21,9 +21,10 @@ from paper_1805_02372_b200 import _lib  # noqa: E402
 count = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 rng = np.random.default_rng(int(sys.argv[3]) if len(sys.argv) > 3 else 1805)
-f = _lib._lib.pa_dev_plan_candidates
+f = _lib._lib.pa_dev_plan_features
 f.restype = ctypes.c_int
-f.argtypes = [ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 4 + [ctypes.c_int]
+f.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
+FEAT = ["thr13", "lat13", "thr2", "lat2", "spec13", "spec2", "k1p", "occ13", "occ2"]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
@@ -36,22 +37,25 @@ def words(w):
 for _ in range(count):
     n = int(np.exp(rng.uniform(np.log(1e6), np.log(1e8))))
     m = int(n * float(rng.choice([0.1, 0.2, 0.25])))
-    cost = (ctypes.c_double * 4096)()
-    n1, n2, c = (ctypes.c_uint32 * 4096)(), (ctypes.c_uint32 * 4096)(), (ctypes.c_uint32 * 4096)()
-    k = f(n, m, cost, n1, n2, c, 4096)
-    seen, cands = set(), []
-    for i in range(k):
-        key = (n1[i], n2[i], c[i])
+    buf = (ctypes.c_double * (13 * 4096))()
+    k = f(n, m, buf, 4096)
+    rows = [list(buf[13 * i:13 * i + 13]) for i in range(k)]
+    seen, uniq = set(), []
+    for r in rows:
+        key = (int(r[1]), int(r[2]), int(r[3]))
         if key not in seen:
             seen.add(key)
-            cands.append((cost[i], *key))
-        if len(cands) >= K:
-            break
+            uniq.append(r)
+    # the model's top K/2 plus K/2 drawn from ranks K/2..60 (diverse data for refits)
+    top = uniq[: K // 2]
+    rest = uniq[K // 2: 60]
+    pick = [rest[i] for i in sorted(rng.choice(len(rest), min(len(rest), K - len(top)), replace=False))]
+    cands = [(r[0], int(r[1]), int(r[2]), int(r[3]), dict(zip(FEAT, r[4:]))) for r in top + pick]
     sw, kw = syn.random_bits(syn.seed_stream(80), n + m - 1), syn.random_bits(syn.key_stream(80, 0), n)
     seed, key_t = words(sw), words(kw)
     res = []
     ref = None
-    for cst, a, b, cc in cands:
+    for cst, a, b, cc, feats in cands:
         os.environ["PA_FORCE_PLAN"] = f"{a},{b},{cc}"
         try:
             h = pa.Hasher(n, m, seed, route="transform")
@@ -72,7 +76,8 @@ for _ in range(count):
         o = out.cpu().numpy()[: (m + 31) // 32]
         same = True if ref is None else bool(np.array_equal(o, ref))
         ref = o if ref is None else ref
-        res.append({"plan": [a, b, cc], "model_us": cst * 1e6, "meas_us": float(np.median(ts)) * 1e3, "same": same})
+        res.append({"plan": [a, b, cc], "model_us": cst * 1e6, "meas_us": float(np.median(ts)) * 1e3, "same": same,
+                    "feat": feats})
         h.close()
     os.environ.pop("PA_FORCE_PLAN", None)
     print(json.dumps({"n": n, "m": m, "cands": res}), flush=True)
