@@ -279,9 +279,10 @@ pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t *seed_host
                                uint32_t *out_host, uint64_t max_block_bits, uint64_t device_budget_bytes,
                                void *stream);
 
-/* pa_hash_blocked / pa_hash_blocked_host keep their block handle (one per process, reused by
- * calls of the same block shape on the same device; calls are serialised) because creating and
- * freeing a multi-GB handle costs more than hashing a block.  This frees it. */
+/* pa_hash_blocked / pa_hash_blocked_host keep their block handle and staging buffers (one set per
+ * process, reused by calls of the same block shape on the same device; calls are serialised)
+ * because creating and freeing a multi-GB handle costs more than hashing a block.  This frees
+ * them. */
 void pa_hash_blocked_release(void);
 
 /* Modulo-2 addition of partial hashes (Eq. (7)): dst[w] = XOR over

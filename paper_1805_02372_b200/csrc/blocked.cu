@@ -88,6 +88,9 @@ static struct BlockCache {
     pa_handle h = nullptr;
     uint64_t nb = 0, mb = 0, off = 0;
     int device = -1;
+    uint32_t *stage = nullptr;  // staging slots + accumulators (reused when large enough)
+    size_t stage_bytes = 0;
+    int stage_device = -1;
 } g_bcache;
 
 // The block loop shared by the device- and host-resident entry points.
@@ -134,13 +137,31 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
     st.sw = ((off + nb + mb - 1 + 31) / 32 + 4 + 3) / 4 * 4;
     st.kw = (nb / 32 + 4 + 3) / 4 * 4;
     const uint64_t ow = (mb / 32 + 4 + 3) / 4 * 4;
-    uint32_t *blk = nullptr;
-    cudaError_t e = cudaMalloc(&blk, 4 * (2 * (st.sw + st.kw) + 3 * ow));
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        set_error("%s: staging allocation failed: %s", who, cudaGetErrorString(e));
-        return PA_ERR_NOMEM;
+    std::lock_guard<std::mutex> lock(g_bmutex);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t need = 4 * (2 * (st.sw + st.kw) + 3 * ow);
+    cudaError_t e = cudaSuccess;
+    if (!g_bcache.stage || g_bcache.stage_device != dev || g_bcache.stage_bytes < need) {
+        if (g_bcache.stage) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(g_bcache.stage_device);
+            cudaFree(g_bcache.stage);  // synchronous: no earlier call's copies still use it
+            cudaSetDevice(prev);
+            g_bcache.stage = nullptr;
+            g_bcache.stage_bytes = 0;
+        }
+        if ((e = cudaMalloc(&g_bcache.stage, need)) != cudaSuccess) {
+            cudaGetLastError();
+            g_bcache.stage = nullptr;
+            set_error("%s: staging allocation failed: %s", who, cudaGetErrorString(e));
+            return PA_ERR_NOMEM;
+        }
+        g_bcache.stage_bytes = need;
+        g_bcache.stage_device = dev;
     }
+    uint32_t *blk = g_bcache.stage;
     for (int i = 0; i < 2; ++i) {
         st.seed[i] = blk + i * (st.sw + st.kw);
         st.key[i] = st.seed[i] + st.sw;
@@ -148,15 +169,13 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
     uint32_t *tpart = blk + 2 * (st.sw + st.kw), *tacc[2] = {tpart + ow, tpart + 2 * ow};
     cudaStream_t cs = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_free[2] = {}, ev_acc[2] = {}, ev_out[2] = {};
-    std::lock_guard<std::mutex> lock(g_bmutex);
-    int dev = 0;
-    cudaGetDevice(&dev);
     pa_handle hb = nullptr;
     if (g_bcache.h && g_bcache.nb == nb && g_bcache.mb == mb && g_bcache.off == off && g_bcache.device == dev) {
         hb = g_bcache.h;
     } else if (g_bcache.h) {
         pa_destroy(g_bcache.h);
-        g_bcache = BlockCache{};
+        g_bcache.h = nullptr;
+        g_bcache.device = -1;
     }
     const bool fresh = hb == nullptr;
     pa_status res = PA_OK;
@@ -271,13 +290,14 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
     cudaStreamSynchronize(s);
     if (res != PA_OK && g_bcache.h) {  // a failed call does not leave a handle in an unknown state
         pa_destroy(g_bcache.h);
-        g_bcache = BlockCache{};
+        g_bcache.h = nullptr;
+        g_bcache.nb = g_bcache.mb = g_bcache.off = 0;
+        g_bcache.device = -1;
     }
     (void)fresh;
     for (int i = 0; i < 2; ++i)
         for (cudaEvent_t ev : {ev_in[i], ev_free[i], ev_acc[i], ev_out[i]})
             if (ev) cudaEventDestroy(ev);
-    cudaFree(blk);
     return res;
 }
 
@@ -344,11 +364,13 @@ extern "C" pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t
 extern "C" void pa_hash_blocked_release(void)
 {
     std::lock_guard<std::mutex> lock(g_bmutex);
-    if (g_bcache.h) {
-        int prev = 0;
-        cudaGetDevice(&prev);
-        pa_destroy(g_bcache.h);  // switches to the handle's device itself
-        cudaSetDevice(prev);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (g_bcache.h) pa_destroy(g_bcache.h);  // switches to the handle's device itself
+    if (g_bcache.stage) {
+        cudaSetDevice(g_bcache.stage_device);
+        cudaFree(g_bcache.stage);
     }
+    cudaSetDevice(prev);
     g_bcache = BlockCache{};
 }
