@@ -12,7 +12,7 @@ for c in C4 C3 C2; do
   ncu --set full --clock-control none --import-source on -k regex:"k[0123]p?_" -s 4 -c 4 -o gpurun_out/r2/prof_$c \
       python tools/prof_one.py $c 2 > gpurun_out/r2/ncu_$c.log 2>&1; echo "$c rc=$?"
 done
-python tools/prof_batch.py C1 65536 2 > gpurun_out/r2/plain_C1b.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_toeplitz_bitpacked" -s 1 -c 1 -o gpurun_out/r2/prof_C1_batched \
-    python tools/prof_batch.py C1 65536 2 > gpurun_out/r2/ncu_C1b.log 2>&1; echo "C1b rc=$?"
+python tools/prof_batch.py C1 65535 2 > gpurun_out/r2/plain_C1b.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_toeplitz_bitpacked" -s 1 -c 1 -f -o gpurun_out/r2/prof_C1_batched \
+    python tools/prof_batch.py C1 65535 2 > gpurun_out/r2/ncu_C1b.log 2>&1; echo "C1b rc=$?"
 ./tools/dev/tmp/dmma_bench > gpurun_out/r2/dmma.txt 2>&1; echo "dmma rc=$?"
