@@ -578,23 +578,27 @@ def sweep(torch, pa, dev, steps=10):
     # the metric's curve, Gbit/s vs input length n (m = n/10, the paper's ratio): single
     # keys, arbitrary non-power-of-two lengths from 10^6 to 10^8 bits
     curve = {}
-    for n in (1_000_003, 2_999_999, 10_000_019, 29_999_999, 100_000_007):
-        m = n // 10
+    # (each length planned by the cost model and by measurement, PA_PLAN_MEASURE)
+    for n in (1_000_003, 2_999_999, 10_000_019, 29_999_999, 53_164_100, 100_000_007):
+        m = n // 10 if n != 53_164_100 else n // 5
         sw = syn.random_bits(syn.seed_stream(70), n + m - 1)
         kw = syn.random_bits(syn.key_stream(70, n % 1000), n)
-        h = pa.Hasher(n, m, dev_words(torch, sw, dev))
         key = dev_words(torch, kw, dev)
-        out = h.new_out()
-        for _ in range(3):
-            h.hash(key, out)
-        t = float(np.mean(time_steps(torch, lambda: h.hash(key, out), max(steps, 10), flush)))
-        info = h.info
-        curve[str(n)] = {"m": m, "ms_per_hash": t, "gbit_s": n / (t * 1e-3) / 1e9,
-                         "hbm_frac_whole_hash": hash_bytes(n, m, info["n1"] * info["n2"]) / (t * 1e-3) / 1e9 / peak,
-                         "plan": f"{info['n1']}x{info['n2']} C={info['cols_per_cta']}",
-                         "verified_rows": verify_rows(n, m, sw, kw, out.cpu().numpy(), sampled_rows(m, 32))}
-        h.close()
-    res["length_curve_m_n_0.1"] = curve
+        e = {"m": m}
+        for plan in ("model", "measure"):
+            h = pa.Hasher(n, m, dev_words(torch, sw, dev), plan=plan)
+            out = h.new_out()
+            for _ in range(3):
+                h.hash(key, out)
+            t = float(np.mean(time_steps(torch, lambda: h.hash(key, out), max(steps, 10), flush)))
+            info = h.info
+            e[plan] = {"ms_per_hash": t, "gbit_s": n / (t * 1e-3) / 1e9,
+                       "hbm_frac_whole_hash": hash_bytes(n, m, info["n1"] * info["n2"]) / (t * 1e-3) / 1e9 / peak,
+                       "plan": f"{info['n1']}x{info['n2']} C={info['cols_per_cta']}",
+                       "verified_rows": verify_rows(n, m, sw, kw, out.cpu().numpy(), sampled_rows(m, 32))}
+            h.close()
+        curve[str(n)] = e
+    res["length_curve"] = curve
     # C5 (BASELINE configs[4]): distinct keys against one seed through pa_hash_batch
     for name in ("C5a", "C5b", "C5c", "C5d"):
         n, m, sw, _ = syn.config_inputs(name)

@@ -80,6 +80,16 @@ typedef enum pa_arith {
     PA_ARITH_NTT64 = 3
 } pa_arith;
 
+/* How route (a) picks its transform plan (N1 x N2 split, column-group width).  MODEL: the
+ * planner's cost model (host-only, what pa_plan reports).  MEASURE: the model's best few
+ * candidates are built and timed on the device at create (FFTW-style), the fastest kept and
+ * remembered per (n, m, max_transform_len, device) for the life of the process; create then
+ * synchronises `stream`.  Ignored by route (b), split handles and caller workspaces. */
+typedef enum pa_plan_mode {
+    PA_PLAN_MODEL = 0,
+    PA_PLAN_MEASURE = 1
+} pa_plan_mode;
+
 #define PA_RESIDUAL_LIMIT 0.25
 
 typedef struct pa_options {
@@ -107,7 +117,7 @@ typedef struct pa_options {
                                  later call on the handle runs on it (the library switches to it
                                  for the call and back); seed, keys, outputs and workspace must
                                  live there and `stream` must belong to it */
-    uint32_t reserved[1];     /* must be zero */
+    uint32_t plan_mode;       /* pa_plan_mode: MODEL (default) or MEASURE */
 } pa_options;
 
 /* Runtime facts about a handle (all lengths in bits or elements). */

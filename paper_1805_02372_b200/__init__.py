@@ -19,7 +19,8 @@ from __future__ import annotations
 import torch  # loads the CUDA runtime that libpa.so binds to
 
 from . import _lib
-from ._lib import (PA_ARITH_AUTO, PA_ARITH_FP64, PA_ARITH_NTT32, PA_ARITH_NTT64,  # noqa: F401
+from ._lib import (PA_ARITH_AUTO, PA_ARITH_FP64, PA_ARITH_NTT32, PA_ARITH_NTT64, PA_PLAN_MEASURE,  # noqa: F401
+                   PA_PLAN_MODEL,
                    PA_ERR_CUDA, PA_ERR_INVALID_ARG, PA_ERR_NOMEM, PA_ERR_PRECISION,  # noqa: F401
                    PA_ERR_UNSUPPORTED, PA_OK, PA_RESIDUAL_LIMIT, PA_ROUTE_AUTO, PA_ROUTE_BITPACKED,
                    PA_ROUTE_TRANSFORM, PaError, pa_create, pa_create_ex, pa_create_u64, pa_destroy,
@@ -56,9 +57,11 @@ def _need_cuda(t: torch.Tensor, name: str, nbits: int) -> None:
 
 
 def make_options(route: str = "auto", seed_bit_offset: int = 0, allow_wide: bool = False, batch_keys: int = 0,
-                 max_transform_len: int = 0, device: int = -1, arith: int = PA_ARITH_AUTO):
-    """pa_options from keyword arguments (see include/pa.h for each field)."""
+                 max_transform_len: int = 0, device: int = -1, arith: int = PA_ARITH_AUTO, plan: str = "model"):
+    """pa_options from keyword arguments (see include/pa.h for each field); plan = "model" or
+    "measure" (PA_PLAN_MEASURE: time the planner's best candidates at create)."""
     opt = pa_options_init()
+    opt.plan_mode = {"model": PA_PLAN_MODEL, "measure": PA_PLAN_MEASURE}[plan]
     opt.device = int(device)
     opt.arith = int(arith)
     opt.route = ROUTES[route]
@@ -97,13 +100,13 @@ class Hasher:
 
     def __init__(self, n: int, m: int, seed: torch.Tensor, route: str = "auto",
                  seed_bit_offset: int = 0, stream=None, allow_wide: bool = False, batch_keys: int = 0,
-                 max_transform_len: int = 0, workspace: torch.Tensor | None = None):
+                 max_transform_len: int = 0, workspace: torch.Tensor | None = None, plan: str = "model"):
         _need_cuda(seed, "seed", seed_bit_offset + n + m - 1)
         self.n, self.m = int(n), int(m)
         self.seed_bit_offset = int(seed_bit_offset)
         self.device = seed.device
         opt = make_options(route, seed_bit_offset, allow_wide, batch_keys, max_transform_len,
-                           device=seed.device.index if seed.device.index is not None else -1)
+                           device=seed.device.index if seed.device.index is not None else -1, plan=plan)
         self._ws = workspace
         with torch.cuda.device(self.device):
             if workspace is None:

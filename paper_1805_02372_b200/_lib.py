@@ -28,6 +28,7 @@ PA_ROUTE_AUTO = 0
 PA_ROUTE_TRANSFORM = 1
 PA_ROUTE_BITPACKED = 2
 PA_ARITH_AUTO, PA_ARITH_FP64, PA_ARITH_NTT32, PA_ARITH_NTT64 = 0, 1, 2, 3
+PA_PLAN_MODEL, PA_PLAN_MEASURE = 0, 1
 PA_RESIDUAL_LIMIT = 0.25
 
 EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_batch",
@@ -53,7 +54,7 @@ class pa_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("route", ctypes.c_int32),
                 ("seed_bit_offset", ctypes.c_uint64), ("allow_wide", ctypes.c_uint32),
                 ("batch_keys", ctypes.c_uint32), ("max_transform_len", ctypes.c_uint64),
-                ("arith", ctypes.c_int32), ("device", ctypes.c_int32), ("reserved", ctypes.c_uint32 * 1)]
+                ("arith", ctypes.c_int32), ("device", ctypes.c_int32), ("plan_mode", ctypes.c_uint32)]
 
 
 class pa_info(ctypes.Structure):

@@ -5,7 +5,11 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
 #include <new>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -334,15 +338,15 @@ static pa_status parse_options(const pa_options *opt, uint64_t n, uint64_t m, pa
         set_error("opt->arith = %d is not a pa_arith", o->arith);
         return PA_ERR_INVALID_ARG;
     }
+    if (o->plan_mode > PA_PLAN_MEASURE) {
+        set_error("opt->plan_mode = %u is not a pa_plan_mode", o->plan_mode);
+        return PA_ERR_INVALID_ARG;
+    }
     if (o->device < -1) {
         set_error("opt->device = %d: use -1 (current device) or a CUDA device ordinal", o->device);
         return PA_ERR_INVALID_ARG;
     }
-    for (int i = 0; i < 1; ++i)
-        if (o->reserved[i]) {
-            set_error("opt->reserved[%d] = %u must be 0", i, o->reserved[i]);
-            return PA_ERR_INVALID_ARG;
-        }
+
     if (o->route == PA_ROUTE_AUTO) o->route = choose_route(n, m);
     return PA_OK;
 }
@@ -435,8 +439,12 @@ static pa_status handle_bytes(uint64_t n, uint64_t m, const pa_options &o, bool 
     return PA_OK;
 }
 
+static pa_status measure_plan(uint64_t n, uint64_t m, const uint32_t *seed_bits, const pa_options &o,
+                              cudaStream_t s, PlanChoice *best);
+
 static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint32_t *seed_bits,
-                             const pa_options *opt, void *workspace, uint64_t workspace_bytes, void *stream)
+                             const pa_options *opt, void *workspace, uint64_t workspace_bytes, void *stream,
+                             const PlanChoice *force = nullptr)
 {
     if (!out) {
         set_error("h (output handle pointer) is NULL");
@@ -468,6 +476,13 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
     }
     std::vector<uint64_t> c0;
     if (o.route == PA_ROUTE_TRANSFORM && (st = split_plan(n, m, o.max_transform_len, &c0)) != PA_OK) return st;
+    // measured planning (PA_PLAN_MEASURE): an unsplit route-(a) handle without a caller workspace
+    // (whose size pa_workspace_size fixed from the model's plan) times the model's best candidates
+    PlanChoice measured;
+    if (!force && o.plan_mode == PA_PLAN_MEASURE && o.route == PA_ROUTE_TRANSFORM && c0.size() == 1 && !workspace) {
+        if ((st = measure_plan(n, m, seed_bits, o, (cudaStream_t)stream, &measured)) != PA_OK) return st;
+        if (measured.N1) force = &measured;
+    }
 
     pa_ctx *h = new (std::nothrow) pa_ctx();
     if (!h) {
@@ -482,6 +497,10 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
     h->route = o.route;
     h->batch_opt = o.batch_keys;
     h->max_len = o.route == PA_ROUTE_TRANSFORM ? o.max_transform_len : 0;
+    if (force && c0.size() == 1) {
+        h->force = *force;
+        h->has_force = true;
+    }
     if (o.route == PA_ROUTE_TRANSFORM && c0.size() > 1 && !h->max_len) h->max_len = kMaxPlanLen;  // auto split
     if (workspace) {
         h->arena = new (std::nothrow) Arena();
@@ -548,6 +567,105 @@ static pa_status create_impl(pa_handle *out, uint64_t n, uint64_t m, const uint3
         return st;
     }
     *out = h;
+    return PA_OK;
+}
+
+// Measured planning: the model's best few candidate plans, each built as a real handle on the
+// caller's seed and timed on an all-zero key (route (a)'s time is independent of the data) after
+// an L2 flush, median of five (a challenger must beat the model's pick by 2%); the fastest is
+// remembered per (n, m, max_transform_len, device)
+// for the life of the process (FFTW-style "wisdom"), so later handles of the shape skip it.
+static std::mutex g_wisdom_mutex;
+static std::map<std::tuple<uint64_t, uint64_t, uint64_t, int>, PlanChoice> g_wisdom;
+
+static pa_status measure_plan(uint64_t n, uint64_t m, const uint32_t *seed_bits, const pa_options &o,
+                              cudaStream_t s, PlanChoice *best)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(n, m, (uint64_t)o.max_transform_len, dev);
+    {
+        std::lock_guard<std::mutex> lock(g_wisdom_mutex);
+        auto it = g_wisdom.find(key);
+        if (it != g_wisdom.end()) {
+            *best = it->second;
+            return PA_OK;
+        }
+    }
+    constexpr int kCand = 6;
+    PlanChoice cand[kCand];
+    const int k = ra_plan_candidates(n, m, o.max_transform_len, cand, kCand);
+    *best = PlanChoice{};
+    if (k <= 1) {
+        if (k == 1) *best = cand[0];
+        return PA_OK;
+    }
+    uint32_t *key_bits = nullptr, *out_bits = nullptr;
+    void *flush = nullptr;
+    const size_t kb = ((n + 31) / 32 + 4) * 4, ob = ((m + 31) / 32 + 4) * 4, fb = 256u << 20;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&key_bits, kb)) != cudaSuccess || (e = cudaMalloc(&out_bits, ob)) != cudaSuccess ||
+        (e = cudaMemsetAsync(key_bits, 0, kb, s)) != cudaSuccess || (e = cudaEventCreate(&e0)) != cudaSuccess ||
+        (e = cudaEventCreate(&e1)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(key_bits);
+        cudaFree(out_bits);
+        if (e0) cudaEventDestroy(e0);
+        return cuda_fail(e, "measured planning scratch");
+    }
+    if (cudaMalloc(&flush, fb) != cudaSuccess) {  // no room for an L2 flush: time warm
+        cudaGetLastError();
+        flush = nullptr;
+    } else {
+        cudaMemsetAsync(flush, 0, fb, s);  // first touch outside the timings
+    }
+    pa_options oo = o;
+    oo.plan_mode = PA_PLAN_MODEL;
+    float best_ms = 3.4e38f;
+    for (int i = 0; i < k; ++i) {
+        pa_handle t = nullptr;
+        if (create_impl(&t, n, m, seed_bits, &oo, nullptr, 0, s, &cand[i]) != PA_OK) {
+            cudaGetLastError();
+            continue;  // e.g. out of memory for a larger candidate: skip it
+        }
+        float ms[5];
+        pa_status st = pa_hash(t, key_bits, out_bits, s);  // warm-up (code, tables)
+        if (st == PA_OK) st = pa_hash(t, key_bits, out_bits, s);
+        for (int r = 0; r < 5 && st == PA_OK; ++r) {
+            if (flush) cudaMemsetAsync(flush, 0, fb, s);
+            cudaEventRecord(e0, s);
+            st = pa_hash(t, key_bits, out_bits, s);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms[r], e0, e1);
+        }
+        pa_destroy(t);
+        if (st != PA_OK) continue;
+        std::sort(ms, ms + 5);
+#ifdef PA_DEV
+        if (dev_env("PA_PLAN_DEBUG"))
+            fprintf(stderr, "measure_plan n=%llu m=%llu cand %d: %ux%u C=%u median %.2f us (min %.2f max %.2f)\n",
+                    (unsigned long long)n, (unsigned long long)m, i, cand[i].N1, cand[i].N2, cand[i].C, ms[2] * 1e3,
+                    ms[0] * 1e3, ms[4] * 1e3);
+#endif
+        // a challenger must beat the incumbent by 2% (measurement noise must not trade the
+        // model's choice for an equal plan)
+        if (ms[2] < best_ms * (best->N1 ? 0.98f : 1.0f)) {
+            best_ms = ms[2];
+            *best = cand[i];
+        }
+    }
+    cudaStreamSynchronize(s);
+    cudaFree(key_bits);
+    cudaFree(out_bits);
+    if (flush) cudaFree(flush);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (best->N1) {
+        std::lock_guard<std::mutex> lock(g_wisdom_mutex);
+        g_wisdom[key] = *best;
+    }
     return PA_OK;
 }
 

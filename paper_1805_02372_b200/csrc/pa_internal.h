@@ -49,6 +49,11 @@ struct Geometry {
     int k13;                // K1/K3 instantiation (route_a.cu kK13), 0: general
 };
 
+// a route-(a) plan: rows of N1 points, N2 rows, C columns per K1 CTA
+struct PlanChoice {
+    uint32_t N1 = 0, N2 = 0, C = 0;
+};
+
 struct RouteTables {
     double2 *W1lo, *W1hi;   // omega_N1^e = W1hi[e >> 6] * W1lo[e & 63]
     double2 *W2lo, *W2hi;   // omega_N2^e
@@ -139,6 +144,8 @@ struct pa_ctx {
     uint64_t *sub_c0 = nullptr;  // first key bit of each block (multiple of 128)
     uint32_t nsub = 0;
     uint64_t max_len = 0;        // pa_options.max_transform_len (route (a) planning cap)
+    pa::PlanChoice force;        // a measured plan (PA_PLAN_MEASURE) replacing the model's
+    bool has_force = false;
     char *share_w = nullptr;     // column blocks 1..: the first block's work block, if large enough
     size_t share_w_bytes = 0;
     // pa_hash_host as one CUDA graph (H2D, kernels, D2H); host pointers patched per call
@@ -163,7 +170,10 @@ namespace pa {
 
 // route (a)
 // max_len: cap on the real transform length 2 M (0 = none), pa_options.max_transform_len
-pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len = 0);
+pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len = 0,
+                  const PlanChoice *force = nullptr);
+// the cost model's distinct candidate plans, cheapest first (PA_PLAN_MEASURE)
+int ra_plan_candidates(uint64_t n, uint64_t m, uint64_t max_len, PlanChoice *out, int max);
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_words,

@@ -921,14 +921,35 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
 }
 
 // the shapes k2_rows_t is instantiated for (g.k2shape: 0 = general k2_rows)
+// shape-specialised K2 instantiations: rows [R0, R1, 16, ...] with NS stages (kK2[0] = general)
+using K2Fn = void (*)(double2 *, double2 *, const double2 *, Geometry, RouteTables, uint64_t);
+struct K2Shape {
+    int a, b, s;
+    K2Fn fn;
+};
+static const K2Shape kK2[] = {
+    {0, 0, 0, nullptr},
+    {16, 16, 3, k2_rows_t<16, 16, 3>},  // 4096 (C2, C3, C5a-c)
+    {5, 8, 4, k2_rows_t<5, 8, 4>},      // 10240 (C4, C5d)
+    {3, 8, 4, k2_rows_t<3, 8, 4>},      // 6144
+    {7, 4, 4, k2_rows_t<7, 4, 4>},      // 7168
+    {2, 16, 4, k2_rows_t<2, 16, 4>},    // 8192 (round 2: the calibration sweep's worst misses)
+    {3, 16, 4, k2_rows_t<3, 16, 4>},    // 12288
+    {7, 5, 4, k2_rows_t<7, 5, 4>},      // 8960
+    {5, 4, 4, k2_rows_t<5, 4, 4>},      // 5120
+    {8, 16, 3, k2_rows_t<8, 16, 3>},    // 2048
+    {3, 4, 4, k2_rows_t<3, 4, 4>},      // 3072
+};
+
 static int k2_shape(const FftPlan &p)
 {
     if (p.S < 3) return 0;
     for (int i = 2; i < p.S; ++i)
         if (p.st[i].R != 16) return 0;
-    const uint32_t a = p.st[0].R, b = p.st[1].R;  // the stage count is a template parameter too
-    return a == 16 && b == 16 && p.S == 3 ? 1 : a == 5 && b == 8 && p.S == 4 ? 2 : a == 3 && b == 8 && p.S == 4 ? 3
-           : a == 7 && b == 4 && p.S == 4 ? 4 : 0;
+    const int a = (int)p.st[0].R, b = (int)p.st[1].R;  // the stage count is a template parameter too
+    for (int k = 1; k < (int)(sizeof kK2 / sizeof kK2[0]); ++k)
+        if (kK2[k].a == a && kK2[k].b == b && kK2[k].s == p.S) return k;
+    return 0;
 }
 
 
@@ -1328,20 +1349,31 @@ static uint32_t smem_k13(uint32_t N2, uint32_t C, const FftPlan &p2)
 }
 static uint32_t smem_k2(uint32_t N1, const FftPlan &p1) { return tile_bytes(N1) + (2 * (64 + p1.nhi) + p1.ntw) * 16; }
 
-#ifdef PA_DEV
-// developer build: every candidate plan the cost model scored (pa_dev_plan_candidates)
+// every candidate plan the cost model scored (ra_plan_candidates: measured planning,
+// PA_PLAN_MEASURE; pa_dev_plan_features in the developer build)
 struct PlanCand {
     double cost;
     uint32_t N1, N2, C;
     double f[9];  // thr13, lat13, thr2, lat2, spec13, spec2, k1p, occ13, occ2 (calibration features)
 };
-constexpr int kMaxCand = 4096;
+constexpr int kMaxCand = 256;  // the cheapest kMaxCand candidates (a plan search scores thousands)
 static thread_local PlanCand g_cand[kMaxCand];
 static thread_local int g_ncand = 0;
 static thread_local bool g_cand_on = false;
-#endif
+static void keep_cand(const PlanCand &c)
+{
+    if (g_ncand < kMaxCand) {
+        g_cand[g_ncand++] = c;
+        return;
+    }
+    int worst = 0;
+    for (int i = 1; i < kMaxCand; ++i)
+        if (g_cand[i].cost > g_cand[worst].cost) worst = i;
+    if (c.cost < g_cand[worst].cost) g_cand[worst] = c;
+}
 
-pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len)
+pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len,
+                  const PlanChoice *force)
 {
     const uint64_t L = n + m - 1;
     const uint64_t Mmin = (L + 1) / 2;
@@ -1413,17 +1445,14 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             // us -- so the calibrated throughput terms stay as they are)
             const double t13 = f13 * ktime(pass13, cfac * ov13, occ13, (double)(N1 / C));
             double cost = t13 * (k1p ? 0.91 : 1.0) + t13 + f2 * ktime(pass2, ov2, occ2, (double)N2);
-#ifdef PA_DEV
-            if (g_cand_on && g_ncand < kMaxCand) {
+            if (g_cand_on) {
                 const double th13 = M * pass13 * 0.62 * cfac * ov13 / sm_rate;
                 const double la13 = std::ceil((double)(N1 / C) / (148.0 * occ13)) * pass13 * 1.3e-6;
                 const double th2 = M * pass2 * 0.62 * ov2 / sm_rate;
                 const double la2 = std::ceil((double)N2 / (148.0 * occ2)) * pass2 * 1.3e-6;
-                g_cand[g_ncand++] = {cost, N1, N2, C, {th13, la13, th2, la2, spec13 ? 1.0 : 0.0,
-                                                       k2_shape(p1) ? 1.0 : 0.0, k1p ? 1.0 : 0.0,
-                                                       (double)occ13, (double)occ2}};
+                keep_cand({cost, N1, N2, C, {th13, la13, th2, la2, spec13 ? 1.0 : 0.0, k2_shape(p1) ? 1.0 : 0.0,
+                                             k1p ? 1.0 : 0.0, (double)occ13, (double)occ2}});
             }
-#endif
             if (cost < best) {
                 best = cost;
                 found = true;
@@ -1435,12 +1464,12 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         }
         }
     }
-    // developer override for plan experiments: PA_FORCE_PLAN="N1,N2,C"
-    if (const char *fp = dev_env("PA_FORCE_PLAN")) {
-        unsigned f1 = 0, f2 = 0, fc = 0;
+    // a plan chosen by measurement (PA_PLAN_MEASURE, pa_api.cu) or the developer override
+    // PA_FORCE_PLAN="N1,N2,C" replaces the model's choice when it is valid for (n, m)
+    auto apply_force = [&](unsigned f1, unsigned f2, unsigned fc) {
         FftPlan q1, q2;
-        if (sscanf(fp, "%u,%u,%u", &f1, &f2, &fc) == 3 && (uint64_t)f1 * f2 >= Mmin && fc >= 1 &&
-            fc <= 16 && (fc & (fc - 1)) == 0 && f1 % fc == 0 && make_plan(f1, &q1) && make_plan(f2, &q2) &&
+        if ((uint64_t)f1 * f2 >= Mmin && fc >= 1 && fc <= 16 && (fc & (fc - 1)) == 0 && f1 % fc == 0 &&
+            (!max_len || 2ull * f1 * f2 <= max_len) && make_plan(f1, &q1) && make_plan(f2, &q2) &&
             smem_k2(f1, q1) <= kSmemLimit && smem_k13(f2, fc, q2) <= kSmemLimit) {
             g->N1 = f1;
             g->N2 = f2;
@@ -1448,6 +1477,11 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             g->M = (uint64_t)f1 * f2;
             found = true;
         }
+    };
+    if (force) apply_force(force->N1, force->N2, force->C);
+    if (const char *fp = dev_env("PA_FORCE_PLAN")) {
+        unsigned f1 = 0, f2 = 0, fc = 0;
+        if (sscanf(fp, "%u,%u,%u", &f1, &f2, &fc) == 3) apply_force(f1, f2, fc);
     }
     if (!found) {
         snprintf(err, errlen,
@@ -1655,7 +1689,7 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 {
     char err[256];
     Geometry &g = h->a.g;
-    pa_status st = ra_plan(h->n, h->m, &g, err, sizeof err, h->max_len);
+    pa_status st = ra_plan(h->n, h->m, &g, err, sizeof err, h->max_len, h->has_force ? &h->force : nullptr);
     if (st != PA_OK) {
         set_error("%s", err);
         return st;
@@ -1732,17 +1766,14 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
     if (
         (e = cudaFuncSetAttribute(k2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<16, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<5, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<3, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k2_rows_t<7, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemLimit)) != cudaSuccess ||
+
         (e = cudaFuncSetAttribute(k3t_inv_columns, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
+    for (const K2Shape &f : kK2)
+        if (f.fn && (e = cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
+                        cudaSuccess)
+            return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     attr_done.fetch_or(bit);
 launch:
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
@@ -1839,13 +1870,10 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         const dim3 g2(count, g.N2);
         const double2 *sp = spec ? spec : a.spec;  // fresh seeds: one spectrum per key
         const uint64_t ss = spec ? spec_stride : 0;
-        switch (g.k2shape) {
-        case 1: launch_pdl(k2_rows_t<16, 16, 3>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        case 2: launch_pdl(k2_rows_t<5, 8, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        case 3: launch_pdl(k2_rows_t<3, 8, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        case 4: launch_pdl(k2_rows_t<7, 4, 4>, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss); break;
-        default: launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
-        }
+        if (g.k2shape)
+            launch_pdl(kK2[g.k2shape].fn, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss);
+        else
+            launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
     }
     prof_end(h, s);
     prof_begin(h, 2, s);
@@ -1937,6 +1965,33 @@ void ra_destroy(pa_ctx *h)
     a = RouteA{};
 }
 
+}  // namespace pa
+
+namespace pa {
+// The cost model's distinct candidate plans for (n, m), cheapest first (measured planning).
+int ra_plan_candidates(uint64_t n, uint64_t m, uint64_t max_len, PlanChoice *out, int max)
+{
+    Geometry g;
+    char err[256];
+    g_ncand = 0;
+    g_cand_on = true;
+    ra_plan(n, m, &g, err, sizeof err, max_len);
+    g_cand_on = false;
+    std::sort(g_cand, g_cand + g_ncand, [](const PlanCand &a, const PlanCand &b) { return a.cost < b.cost; });
+    int k = 0;
+    for (int i = 0; i < g_ncand && k < max; ++i) {
+        bool dup = false;
+        for (int j = 0; j < k; ++j)
+            dup |= out[j].N1 == g_cand[i].N1 && out[j].N2 == g_cand[i].N2 && out[j].C == g_cand[i].C;
+        if (!dup) {
+            out[k].N1 = g_cand[i].N1;
+            out[k].N2 = g_cand[i].N2;
+            out[k].C = g_cand[i].C;
+            ++k;
+        }
+    }
+    return k;
+}
 }  // namespace pa
 
 #ifdef PA_DEV

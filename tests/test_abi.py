@@ -170,10 +170,10 @@ def test_option_and_pointer_errors_before_device_work():
         pa.workspace_size(100, 10, batch_keys=5000)
     assert e.value.status == pa.PA_ERR_INVALID_ARG and "batch_keys" in pa.pa_last_error()
     o = pa.make_options()
-    o.reserved[0] = 7
+    o.plan_mode = 7
     with pytest.raises(pa.PaError) as e:
         pa.pa_workspace_size(100, 10, o)
-    assert e.value.status == pa.PA_ERR_INVALID_ARG and "reserved[0]" in pa.pa_last_error()
+    assert e.value.status == pa.PA_ERR_INVALID_ARG and "plan_mode" in pa.pa_last_error()
     # SURVEY 8(b) pa_options.arith: FP64 is the built arithmetic, the NTTs are refused by name
     for a, ok in ((pa.PA_ARITH_AUTO, True), (pa.PA_ARITH_FP64, True), (pa.PA_ARITH_NTT32, False),
                   (pa.PA_ARITH_NTT64, False), (9, False)):

@@ -1079,3 +1079,28 @@ def test_blocked_host_4gbit_under_16gib_budget():
     d = np.bitwise_xor(lo[: m - 1], hi[: m - 1])
     want = np.concatenate([[y0], np.bitwise_xor.accumulate(d) ^ y0]).astype(np.uint8)
     assert np.array_equal(got_ones, want)
+
+
+@pytest.mark.parametrize("n,m", [(1_067_928, 266_982), (300_007, 60_001), (1_000_003, 250_000)])
+def test_measured_planning(n, m):
+    """PA_PLAN_MEASURE: the planner's best candidates are built and timed at create and the
+    fastest kept (remembered per shape): the hash stays bit-exact against the oracle, the plan is
+    a valid split of a transform >= n + m - 1, and a second handle of the shape reuses it."""
+    import time
+    sw = syn.random_bits(syn.seed_stream(181), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(181, 0), n)
+    seed = to_dev(sw)
+    with pa.Hasher(n, m, seed, route="transform", plan="measure") as h:
+        info = h.info
+        got = from_dev(h.hash(to_dev(kw)), m)
+        torch.cuda.synchronize()
+        assert h.residual() < 1e-3
+    assert info["transform_len"] >= n + m - 1 and info["n1"] * info["n2"] * 2 == info["transform_len"]
+    assert np.array_equal(got, oracle.unpack(oracle.toeplitz_words(n, m, sw, kw), m))
+    t0 = time.perf_counter()
+    with pa.Hasher(n, m, seed, route="transform", plan="measure") as h2:
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        assert (h2.info["n1"], h2.info["n2"], h2.info["cols_per_cta"]) == (info["n1"], info["n2"],
+                                                                          info["cols_per_cta"])
+    assert dt < 0.5  # remembered: no second round of trial handles
