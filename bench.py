@@ -68,6 +68,13 @@ def parse_args():
     return ap.parse_args()
 
 
+def config_dict(name, n, m):
+    """The workload, identical in both arms' lines (the driver compares them)."""
+    return {"workload": workload_desc(name), "n": n, "m": m,
+            "l2": "GPU arm: L2 flushed before every timed step (256 MiB memset, untimed) and the C4 "
+                  "working set (2 GB) exceeds L2"}
+
+
 def workload_desc(name):
     c = syn.CONFIGS[name]
     return f"{name}: {c['desc']} (n={c['n']}, m={c['m']})"
@@ -438,7 +445,7 @@ def run_ours(args):
             "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits (SURVEY 8(d) streams)",
             # config: the same keys as the reference arm's line (the workload); how it ran is in
             # "plan" / "parallelism"
-            "config": {"workload": workload_desc(name), "n": n, "m": m},
+            "config": config_dict(name, n, m),
             "plan": {"route": h.route, "transform_len": info["transform_len"], "n1": info["n1"], "n2": info["n2"],
                      "cols_per_cta": info["cols_per_cta"], "split": split,
                      "l2": "flushed before every step (256 MiB memset, untimed); working set > L2",
@@ -757,7 +764,7 @@ def run_reference(args):
             "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u64",
             "impl": "reference",
             "data": "synthetic: SplitMix64 i.i.d. Bernoulli(1/2) key and seed bits",
-            "config": {"workload": workload_desc(name), "n": n, "m": m},
+            "config": config_dict(name, n, m),
             "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
