@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(PA_TMAX, 1)
 k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geometry g, RouteTables T,
                 uint32_t *__restrict__ zero_out, uint64_t zero_words, uint64_t out_stride, uint32_t count)
 {
+    const uint32_t tcols = g.k1p_tcols;  // 512 (one CTA per SM) or 256 (two)
     extern __shared__ double2 sm[];
     __shared__ uint32_t tm_base;
     const uint32_t logC = g.logC, C = 1u << logC;
@@ -637,8 +638,8 @@ k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geom
     if (kBits)
         for (uint32_t i = threadIdx.x; i < g.ntb; i += blockDim.x) cp_async16(tb + i, T.tb + i);
     if (threadIdx.x < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&tm_base)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tm_base)), "r"(tcols) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     grid_dep_wait();  // K0's bit streams
@@ -699,7 +700,7 @@ k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geom
     grid_dep_launch();  // K2 may start its prologue
     if (prev) k1p_drain(prev, g.N1, nb_last, logC, tm, kmax, 0, nchunks);
     cta_sync_tmem();
-    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(tcols) : "memory");
 }
 
 // ------------------------------------------------------------------ K2
@@ -1609,11 +1610,18 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const char *et = dev_env("PA_K1P_T");  // developer override of K1P's threads (multiple of 128)
         const int tv = et ? atoi(et) : 0;
         g->k1p_t = tv >= 256 && tv <= PA_TMAX && tv % 128 == 0 ? (uint32_t)tv : PA_TMAX;
+        // two CTAs per SM (256 threads, 256 TMEM columns each) when the tiles are small enough --
+        // developer opt-in PA_K1P2=1 while it is measured
+        const char *e2 = dev_env("PA_K1P2");
+        const bool two = e2 && atoi(e2) == 1 && g->t1 == PA_TMAX / 2 && 2 * (g->smem1p + 64) <= kSmemLimit;
+        if (two) g->k1p_t = PA_TMAX / 2;
+        g->k1p_tcols = two ? 256u : 512u;
         const uint32_t nbl = g->f2.S ? (g->f2.st[g->f2.S - 1].nb << g->logC) : 0;
         const uint32_t kmax = (nbl + g->k1p_t - 1) / g->k1p_t;
-        if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 3 && g->f2.st[g->f2.S - 1].R == 16 && g->t1 == PA_TMAX &&
-            g->C < 16 && kmax >= 1 && (g->k1p_t / 128) * kmax * 64 <= 512 && g->smem1p + 64 <= kSmemLimit &&
-            g->N1 / g->C >= 2 * 148u)
+        if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 3 && g->f2.st[g->f2.S - 1].R == 16 &&
+            (g->t1 == PA_TMAX || two) && g->C < 16 && kmax >= 1 &&
+            (g->k1p_t / 128) * kmax * 64 <= g->k1p_tcols && g->smem1p + 64 <= kSmemLimit &&
+            g->N1 / g->C >= 2 * 148u * (two ? 2u : 1u))
             g->k1p_kmax = kmax;
     }
     g->C3 = g->C;
@@ -1858,7 +1866,8 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
     prof_begin(h, 0, s);
     if (g.k1p_kmax && !direct) {
         const uint32_t tiles = (g.N1 / g.C) * count;
-        launch_pdl(kK13[g.k13].k1p, dim3(tiles < 148 ? tiles : 148), dim3(g.k1p_t), g.smem1p, s,
+        const uint32_t slots = g.k1p_tcols == 256 ? 2 * 148 : 148;
+        launch_pdl(kK13[g.k13].k1p, dim3(tiles < slots ? tiles : slots), dim3(g.k1p_t), g.smem1p, s,
                    (const uint32_t *)a.kb, a.buf, g, a.T, outs, zero_words, out_stride, count);
     } else {
         launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, a.kb, a.buf, g, a.T, outs, zero_words,
