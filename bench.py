@@ -632,8 +632,12 @@ def sweep(torch, pa, dev, steps=10):
     keys = c5_keys(torch, "C1", count, dev)
     outs = h.new_out(count)
     t = time_batch(torch, h, keys, outs, flush, reps=3) / count
+    ok = True
+    for k in (0, 65534, count - 1):  # both launches of the batch (65535 keys per grid)
+        kw = syn.random_bits(syn.key_stream(syn.CONFIG_INDEX["C1"], k), n)
+        ok &= verify_rows(n, m, sw, kw, outs[k].cpu().numpy(), np.arange(m, dtype=np.uint64))
     res["C1_batched"] = {"n": n, "m": m, "keys": count, "distinct_keys": True, "route": h.route,
-                         "us_per_key": t * 1e3, "gbit_s": n / (t * 1e-3) / 1e9}
+                         "us_per_key": t * 1e3, "gbit_s": n / (t * 1e-3) / 1e9, "verified_rows": ok}
     h.close()
     # C5a end to end from pinned host memory (pa_hash_host_batch: H2D / batched hash / D2H of
     # neighbouring chunks overlapped), 1024 distinct keys
