@@ -375,11 +375,15 @@ __device__ __forceinline__ void dit_t(double2 *sm, const FftPlan &P, int i0, int
 // butterfly (column c, j < Ls) the R real and R imaginary bits of rows j + r Ls index the table,
 // v_k = theta_j (T[p_re][k] + i T[p_im][k]) * w_N2^{jk}, written where stage 0 writes.  Replaces
 // the z generation pass and stage 0's DFT.
-template <int R>
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+// Hook: called once per butterfly iteration (K1P drains a piece of the previous tile there)
+template <int R, typename Hook = NoHook>
 __device__ __forceinline__ void k1_first_stage_bits(double2 *sm, const StageDesc &sd, uint32_t logC,
                                                     const uint32_t *rowbits, const double2 *tb,
                                                     const double2 *thlo, const double2 *thhi,
-                                                    const double2 *wlo, const double2 *whi)
+                                                    const double2 *wlo, const double2 *whi, Hook hook = Hook{})
 {
     const uint32_t C = 1u << logC, twoC = 2 * C, epw = 32 / twoC;
     const uint32_t nb = sd.nb << logC, cm = C - 1, stride = sd.Ls << logC;
@@ -404,6 +408,7 @@ __device__ __forceinline__ void k1_first_stage_bits(double2 *sm, const StageDesc
         const uint32_t base = (j << logC) + c;
 #pragma unroll
         for (int r = 0; r < R; ++r) sm[pidx(base + r * stride)] = v[r];
+        hook();
     }
 }
 
@@ -588,30 +593,64 @@ __device__ __forceinline__ void k1p_last_stage(const double2 *sm, const StageDes
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// drain chunks [ch0, ch1) of the previous tile (chunk = 8 outputs of one butterfly: k = ch / 2,
-// half = ch & 1) from TMEM to its rows: output r of butterfly (c, g) is work-array row 16 g + r
-__device__ __forceinline__ void k1p_drain(double2 *__restrict__ dst, uint32_t N1, uint32_t nb, uint32_t logC,
-                                          uint32_t tm, uint32_t kmax, uint32_t ch0, uint32_t ch1)
+// drain pieces [p0, p1) of the previous tile: piece = 2 outputs of one butterfly (k = pc / 8,
+// outputs 2 (pc % 8) and 2 (pc % 8) + 1) -- small pieces spread over the next tile's first
+// stage keep the store queue from filling (lg_throttle) as whole 8-output chunks did
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&r)[16])
 {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                 "%14, %15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, uint32_t (&r)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+template <int PW>  // outputs per piece: 2, 4 or 8
+__device__ __forceinline__ void k1p_drain_pieces_t(double2 *__restrict__ dst, uint32_t N1, uint32_t nb, uint32_t logC,
+                                                   uint32_t tm, uint32_t kmax, uint32_t p0, uint32_t p1)
+{
+    constexpr uint32_t PPB = 16 / PW;  // pieces per butterfly
     const uint32_t cm = (1u << logC) - 1;
     const uint32_t lane_base = tm + ((32u * ((threadIdx.x >> 5) & 3)) << 16);
-    for (uint32_t ch = ch0; ch < ch1; ++ch) {
-        const uint32_t k = ch >> 1, h = ch & 1;
+    for (uint32_t pc = p0; pc < p1; ++pc) {
+        const uint32_t k = pc / PPB, pr = pc % PPB;
         const uint32_t qb = (threadIdx.x & ~31u) + k * blockDim.x;
         if (k >= kmax || qb >= nb) break;  // warp-uniform
-        uint32_t w[32];
-        tm_ld32(lane_base + k1p_col(k, kmax) + 32u * h, w);
+        uint32_t w[4 * PW];
+        const uint32_t ta = lane_base + k1p_col(k, kmax) + 4u * PW * pr;
+        if constexpr (PW == 2) {
+            uint32_t (&v)[8] = reinterpret_cast<uint32_t (&)[8]>(w);
+            tm_ld8(ta, v);
+        } else if constexpr (PW == 4) {
+            uint32_t (&v)[16] = reinterpret_cast<uint32_t (&)[16]>(w);
+            tm_ld16(ta, v);
+        } else {
+            uint32_t (&v)[32] = reinterpret_cast<uint32_t (&)[32]>(w);
+            tm_ld32(ta, v);
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const uint32_t q = qb + (threadIdx.x & 31);
         if (q < nb) {
             const uint32_t c = q & cm, g = q >> logC;
-            double2 *p = dst + (uint64_t)(16u * g + 8u * h) * N1 + c;
+            double2 *p = dst + (uint64_t)(16u * g + PW * pr) * N1 + c;
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < PW; ++i)
                 p[(uint64_t)i * N1] = make_double2(__hiloint2double(w[4 * i + 1], w[4 * i]),
                                                    __hiloint2double(w[4 * i + 3], w[4 * i + 2]));
         }
     }
+}
+__device__ __forceinline__ void k1p_drain_pieces(double2 *__restrict__ dst, uint32_t N1, uint32_t nb, uint32_t logC,
+                                                 uint32_t tm, uint32_t kmax, uint32_t p0, uint32_t p1, uint32_t pw)
+{
+    if (pw == 2) k1p_drain_pieces_t<2>(dst, N1, nb, logC, tm, kmax, p0, p1);
+    else if (pw == 4) k1p_drain_pieces_t<4>(dst, N1, nb, logC, tm, kmax, p0, p1);
+    else k1p_drain_pieces_t<8>(dst, N1, nb, logC, tm, kmax, p0, p1);
 }
 
 template <int RA, int RB, int RC>
@@ -632,7 +671,6 @@ k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geom
     const int S = g.f2.S;
     const StageDesc &last = g.f2.st[S - 1];
     const uint32_t nb_last = last.nb << logC, kmax = g.k1p_kmax;
-    const uint32_t nchunks = 2 * kmax;  // per thread and tile (some may be empty)
     load_tables_async(wlo, whi, T.W2lo, T.W2hi, g.f2.nhi + g.f2.ntw);
     load_tables_async(thlo, thhi, T.thlo, T.thhi, g.f2.nhi);
     if (kBits)
@@ -664,18 +702,28 @@ k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geom
         cp_async_wait_all();
         __syncthreads();  // this tile's bits (and the tables) landed; the last tile's smem reads done
         if (t + gridDim.x < ntiles) fetch_bits(t + gridDim.x, (it & 1) ? rowbits0 : rowbits1);
-        // spread the previous tile's drain over this tile's S stage passes
-        uint32_t ch = 0;
-        auto drain_step = [&](int i) {
-            if (!prev) return;
-            const uint32_t upto = (nchunks * (uint32_t)(i + 1) + S - 1) / S;
-            k1p_drain(prev, g.N1, nb_last, logC, tm, kmax, ch, upto);
-            ch = upto;
+        // spread the previous tile's drain (npieces pieces of 2 outputs per thread) over this tile:
+        // one piece per first-stage butterfly iteration, the rest before the later stage passes
+        uint32_t pc = 0;
+        const uint32_t pw = g.k1p_piece, npieces = (16 / pw) * kmax;
+        auto drain_upto = [&](uint32_t upto) {
+            if (!prev || upto <= pc) return;
+            k1p_drain_pieces(prev, g.N1, nb_last, logC, tm, kmax, pc, upto, pw);
+            pc = upto;
+        };
+        auto drain_step = [&](int i) {  // before stage i (1 <= i <= S - 1): an even share of what is left
+            const uint32_t left = npieces - pc, passes = (uint32_t)(S - i);
+            drain_upto(pc + (left + passes - 1) / passes);
         };
         int s0 = 0;
-        drain_step(0);
+        const uint32_t nb0 = g.f2.st[0].nb << logC;
         if (kBits && g.ntb) {
-            k1_first_stage_bits<kBits ? RA : 2>(sm, g.f2.st[0], logC, rowbits, tb, thlo, thhi, wlo, whi);
+            if (prev && nb0 % 32 == 0) {  // warp-uniform trip counts: the warp-collective TMEM loads may sit in the loop
+                auto hook = [&]() { drain_upto(pc + 1 < npieces ? pc + 1 : npieces); };
+                k1_first_stage_bits<kBits ? RA : 2>(sm, g.f2.st[0], logC, rowbits, tb, thlo, thhi, wlo, whi, hook);
+            } else {
+                k1_first_stage_bits<kBits ? RA : 2>(sm, g.f2.st[0], logC, rowbits, tb, thlo, thhi, wlo, whi);
+            }
             s0 = 1;
         } else {
             const uint32_t twoC = 2 * C, epw = 32 / twoC, tot = g.N2 << logC;
@@ -693,12 +741,12 @@ k1p_fwd_columns(const uint32_t *__restrict__ kb, double2 *__restrict__ buf, Geom
             stage_t<false, MODE_PLAIN, RA, RB, RC>(sm, g.f2, i, logC, wlo, whi);
             __syncthreads();
         }
-        drain_step(S - 1);  // everything of the previous tile is out of TMEM now
+        drain_upto(npieces);  // everything of the previous tile is out of TMEM now
         k1p_last_stage(sm, last, logC, tm, kmax);
         prev = buf + (uint64_t)key * g.M + a0;
     }
     grid_dep_launch();  // K2 may start its prologue
-    if (prev) k1p_drain(prev, g.N1, nb_last, logC, tm, kmax, 0, nchunks);
+    if (prev) k1p_drain_pieces(prev, g.N1, nb_last, logC, tm, kmax, 0, (16 / g.k1p_piece) * kmax, g.k1p_piece);
     cta_sync_tmem();
     if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(tcols) : "memory");
 }
@@ -1616,6 +1664,10 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const bool two = e2 && atoi(e2) == 1 && g->t1 == PA_TMAX / 2 && 2 * (g->smem1p + 64) <= kSmemLimit;
         if (two) g->k1p_t = PA_TMAX / 2;
         g->k1p_tcols = two ? 256u : 512u;
+        // outputs per drain piece (developer override PA_K1P_PIECE = 2 / 4 / 8)
+        const char *ep = dev_env("PA_K1P_PIECE");
+        const int pv = ep ? atoi(ep) : 2;
+        g->k1p_piece = pv == 4 || pv == 8 ? (uint32_t)pv : 2u;
         const uint32_t nbl = g->f2.S ? (g->f2.st[g->f2.S - 1].nb << g->logC) : 0;
         const uint32_t kmax = (nbl + g->k1p_t - 1) / g->k1p_t;
         if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 3 && g->f2.st[g->f2.S - 1].R == 16 &&
