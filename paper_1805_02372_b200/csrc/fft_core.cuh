@@ -273,6 +273,7 @@ struct StageCtx {
     const double2 *gin = nullptr;                    // MODE_TAU_IN / MODE_GCOL: global input
     uint32_t ld = 0;                                 // MODE_GCOL(_OUT): row(-block) pitch in elements
     uint32_t nth = 0;                                // threads sharing the stage (0 = blockDim.x)
+    uint32_t q0 = 0, q1 = 0;                         // butterfly range [q0, q1) (q1 = 0: all)
     // work-array layout (route_a.cu widx): rows in blocks of 2^lr, column groups of 2^lc
     uint32_t lr = 0, lc = 0;
 };
@@ -340,7 +341,8 @@ __device__ __forceinline__ void stage_inl(double2 *sm, const StageDesc &sd, uint
             return;
         }
     }
-    for (uint32_t q = threadIdx.x; q < nb; q += nth) {
+    const uint32_t qend = x.q1 ? x.q1 : nb;
+    for (uint32_t q = x.q0 + threadIdx.x; q < qend; q += nth) {
         const uint32_t c = q & cm, t = q >> logC;
         const uint32_t g = (uint32_t)(((uint64_t)t * sd.magic) >> 40);
         const uint32_t j = t - g * sd.Ls;

@@ -47,6 +47,7 @@ struct Geometry {
     uint32_t k1p_t;         // K1P threads per CTA
     uint32_t k1p_tcols;     // K1P TMEM columns per CTA (512: one CTA per SM, 256: two)
     uint32_t k1p_piece;     // K1P drain piece: outputs per TMEM load (2, 4, 8)
+    uint32_t k3parts;       // K3 staged tile loaded in parts, the first inverse stage per part
     int k2shape;            // K2 as k2_rows_t<R0, R1> (1: 16,16  2: 5,8  3: 3,8  4: 7,4), 0: k2_rows
     int k13;                // K1/K3 instantiation (route_a.cu kK13), 0: general
 };

@@ -1122,14 +1122,43 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
     // >= 64 B (C >= 4); with 32 B chunks (C = 2) the staged cp.async copy is faster (round 1:
     // C4 K3 731 vs 986 us; C5c at C = 4 117 -> 111 us, C3 at C = 8 68 -> 64.5 us)
     const bool direct = g.f2.S > 1 && C >= 4;
+    // staged tiles load in KP parts (separate cp.async groups), and the first inverse stage
+    // (radix 16 over 16 consecutive rows: Ls = 1) runs on each part as soon as it has landed, under
+    // the loads of the later parts (developer override PA_K3_PARTS=1 for the single-wait form)
+    const uint32_t kp = !direct && g.k3parts > 1 && g.f2.S > 1 && g.f2.st[g.f2.S - 1].Ls == 1 ? g.k3parts : 1;
     if (!direct) {
-        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x)
-            cp_async16(sm + pidx(e), buf + wrow(g, e >> logC) + ((uint64_t)a0 << g.lr) + (e & (C - 1)));
+        for (uint32_t p = 0; p < kp; ++p) {
+            const uint32_t e0 = tot / kp * p, e1 = p + 1 == kp ? tot : tot / kp * (p + 1);
+            for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+                cp_async16(sm + pidx(e), buf + wrow(g, e >> logC) + ((uint64_t)a0 << g.lr) + (e & (C - 1)));
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        }
     }
-    cp_async_wait_all();  // tables (and the staged tile)
-    __syncthreads();
     int64_t b_lo, b_hi;
     k3_window_rows(g, a0, C, n, m, &b_lo, &b_hi);
+    int s_hi = g.f2.S;  // stages [lo, s_hi) of the DIT still to run
+    if (kp > 1) {
+        const StageDesc &sd = g.f2.st[g.f2.S - 1];
+        const uint32_t nbq = sd.nb << logC;  // butterflies of the stage; part p owns an equal slice
+        for (uint32_t p = 0; p < kp; ++p) {
+            switch (kp - 1 - p) {  // groups still allowed in flight
+            case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+            case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+            case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+            default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+            }
+            __syncthreads();
+            StageCtx px;
+            px.q0 = nbq / kp * p;
+            px.q1 = p + 1 == kp ? nbq : nbq / kp * (p + 1);
+            stage_t<true, MODE_PLAIN, RA, RB, RC>(sm, g.f2, g.f2.S - 1, logC, wlo, whi, px);
+        }
+        __syncthreads();
+        s_hi = g.f2.S - 1;
+    } else {
+        cp_async_wait_all();  // tables (and the staged tile)
+        __syncthreads();
+    }
     TSTAMPK(2, 1);
     if (direct) {
         StageCtx gx;
@@ -1141,7 +1170,7 @@ k3_inv_columns(const double2 *__restrict__ buf, Geometry g, RouteTables T, uint6
         __syncthreads();
         dit_t<RA, RB, RC>(sm, g.f2, kFuse ? 1 : 0, g.f2.S - 1, logC, wlo, whi);
     } else {
-        dit_t<RA, RB, RC>(sm, g.f2, kFuse ? 1 : 0, g.f2.S, logC, wlo, whi);
+        dit_t<RA, RB, RC>(sm, g.f2, kFuse ? 1 : 0, s_hi, logC, wlo, whi);
     }
     TSTAMPK(2, 2);
     const double rmax = k3_epilogue<kFuse ? RA : 0>(sm, g, a0, logC, n, m, thlo, thhi, out, (uint32_t)b_lo,
@@ -1685,6 +1714,16 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     }
     g->logC3 = 0;
     while ((1u << g->logC3) < g->C3) ++g->logC3;
+    // K3's staged tile in parts (see k3_inv_columns); the part boundaries must fall on
+    // butterflies of the first inverse stage (16-row groups): N2 a multiple of 16 * parts
+    {
+        // measured (round 2): C4 K3 587 (1 part) / 592 (2) / 620 us (4), C5d 207.5 / 217 / 228 us --
+        // the per-part barriers cost more than the overlap gains (two CTAs per SM already overlap
+        // one tile's load with the other's stages); off by default, developer override PA_K3_PARTS
+        const char *e = dev_env("PA_K3_PARTS");
+        const int pv = e ? atoi(e) : 1;
+        g->k3parts = pv >= 1 && pv <= 4 && g->N2 % (16u * (uint32_t)pv) == 0 ? (uint32_t)pv : 1u;
+    }
     g->tile3 = tile_bytes((uint64_t)g->N2 * g->C3) / 16;
     g->smem3 = smem_k13(g->N2, g->C3, g->f2);
     g->t3 = g->C3 == g->C ? g->t1 : 2 * g->smem3 <= kSmemLimit ? PA_TMAX / 2 : PA_TMAX;
