@@ -1323,6 +1323,10 @@ struct K13 {
 static const K13 kK13[] = {
     PA_K13(0, 0, 0), PA_K13(2, 5, 0), PA_K13(3, 4, 7), PA_K13(3, 8, 0), PA_K13(3, 3, 0), PA_K13(7, 4, 0),
     PA_K13(3, 7, 8),
+    // round 2: column lengths the planner reaches for other n (4096, 2048, 1024, 768, 1280, 3072)
+    // ([16, 16, 16] columns were tried too: the planner then took 4096-column plans that measured
+    // slower -- C5d 7168 x 4096 1040 vs 10240 x 2688 888 us per batched key -- so they stay general)
+    PA_K13(8, 16, 0), PA_K13(4, 16, 0), PA_K13(3, 16, 0), PA_K13(5, 16, 0), PA_K13(3, 4, 0),
 };
 #undef PA_K13
 
