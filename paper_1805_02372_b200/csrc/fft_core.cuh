@@ -289,6 +289,30 @@ __device__ __forceinline__ uint32_t grow_off(const StageCtx &x, uint32_t a)
     return ((a >> x.lc) << (x.lc + x.lr)) + (a & ((1u << x.lc) - 1));
 }
 
+// K2's row twist on a butterfly's inputs v[r] (element idx0 + r Ls): rho^{idx0 + r Ls} =
+// rho^{idx0} * rho^{r Ls}, and when 64 | Ls the second factor is the single entry rhi[r Ls / 64]
+// (the same for every lane: a broadcast), so a radix-16 butterfly reads one two-level lookup
+// instead of 16 -- the lookups' shared-memory wavefronts, not their FP64 work, are what the pass
+// pays for (C5b K2 20.8 -> 19.7 us; at radix 5, C4, it measured neutral to
+// 0.2% slower and keeps the per-element lookups).  The factor is a product of three correctly
+// rounded entries (Sec. 5).
+template <int R>
+__device__ __forceinline__ bool twist_factored(uint32_t Ls) { return R >= 16 && (Ls & 63) == 0; }
+
+template <int R>
+__device__ __forceinline__ void twist_in(double2 *v, const StageCtx &x, uint32_t idx0, uint32_t Ls)
+{
+    if (twist_factored<R>(Ls)) {
+        const double2 t0 = twiddle(x.rlo, x.rhi, idx0);
+        v[0] = cmul(v[0], t0);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], cmul(t0, x.rhi[(r * Ls) >> 6]));
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * Ls));
+    }
+}
+
 // One in-place stage over all butterflies of a batch of 2^logC sequences held
 // in padded shared memory (element idx of sequence c at pidx((idx << logC) + c)).
 //   DIF (forward): v = DFT_R(v); v_k *= omega_L^{jk}
@@ -332,8 +356,7 @@ __device__ __forceinline__ void stage_inl(double2 *sm, const StageDesc &sd, uint
 #pragma unroll
                     for (int r = 0; r < R; ++r) nv[r] = x.gin[grow_off(x, i1 + r * sd.Ls)];
                 }
-#pragma unroll
-                for (int r = 0; r < R; ++r) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
+                twist_in<R>(v, x, idx0, sd.Ls);
                 butterfly<R, INV>(v, j, sd, wlo, whi);
 #pragma unroll
                 for (int r = 0; r < R; ++r) sm[pidx(base + r * stride)] = v[r];
@@ -354,14 +377,18 @@ __device__ __forceinline__ void stage_inl(double2 *sm, const StageDesc &sd, uint
             if (MODE == MODE_TAU_IN && x.gin) v[r] = x.gin[grow_off(x, idx0 + r * sd.Ls)];
             else if (MODE == MODE_GCOL) v[r] = x.gin[gcol_off(x, idx0 + r * sd.Ls, c)];
             else v[r] = sm[pidx(base + r * stride)];
-            if (MODE == MODE_TAU_IN) v[r] = cmul(v[r], twiddle(x.rlo, x.rhi, idx0 + r * sd.Ls));
         }
+        if (MODE == MODE_TAU_IN) twist_in<R>(v, x, idx0, sd.Ls);
         butterfly<R, INV>(v, j, sd, wlo, whi);
+        double2 t0;
+        if (MODE == MODE_TAU_OUT && twist_factored<R>(sd.Ls)) t0 = twiddle(x.rlo, x.rhi, idx0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (MODE == MODE_TAU_OUT) {
                 const uint32_t idx = idx0 + r * sd.Ls;
-                x.gout[grow_off(x, idx)] = cmulc(v[r], twiddle(x.rlo, x.rhi, idx));
+                x.gout[grow_off(x, idx)] =
+                    cmulc(v[r], twist_factored<R>(sd.Ls) ? (r ? cmul(t0, x.rhi[(r * sd.Ls) >> 6]) : t0)
+                                                         : twiddle(x.rlo, x.rhi, idx));
             } else if (MODE == MODE_GCOL_OUT) {
                 x.gout[gcol_off(x, idx0 + r * sd.Ls, c)] = v[r];
             } else {
