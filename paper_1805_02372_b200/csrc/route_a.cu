@@ -815,7 +815,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     if (g.pfs && mode == 0) l2_prefetch_row(sp, N1);
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
-    if (P0.S <= 1 || mode == 1) {  // tiny rows / seed path: stage through shared memory
+    if (P0.S <= 1) {  // tiny rows: stage through shared memory
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) cp_async16(sm + pidx(e), rp + e);
     }
     cp_async_wait_all();  // tables (and the staged row)
@@ -829,11 +829,8 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     if (P.S <= 1) {  // N1 <= 16: tau elementwise, then the single stage below runs plain
         for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x) sm[pidx(e)] = cmul(sm[pidx(e)], twiddle(rlo, rhi, e));
         __syncthreads();
-    } else if (mode == 1) {
-        stage_any<false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
-        __syncthreads();
     } else {
-        rt.gin = rp;  // hash path: the first stage reads the row straight from global memory
+        rt.gin = rp;  // the first stage reads the row straight from global memory
         stage_any<false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
         rt.gin = nullptr;
         __syncthreads();
@@ -841,10 +838,14 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
     const int dif_from = P.S <= 1 ? 0 : 1;
     if (mode == 1) {
         dif_stages(sm, P, dif_from, P.S, 0, wlo, whi);
-        // spectrum row in the [r][g] order fused_mid reads (R = last stage's radix)
+        // spectrum row in the [r][g] order fused_mid reads (R = last stage's radix): consecutive
+        // threads write consecutive spectrum entries (element g R + r at sp[r nbl + g])
+        grid_dep_launch();
         const uint32_t R = P.S ? P.st[P.S - 1].R : 1, nbl = N1 / R;
-        for (uint32_t e = threadIdx.x; e < N1; e += blockDim.x)
-            sp[(e % R) * nbl + e / R] = cscale(sm[pidx(e)], scale);
+        for (uint32_t f = threadIdx.x; f < N1; f += blockDim.x) {
+            const uint32_t r = f / nbl, gq = f - r * nbl;
+            sp[f] = cscale(sm[pidx(gq * R + r)], scale);
+        }
         return;
     }
     if (P.S == 0) {
@@ -897,9 +898,12 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 #ifndef PA_K2MAX
 #define PA_K2MAX PA_TMAX  // developer experiments: K2's launch bound (PA_FORCE_T2 up to it)
 #endif
-template <int R0, int R1, int NS>
+// SEED: the create-time / fresh-seed forward half instead (k2_rows mode 1): the last DIF stage
+// (radix 16, span 16, no twiddles) runs from shared memory straight into the spectrum row,
+// scaled by 1/M, in the [r][g] order fused_mid reads -- coalesced across lanes, no write-back.
+template <int R0, int R1, int NS, bool SEED = false>
 __global__ void __launch_bounds__(PA_K2MAX, PA_MINB)
-k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometry g, RouteTables T,
+k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, RouteTables T,
           uint64_t spec_stride)
 {
     extern __shared__ double2 sm[];
@@ -912,13 +916,13 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
     TSTAMP(0);
     double2 *rp = buf + (uint64_t)row * N1;
     double2 *rq = out2 + wrow(g, row);
-    const double2 *sp = spec + blockIdx.x * spec_stride + (uint64_t)row * N1;
+    double2 *sp = spec + blockIdx.x * spec_stride + (uint64_t)row * N1;
     load_tables_async(wlo, whi, T.W1lo, T.W1hi, g.f1.nhi + g.f1.ntw);
     {
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
-    if (g.pfs) l2_prefetch_row(sp, N1);  // this row's spectrum, pulled in under the forward stages
+    if (!SEED && g.pfs) l2_prefetch_row(sp, N1);  // this row's spectrum, pulled in under the forward stages
     grid_dep_wait();  // K1's work array
     cp_async_wait_all();  // the tables
     __syncthreads();
@@ -948,6 +952,20 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
         __syncthreads();
     }
     TSTAMP(3);
+    if constexpr (SEED) {
+        grid_dep_launch();
+        const StageDesc &sd = P.st[NS - 1];
+        const double sc = 1.0 / (double)g.M;
+        for (uint32_t gq = threadIdx.x; gq < sd.nb; gq += blockDim.x) {
+            double2 v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = sm[pidx(gq * 16 + r)];
+            Dft<16, false>::run(v);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) sp[r * sd.nb + gq] = cscale(v[r], sc);
+        }
+        return;
+    }
     fused_mid<16>(P.st[NS - 1], sm, sp);
     __syncthreads();
     TSTAMP(4);
@@ -971,24 +989,26 @@ k2_rows_t(double2 *buf, double2 *out2, const double2 *__restrict__ spec, Geometr
 
 // the shapes k2_rows_t is instantiated for (g.k2shape: 0 = general k2_rows)
 // shape-specialised K2 instantiations: rows [R0, R1, 16, ...] with NS stages (kK2[0] = general)
-using K2Fn = void (*)(double2 *, double2 *, const double2 *, Geometry, RouteTables, uint64_t);
+using K2Fn = void (*)(double2 *, double2 *, double2 *, Geometry, RouteTables, uint64_t);
 struct K2Shape {
     int a, b, s;
-    K2Fn fn;
+    K2Fn fn, seed;  // hash path, seed forward half
 };
+#define PA_K2(A, B, S) {A, B, S, k2_rows_t<A, B, S>, k2_rows_t<A, B, S, true>}
 static const K2Shape kK2[] = {
-    {0, 0, 0, nullptr},
-    {16, 16, 3, k2_rows_t<16, 16, 3>},  // 4096 (C2, C3, C5a-c)
-    {5, 8, 4, k2_rows_t<5, 8, 4>},      // 10240 (C4, C5d)
-    {3, 8, 4, k2_rows_t<3, 8, 4>},      // 6144
-    {7, 4, 4, k2_rows_t<7, 4, 4>},      // 7168
-    {2, 16, 4, k2_rows_t<2, 16, 4>},    // 8192 (round 2: the calibration sweep's worst misses)
-    {3, 16, 4, k2_rows_t<3, 16, 4>},    // 12288
-    {7, 5, 4, k2_rows_t<7, 5, 4>},      // 8960
-    {5, 4, 4, k2_rows_t<5, 4, 4>},      // 5120
-    {8, 16, 3, k2_rows_t<8, 16, 3>},    // 2048
-    {3, 4, 4, k2_rows_t<3, 4, 4>},      // 3072
+    {0, 0, 0, nullptr, nullptr},
+    PA_K2(16, 16, 3),  // 4096 (C2, C3, C5a-c)
+    PA_K2(5, 8, 4),    // 10240 (C4, C5d)
+    PA_K2(3, 8, 4),    // 6144
+    PA_K2(7, 4, 4),    // 7168
+    PA_K2(2, 16, 4),   // 8192 (round 2: the calibration sweep's worst misses)
+    PA_K2(3, 16, 4),   // 12288
+    PA_K2(7, 5, 4),    // 8960
+    PA_K2(5, 4, 4),    // 5120
+    PA_K2(8, 16, 3),   // 2048
+    PA_K2(3, 4, 4),    // 3072
 };
+#undef PA_K2
 
 static int k2_shape(const FftPlan &p)
 {
@@ -1847,6 +1867,36 @@ pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 
 // Seed spectrum: K0 + K1 + forward half of K2 on the seed, scaled by 1/M.  Uses the
 // hash work buffers as scratch (stream-ordered with the hashes).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args);
+
+// The seed half of the path for `count` seeds (a0, create time or a fresh seed): K0 -> K1 (K1P
+// where the hash uses it) -> K2 forward half, spectrum / M of seed k at spec + k spec_stride.
+static void ra_seed_transform(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride, uint32_t count,
+                              double2 *spec, uint64_t spec_stride, cudaStream_t s)
+{
+    RouteA &a = h->a;
+    const Geometry &g = a.g;
+    const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), count);
+    launch_pdl(k0_bits_transpose, g0, dim3(256), 0, s, seeds, h->off, h->L, a.kb, g, seed_stride);
+    if (g.k1p_kmax) {
+        const uint32_t tiles = (g.N1 / g.C) * count;
+        const uint32_t slots = g.k1p_tcols == 256 ? 2 * 148 : 148;
+        launch_pdl(kK13[g.k13].k1p, dim3(tiles < slots ? tiles : slots), dim3(g.k1p_t), g.smem1p, s,
+                   (const uint32_t *)a.kb, a.buf, g, a.T, (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0, count);
+    } else {
+        launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, (const uint32_t *)a.kb, a.buf, g, a.T,
+                   (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0, (const uint32_t *)nullptr, (uint64_t)0,
+                   (uint64_t)0);
+    }
+    if (g.k2shape)
+        launch_pdl(kK2[g.k2shape].seed, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf, spec, g, a.T, spec_stride);
+    else
+        launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf, spec, g, a.T, 1, 1.0 / (double)g.M,
+                   spec_stride);
+}
+
 pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 {
     RouteA &a = h->a;
@@ -1874,15 +1924,14 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
                                   (int)kSmemLimit - 1024)) != cudaSuccess)  // K3T has static smem too
         return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     for (const K2Shape &f : kK2)
-        if (f.fn && (e = cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
-                        cudaSuccess)
+        if (f.fn && ((e = cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
+                         cudaSuccess ||
+                     (e = cudaFuncSetAttribute(f.seed, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kSmemLimit)) != cudaSuccess))
             return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     attr_done.fetch_or(bit);
 launch:
-    const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g));
-    k0_bits_transpose<<<g0, 256, 0, s>>>(seed, h->off, h->L, a.kb, g, 0);
-    kK13[g.k13].k1<<<g.N1 / g.C, g.t1, g.smem1, s>>>(a.kb, a.buf, g, a.T, nullptr, 0, 0, nullptr, 0, 0);
-    k2_rows<<<dim3(1, g.N2), g.t2, g.smem2, s>>>(a.buf, a.buf, a.spec, g, a.T, 1, 1.0 / (double)g.M, 0);
+    ra_seed_transform(h, seed, 0, 1, a.spec, 0, s);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "route (a) seed transform launches");
     return PA_OK;
 }
@@ -1975,7 +2024,7 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         const double2 *sp = spec ? spec : a.spec;  // fresh seeds: one spectrum per key
         const uint64_t ss = spec ? spec_stride : 0;
         if (g.k2shape)
-            launch_pdl(kK2[g.k2shape].fn, g2, g.t2, g.smem2, s, a.buf, a.buf2, sp, g, a.T, ss);
+            launch_pdl(kK2[g.k2shape].fn, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, ss);
         else
             launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
     }
@@ -2028,14 +2077,7 @@ pa_status ra_fresh_batch(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride,
     }
     for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
         const uint32_t c = std::min(chunk, count - k0);
-        const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), c);
-        launch_pdl(k0_bits_transpose, g0, dim3(256), 0, s, seeds + k0 * seed_stride, h->off, h->L, a.kb, g,
-                   seed_stride);
-        launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, c), g.t1, g.smem1, s, (const uint32_t *)a.kb, a.buf, g, a.T,
-                   (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0, (const uint32_t *)nullptr, (uint64_t)0,
-                   (uint64_t)0);
-        launch_pdl(k2_rows, dim3(c, g.N2), g.t2, g.smem2, s, a.buf, a.buf, a.fspec, g, a.T, 1, 1.0 / (double)g.M,
-                   (uint64_t)g.M);
+        ra_seed_transform(h, seeds + k0 * seed_stride, seed_stride, c, a.fspec, g.M, s);
         if ((st = ra_hash_batch(h, keys + k0 * key_stride, key_stride, outs + k0 * out_stride, out_stride, c,
                                 zero_words, s, a.fspec, g.M)) != PA_OK)
             return st;
