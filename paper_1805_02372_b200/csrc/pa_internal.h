@@ -35,6 +35,7 @@ struct Geometry {
     uint32_t k0rb, k0cb;    // K0 tile: rows x columns per CTA
     FftPlan f1, f2;         // stage plans of N1 (row pass) and N2 (strided passes)
     uint32_t t1, t2;        // threads per CTA: strided passes (K1/K3), row pass (K2)
+    uint32_t t2one;         // K2's threads when its grid is at most one CTA per SM (route_a.cu k2_threads)
     uint32_t tile1, tile2;  // padded tile sizes in double2 (tables follow the tile)
     uint32_t smem1, smem2;  // dynamic shared bytes: K1/K3, K2
     uint32_t kbw;           // K0 bit-stream words per column group

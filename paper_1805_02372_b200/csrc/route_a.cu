@@ -1681,7 +1681,11 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         return v >= 64 && v <= (PA_K2MAX > PA_TMAX ? PA_K2MAX : PA_TMAX) && v % 32 == 0;
     };
     if (const char *e = dev_env("PA_FORCE_T1"); threads_ok(e)) g->t1 = (uint32_t)atoi(e);
-    if (const char *e = dev_env("PA_FORCE_T2"); threads_ok(e)) g->t2 = (uint32_t)atoi(e);
+    // K2 whose grid (rows x keys) fits one wave of one CTA per SM runs 512 threads even where two
+    // CTAs per SM would fit: nothing shares the SM, so the row's latency chain is all there is
+    // (C5a single key, 144 rows: 34.3 -> 30.3 us; at C2's 160 rows two CTAs per SM stay faster)
+    g->t2one = PA_TMAX;
+    if (const char *e = dev_env("PA_FORCE_T2"); threads_ok(e)) g->t2 = g->t2one = (uint32_t)atoi(e);
     // K3's column groups: half of K1's when K1's tile allows one CTA per SM and the half tile
     // two -- a second CTA's loads overlap the first one's stages, worth more than the longer
     // 16-byte row pieces (C4: K3 721 -> 630 us; K1 itself measured slower at C = 1, 778 -> 919
@@ -1871,6 +1875,12 @@ template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args);
 
+// K2's threads for a grid of `count` keys x N2 rows (Geometry::t2one)
+static uint32_t k2_threads(const Geometry &g, uint32_t count)
+{
+    return (uint64_t)g.N2 * count <= 148u ? g.t2one : g.t2;
+}
+
 // The seed half of the path for `count` seeds (a0, create time or a fresh seed): K0 -> K1 (K1P
 // where the hash uses it) -> K2 forward half, spectrum / M of seed k at spec + k spec_stride.
 static void ra_seed_transform(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride, uint32_t count,
@@ -1891,9 +1901,10 @@ static void ra_seed_transform(pa_ctx *h, const uint32_t *seeds, uint64_t seed_st
                    (uint64_t)0);
     }
     if (g.k2shape)
-        launch_pdl(kK2[g.k2shape].seed, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf, spec, g, a.T, spec_stride);
+        launch_pdl(kK2[g.k2shape].seed, dim3(count, g.N2), k2_threads(g, count), g.smem2, s, a.buf, a.buf, spec, g, a.T, spec_stride);
     else
-        launch_pdl(k2_rows, dim3(count, g.N2), g.t2, g.smem2, s, a.buf, a.buf, spec, g, a.T, 1, 1.0 / (double)g.M,
+        launch_pdl(k2_rows, dim3(count, g.N2), k2_threads(g, count), g.smem2, s, a.buf, a.buf, spec, g, a.T, 1,
+                   1.0 / (double)g.M,
                    spec_stride);
 }
 
@@ -2024,9 +2035,9 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         const double2 *sp = spec ? spec : a.spec;  // fresh seeds: one spectrum per key
         const uint64_t ss = spec ? spec_stride : 0;
         if (g.k2shape)
-            launch_pdl(kK2[g.k2shape].fn, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, ss);
+            launch_pdl(kK2[g.k2shape].fn, g2, k2_threads(g, count), g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, ss);
         else
-            launch_pdl(k2_rows, g2, g.t2, g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
+            launch_pdl(k2_rows, g2, k2_threads(g, count), g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
     }
     prof_end(h, s);
     prof_begin(h, 2, s);
