@@ -49,6 +49,9 @@ struct Geometry {
     uint32_t k1p_tcols;     // K1P TMEM columns per CTA (512: one CTA per SM, 256: two)
     uint32_t k1p_piece;     // K1P drain piece: outputs per TMEM load (2, 4, 8)
     uint32_t k3parts;       // K3 staged tile loaded in parts, the first inverse stage per part
+    bool k2fresh;           // pa_hash_fresh_batch fuses the seeds' forward half into K2 (k2_rows_t kFresh)
+    double2 *fout;          // kFresh launches: key fkey's spectrum row also goes to fout (the handle's)
+    uint32_t fkey;
     int k2shape;            // K2 as k2_rows_t<R0, R1> (1: 16,16  2: 5,8  3: 3,8  4: 7,4), 0: k2_rows
     int k13;                // K1/K3 instantiation (route_a.cu kK13), 0: general
 };
@@ -184,7 +187,7 @@ pa_status ra_hash(pa_ctx *h, const uint32_t *key, uint32_t *out, uint64_t zero_w
                   cudaStream_t s);
 pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
                         uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s,
-                        const double2 *spec = nullptr, uint64_t spec_stride = 0);
+                        const double2 *spec = nullptr, uint64_t spec_stride = 0, bool fresh = false);
 pa_status ra_fresh_batch(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride, const uint32_t *keys,
                          uint64_t key_stride, uint32_t *outs, uint64_t out_stride, uint32_t count,
                          uint64_t zero_words, cudaStream_t s);

@@ -886,6 +886,20 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 }
 
 // ------------------------------------------------------------------ K2 for fixed radix shapes
+// TMEM columns of a fresh-seed K2 CTA (k2_rows_t<..., kFresh>): 256 when two CTAs share the SM
+// (<= 256 threads and two tiles of shared memory), else 512
+__host__ __device__ inline uint32_t k2f_tcols(const Geometry &g, uint32_t nth)
+{
+    return nth <= PA_TMAX / 2 && 2 * (g.smem2 + 16) <= kSmemLimit ? 256u : 512u;
+}
+// a fresh-seed K2 fits when every thread's last-stage butterflies (64 columns each) fit its
+// lane quarter's share of the columns
+inline bool k2f_fits(const Geometry &g, uint32_t nth)
+{
+    if (!g.k2shape || g.smem2 + 16 > kSmemLimit) return false;
+    const uint32_t nb = g.f1.st[g.f1.S - 1].nb, kmax = (nb + nth - 1) / nth;
+    return (nth / 128) * kmax * 64 <= k2f_tcols(g, nth);
+}
 // The hash path of k2_rows for row plans [R0, R1, 16, ..., 16] (S >= 3): 4096 = [16, 16, 16]
 // (C2, C3, C5), 10240 = [5, 8, 16, 16] (C4, C5d), 6144 = [3, 8, 16, 16], 7168 = [7, 4, 16, 16],
 // calling those stage routines directly: the general kernel's radix switch instantiates every
@@ -898,10 +912,16 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
 #ifndef PA_K2MAX
 #define PA_K2MAX PA_TMAX  // developer experiments: K2's launch bound (PA_FORCE_T2 up to it)
 #endif
-// SEED: the create-time / fresh-seed forward half instead (k2_rows mode 1): the last DIF stage
-// (radix 16, span 16, no twiddles) runs from shared memory straight into the spectrum row,
+// KM = kSeed: the create-time / fresh-seed forward half instead (k2_rows mode 1): the last DIF
+// stage (radix 16, span 16, no twiddles) runs from shared memory straight into the spectrum row,
 // scaled by 1/M, in the [r][g] order fused_mid reads -- coalesced across lanes, no write-back.
-template <int R0, int R1, int NS, bool SEED = false>
+// KM = kFresh: a fresh seed per key fused into the hash (pa_hash_fresh_batch): `spec` is the
+// seeds' K1 output, not spectra.  The CTA first runs the seed row's forward half and keeps the
+// scaled spectrum row in tensor memory (each thread its own last-stage butterflies, in its TMEM
+// lane: the layout K1P uses), then the key row's forward half, whose fused middle stage
+// multiplies by the spectrum read back from TMEM -- the spectrum never goes through HBM.
+enum { kHash = 0, kSeed = 1, kFresh = 2 };
+template <int R0, int R1, int NS, int KM = kHash>
 __global__ void __launch_bounds__(PA_K2MAX, PA_MINB)
 k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, RouteTables T,
           uint64_t spec_stride)
@@ -922,40 +942,94 @@ k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, R
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
-    if (!SEED && g.pfs) l2_prefetch_row(sp, N1);  // this row's spectrum, pulled in under the forward stages
+    if (KM == kHash && g.pfs) l2_prefetch_row(sp, N1);  // this row's spectrum, pulled in under the forward stages
+    // kFresh: TMEM for the spectrum row (256 columns when two CTAs share the SM, else 512)
+    uint32_t *tmb = reinterpret_cast<uint32_t *>(rhi + g.f1.nhi);
+    const uint32_t tcols = k2f_tcols(g, blockDim.x);
+    if (KM == kFresh && threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(tmb)), "r"(tcols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
     grid_dep_wait();  // K1's work array
     cp_async_wait_all();  // the tables
-    __syncthreads();
+    if (KM == kFresh) cta_sync_tmem();
+    else __syncthreads();
     TSTAMP(1);
     const FftPlan &P = g.f1;
     StageCtx rt;
     rt.rlo = rlo;
     rt.rhi = rhi;
-    rt.gin = rp;
-    K2T_STAGE<R0, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
-    __syncthreads();
-    TSTAMP(2);
-    if (g.pf2 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
-        const uint32_t q = threadIdx.x;
-        const char *src = reinterpret_cast<const char *>(rp + (size_t)g.pf2 * N1);
-        const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
-        if (q * chunk < bytes) {
-            const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)q * chunk), "r"(sz) : "memory");
-        }
-    }
-    K2T_STAGE<R1, false, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
-    __syncthreads();
-#pragma unroll
-    for (int i = 2; i < NS - 1; ++i) {
-        K2T_STAGE<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
+    // stages 0 .. NS-2 of the forward half on the row at `src` (global), into shared memory
+    auto forward = [&](const double2 *src, bool prefetch) {
+        rt.gin = src;
+        K2T_STAGE<R0, false, MODE_TAU_IN>(sm, P.st[0], 0, wlo, whi, rt);
         __syncthreads();
+        if (prefetch && g.pf2 && blockIdx.x == 0 && row + g.pf2 < g.N2 && threadIdx.x < 32) {
+            const uint32_t q = threadIdx.x;
+            const char *pre = reinterpret_cast<const char *>(src + (size_t)g.pf2 * N1);
+            const uint32_t bytes = N1 * 16u, chunk = ((bytes + 31) / 32 + 15) & ~15u;
+            if (q * chunk < bytes) {
+                const uint32_t sz = bytes - q * chunk < chunk ? bytes - q * chunk : chunk;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pre + (size_t)q * chunk), "r"(sz)
+                             : "memory");
+            }
+        }
+        K2T_STAGE<R1, false, MODE_PLAIN>(sm, P.st[1], 0, wlo, whi, StageCtx{});
+        __syncthreads();
+#pragma unroll
+        for (int i = 2; i < NS - 1; ++i) {
+            K2T_STAGE<16, false, MODE_PLAIN>(sm, P.st[i], 0, wlo, whi, StageCtx{});
+            __syncthreads();
+        }
+    };
+    const StageDesc &sd = P.st[NS - 1];  // radix 16, span 16: no twiddles
+    const double sc = 1.0 / (double)g.M;
+    const uint32_t kmax = (sd.nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t lane_base = (KM == kFresh ? *tmb : 0u) + ((32u * ((threadIdx.x >> 5) & 3)) << 16);
+    if constexpr (KM == kFresh) {
+        // the seed row's forward half, its last DIF stage scaled into this thread's TMEM columns
+        forward(spec + blockIdx.x * spec_stride + (uint64_t)row * N1, false);
+        uint32_t k = 0;
+        for (uint32_t qb = threadIdx.x & ~31u; qb < sd.nb; qb += blockDim.x, ++k) {  // warp-uniform
+            const uint32_t gq = qb + (threadIdx.x & 31);
+            double2 v[16];
+            if (gq < sd.nb) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) v[r] = sm[pidx(gq * 16 + r)];
+                Dft<16, false>::run(v);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) v[r] = cscale(v[r], sc);
+                if (g.fout && blockIdx.x == g.fkey) {  // the handle keeps this key's seed: its spectrum row
+                    double2 *so = g.fout + (uint64_t)row * N1;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) so[r * sd.nb + gq] = v[r];
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) v[r] = make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t w[32];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const double2 d = v[8 * h + i];
+                    w[4 * i] = __double2loint(d.x);
+                    w[4 * i + 1] = __double2hiint(d.x);
+                    w[4 * i + 2] = __double2loint(d.y);
+                    w[4 * i + 3] = __double2hiint(d.y);
+                }
+                tm_st32(lane_base + k1p_col(k, kmax) + 32u * h, w);
+            }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        __syncthreads();  // the shared tile is the key row's next
     }
+    forward(rp, true);
     TSTAMP(3);
-    if constexpr (SEED) {
+    if constexpr (KM == kSeed) {
         grid_dep_launch();
-        const StageDesc &sd = P.st[NS - 1];
-        const double sc = 1.0 / (double)g.M;
         for (uint32_t gq = threadIdx.x; gq < sd.nb; gq += blockDim.x) {
             double2 v[16];
 #pragma unroll
@@ -966,7 +1040,37 @@ k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, R
         }
         return;
     }
-    fused_mid<16>(P.st[NS - 1], sm, sp);
+    if constexpr (KM == kFresh) {
+        // fused_mid with the spectrum from this thread's TMEM columns
+        uint32_t k = 0;
+        for (uint32_t qb = threadIdx.x & ~31u; qb < sd.nb; qb += blockDim.x, ++k) {  // warp-uniform
+            const uint32_t gq = qb + (threadIdx.x & 31);
+            double2 s16[16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t w[32];
+                tm_ld32(lane_base + k1p_col(k, kmax) + 32u * h, w);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    s16[8 * h + i] = make_double2(__hiloint2double(w[4 * i + 1], w[4 * i]),
+                                                  __hiloint2double(w[4 * i + 3], w[4 * i + 2]));
+            }
+            if (gq < sd.nb) {
+                double2 v[16];
+#pragma unroll
+                for (int r = 0; r < 16; ++r) v[r] = sm[pidx(gq * 16 + r)];
+                Dft<16, false>::run(v);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], s16[r]);
+                Dft<16, true>::run(v);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) sm[pidx(gq * 16 + r)] = v[r];
+            }
+        }
+    } else {
+        fused_mid<16>(sd, sm, sp);
+    }
     __syncthreads();
     TSTAMP(4);
 #pragma unroll
@@ -983,6 +1087,11 @@ k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, R
     rt.lr = g.lr;
     rt.lc = g.logC;
     K2T_STAGE<R0, true, MODE_TAU_OUT>(sm, P.st[0], 0, wlo, whi, rt);
+    if constexpr (KM == kFresh) {
+        cta_sync_tmem();
+        if (threadIdx.x < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmb), "r"(tcols) : "memory");
+    }
     TSTAMP(6);
     TRACE_END(2);
 }
@@ -992,11 +1101,11 @@ k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, R
 using K2Fn = void (*)(double2 *, double2 *, double2 *, Geometry, RouteTables, uint64_t);
 struct K2Shape {
     int a, b, s;
-    K2Fn fn, seed;  // hash path, seed forward half
+    K2Fn fn, seed, fresh;  // hash path, seed forward half, fresh seed fused into the hash
 };
-#define PA_K2(A, B, S) {A, B, S, k2_rows_t<A, B, S>, k2_rows_t<A, B, S, true>}
+#define PA_K2(A, B, S) {A, B, S, k2_rows_t<A, B, S>, k2_rows_t<A, B, S, kSeed>, k2_rows_t<A, B, S, kFresh>}
 static const K2Shape kK2[] = {
-    {0, 0, 0, nullptr, nullptr},
+    {0, 0, 0, nullptr, nullptr, nullptr},
     PA_K2(16, 16, 3),  // 4096 (C2, C3, C5a-c)
     PA_K2(5, 8, 4),    // 10240 (C4, C5d)
     PA_K2(3, 8, 4),    // 6144
@@ -1630,6 +1739,12 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
     {
         const char *e = dev_env("PA_K2_T");
         g->k2shape = (!e || atoi(e) != 0) ? k2_shape(g->f1) : 0;
+        // pa_hash_fresh_batch: the seeds' forward half fused into the hash's K2 (developer
+        // override PA_K2_FRESH=0: per-key spectra through HBM)
+        const char *ef = dev_env("PA_K2_FRESH");
+        g->k2fresh = g->k2shape && (!ef || atoi(ef) != 0);
+        g->fout = nullptr;
+        g->fkey = 0;
         const char *e13 = dev_env("PA_K13_T");
         g->k13 = (!e13 || atoi(e13) != 0) ? k13_shape(g->f2) : 0;
     }
@@ -1884,8 +1999,9 @@ static uint32_t k2_threads(const Geometry &g, uint32_t count)
 // The seed half of the path for `count` seeds (a0, create time or a fresh seed): K0 -> K1 (K1P
 // where the hash uses it) -> K2 forward half, spectrum / M of seed k at spec + k spec_stride.
 static void ra_seed_transform(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride, uint32_t count,
-                              double2 *spec, uint64_t spec_stride, cudaStream_t s)
+                              double2 *spec, uint64_t spec_stride, cudaStream_t s, double2 *k1_out = nullptr)
 {
+    // k1_out: stop after K1, its output for seed k at k1_out + k M (the fresh-seed K2's input)
     RouteA &a = h->a;
     const Geometry &g = a.g;
     const dim3 g0((g.N1 + k0_cols(g) - 1) / k0_cols(g), (g.N2 + k0_rows(g) - 1) / k0_rows(g), count);
@@ -1894,12 +2010,14 @@ static void ra_seed_transform(pa_ctx *h, const uint32_t *seeds, uint64_t seed_st
         const uint32_t tiles = (g.N1 / g.C) * count;
         const uint32_t slots = g.k1p_tcols == 256 ? 2 * 148 : 148;
         launch_pdl(kK13[g.k13].k1p, dim3(tiles < slots ? tiles : slots), dim3(g.k1p_t), g.smem1p, s,
-                   (const uint32_t *)a.kb, a.buf, g, a.T, (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0, count);
+                   (const uint32_t *)a.kb, k1_out ? k1_out : a.buf, g, a.T, (uint32_t *)nullptr, (uint64_t)0,
+                   (uint64_t)0, count);
     } else {
-        launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, (const uint32_t *)a.kb, a.buf, g, a.T,
-                   (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0, (const uint32_t *)nullptr, (uint64_t)0,
-                   (uint64_t)0);
+        launch_pdl(kK13[g.k13].k1, dim3(g.N1 / g.C, count), g.t1, g.smem1, s, (const uint32_t *)a.kb,
+                   k1_out ? k1_out : a.buf, g, a.T, (uint32_t *)nullptr, (uint64_t)0, (uint64_t)0,
+                   (const uint32_t *)nullptr, (uint64_t)0, (uint64_t)0);
     }
+    if (k1_out) return;
     if (g.k2shape)
         launch_pdl(kK2[g.k2shape].seed, dim3(count, g.N2), k2_threads(g, count), g.smem2, s, a.buf, a.buf, spec, g, a.T, spec_stride);
     else
@@ -1938,6 +2056,8 @@ pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
         if (f.fn && ((e = cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit)) !=
                          cudaSuccess ||
                      (e = cudaFuncSetAttribute(f.seed, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kSmemLimit)) != cudaSuccess ||
+                     (e = cudaFuncSetAttribute(f.fresh, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)kSmemLimit)) != cudaSuccess))
             return cuda_fail(e, "route (a) cudaFuncSetAttribute");
     attr_done.fetch_or(bit);
@@ -2005,8 +2125,9 @@ uint32_t ra_batch_keys(const pa_ctx *h)
 
 pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, uint32_t *outs,
                         uint64_t out_stride, uint32_t count, uint64_t zero_words, cudaStream_t s,
-                        const double2 *spec, uint64_t spec_stride)
+                        const double2 *spec, uint64_t spec_stride, bool fresh)
 {
+    // fresh: `spec` holds the seeds' K1 output (k2_rows_t<..., kFresh>), not spectra
     pa_status st = ra_reserve(h, count, s);
     if (st != PA_OK) return st;
     RouteA &a = h->a;
@@ -2034,7 +2155,14 @@ pa_status ra_hash_batch(pa_ctx *h, const uint32_t *keys, uint64_t key_stride, ui
         const dim3 g2(count, g.N2);
         const double2 *sp = spec ? spec : a.spec;  // fresh seeds: one spectrum per key
         const uint64_t ss = spec ? spec_stride : 0;
-        if (g.k2shape)
+        if (fresh) {
+            Geometry gf = g;  // the last key's spectrum row also lands in the handle's spectrum
+            gf.fout = a.spec;
+            gf.fkey = count - 1;
+            launch_pdl(kK2[g.k2shape].fresh, g2, k2_threads(g, count), g.smem2 + 16, s, a.buf, a.buf2,
+                       const_cast<double2 *>(sp), gf, a.T, ss);
+        }
+        else if (g.k2shape)
             launch_pdl(kK2[g.k2shape].fn, g2, k2_threads(g, count), g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, ss);
         else
             launch_pdl(k2_rows, g2, k2_threads(g, count), g.smem2, s, a.buf, a.buf2, const_cast<double2 *>(sp), g, a.T, 0, 1.0, ss);
@@ -2088,11 +2216,15 @@ pa_status ra_fresh_batch(pa_ctx *h, const uint32_t *seeds, uint64_t seed_stride,
     }
     for (uint32_t k0 = 0; k0 < count; k0 += chunk) {
         const uint32_t c = std::min(chunk, count - k0);
-        ra_seed_transform(h, seeds + k0 * seed_stride, seed_stride, c, a.fspec, g.M, s);
+        // the seed's forward half inside the hash's K2 (spectra in TMEM, never in HBM) where it
+        // fits; that K2 also writes the chunk's last spectrum into the handle's (every chunk: the
+        // last one's stays)
+        const bool fused = g.k2fresh && k2f_fits(g, k2_threads(g, c));
+        ra_seed_transform(h, seeds + k0 * seed_stride, seed_stride, c, a.fspec, g.M, s, fused ? a.fspec : nullptr);
         if ((st = ra_hash_batch(h, keys + k0 * key_stride, key_stride, outs + k0 * out_stride, out_stride, c,
-                                zero_words, s, a.fspec, g.M)) != PA_OK)
+                                zero_words, s, a.fspec, g.M, fused)) != PA_OK)
             return st;
-        if (k0 + c == count) {
+        if (!fused && k0 + c == count) {
             cudaError_t e = cudaMemcpyAsync(a.spec, a.fspec + (size_t)(c - 1) * g.M, spec_bytes,
                                             cudaMemcpyDeviceToDevice, s);
             if (e != cudaSuccess) return cuda_fail(e, "fresh-seed spectrum copy");
