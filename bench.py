@@ -651,20 +651,23 @@ def sweep(torch, pa, dev, steps=10):
     res["C5a_batched_e2e"] = {"n": n, "m": m, "keys": C5_KEYS, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
                               "note": "pa_hash_host_batch: pinned host keys in, host outputs out"}
     h.close()
-    # fresh seed per key (NEXT-2): seed transform + hash per key, C2 shape
-    n, m, sw, kw = syn.config_inputs("C2")
-    count = 64
-    seeds = syn.random_bits_torch([syn.seed_stream(900 + k) for k in range(count)], n + m - 1, dev)
-    keys = syn.random_bits_torch([syn.key_stream(2, k) for k in range(count)], n, dev)
-    h = pa.Hasher(n, m, seeds[0])
-    outs = h.new_out(count)
-    h.hash_fresh_batch(seeds, keys, outs)
-    ms = time_steps(torch, lambda: h.hash_fresh_batch(seeds, keys, outs), 3, flush)
-    t = float(np.mean(ms)) / count
-    res["C2_fresh_seed"] = {"n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
-                            "note": "pa_hash_fresh_batch: a distinct seed per key (seed transforms batched "
-                                    "into per-key spectra, then the keys hashed as one batch)"}
-    h.close()
+    # fresh seed per key (NEXT-2): seed transform + hash per key, C2 and C4 shapes
+    for cname, count in (("C2", 64), ("C4", 4)):
+        n, m, sw, kw = syn.config_inputs(cname)
+        ci = syn.CONFIG_INDEX[cname]
+        seeds = syn.random_bits_torch([syn.seed_stream(900 + k) for k in range(count)], n + m - 1, dev)
+        keys = syn.random_bits_torch([syn.key_stream(ci, k) for k in range(count)], n, dev)
+        h = pa.Hasher(n, m, seeds[0])
+        outs = h.new_out(count)
+        h.hash_fresh_batch(seeds, keys, outs)
+        ms = time_steps(torch, lambda: h.hash_fresh_batch(seeds, keys, outs), 3, flush)
+        t = float(np.mean(ms)) / count
+        res[f"{cname}_fresh_seed"] = {
+            "n": n, "m": m, "keys": count, "ms_per_key": t, "gbit_s": n / (t * 1e-3) / 1e9,
+            "note": "pa_hash_fresh_batch: a distinct seed per key (each seed's forward half fused into "
+                    "the hash's K2, its spectrum row held in TMEM)"}
+        h.close()
+        del seeds, keys, outs
     # create time (SURVEY 8(d) timing protocol: pa_create timed separately): C4 seed transform
     n, m, sw, _ = syn.config_inputs("C4")
     seed_t = dev_words(torch, sw, dev)
