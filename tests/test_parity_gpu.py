@@ -570,6 +570,38 @@ def test_hash_fresh_batch_per_key_seeds(route, maxlen, count):
     assert np.array_equal(after, oracle.unpack(oracle.toeplitz_words(n, m, seeds[-1], probe), m))
 
 
+@pytest.mark.parametrize("n,m,count", [(250_007, 62_000, 3), (20_000_003, 4_000_000, 2), (50_000_017, 5_000_001, 2)])
+def test_hash_fresh_batch_fused_k2_shapes(n, m, count):
+    """The fresh-seed K2 (each seed's forward half in the hash's K2, its spectrum row held in
+    TMEM) on the row shapes 2048 = [8, 16, 16] (two CTAs per SM, 256 TMEM columns each),
+    6144 = [3, 8, 16, 16] and 10240 = [5, 8, 16, 16] (one CTA per SM, 512 columns, two last-stage
+    butterflies per thread): every key against its own seed, and the handle afterwards holds the
+    last seed (the spectrum row the last key's CTAs wrote).  Full outputs at the small shape,
+    sampled rows (both ends + random) at the large ones."""
+    L = n + m - 1
+    seeds = [syn.random_bits(syn.seed_stream(150 + k), L) for k in range(count)]
+    keys = [syn.random_bits(syn.key_stream(150, k), n) for k in range(count)]
+    probe = syn.random_bits(syn.key_stream(151, 0), n)
+    st, kt = torch.stack([to_dev(s) for s in seeds]), torch.stack([to_dev(k) for k in keys])
+    with pa.Hasher(n, m, to_dev(syn.random_bits(syn.seed_stream(149), L)), route="transform") as h:
+        outs = h.hash_fresh_batch(st, kt)
+        after = from_dev(h.hash(to_dev(probe)), m)
+        assert h.residual() < 0.25
+        torch.cuda.synchronize()
+    full = n * m <= 2 * 10**10
+    rows = sample_rows(m, 29, 384)
+    for k in range(count):
+        got = from_dev(outs[k], m)
+        if full:
+            assert np.array_equal(got, oracle.unpack(oracle.toeplitz_words(n, m, seeds[k], keys[k]), m)), k
+        else:
+            assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, seeds[k], keys[k], rows)), k
+    if full:
+        assert np.array_equal(after, oracle.unpack(oracle.toeplitz_words(n, m, seeds[-1], probe), m))
+    else:
+        assert np.array_equal(after[rows], oracle.toeplitz_rows(n, m, seeds[-1], probe, rows))
+
+
 @pytest.mark.parametrize("n,m,off,count,kwargs", [(120_001, 30_000, 77, 9, {}), (1_000_003, 250_000, 5, 4, {}),
                                                    (50_001, 9_000, 3, 6, {"batch_keys": 2})])
 def test_hash_fresh_batch_seed_offset_and_workspace(n, m, off, count, kwargs):
