@@ -463,10 +463,12 @@ def run_ours(args):
                     if world == 1 else
                     "rank 0: pinned key H2D, NCCL broadcast (rows) / scatter of key blocks (cols), sharded "
                     "hash and merge collectives, y D2H; CUDA events, max over ranks",
-                    "single_call": {"value": n / (e2e_mean * 1e-3) / 1e9, "steps": e2e_steps,
+                    "single_call": {"value": n / (float(np.median(e2e_ms)) * 1e-3) / 1e9,
+                                    "mean_value": n / (e2e_mean * 1e-3) / 1e9, "steps": e2e_steps,
                                     "how": "one key per pa_hash_host_async call (CUDA graph: pinned host key -> "
                                            "copy kernel -> K0..K3 -> copy kernel -> pinned host output), "
-                                           "CUDA events around each step"} if world == 1 else None},
+                                           "CUDA events around each step; value from the median step, "
+                                           "mean_value from the mean"} if world == 1 else None},
             "gpu_launches": args.steps * (info["kernels_per_hash"] + (1 if split == "cols" else 0)),
             "clocks": clk.result(),
         }
