@@ -6,7 +6,9 @@ its body in a child process with PA_LIB pointing at that build and the PA_* over
   * PA_K3T=1  -- the persistent TMEM-staged K3 (loader warps ld.global -> tcgen05.st, compute
                  warps tcgen05.ld -> shared memory), measured slower, off by default;
   * PA_LR=1   -- the row-block work-array layout between K2 and K3;
-  * PA_FORCE_PLAN / PA_K3_HALF -- forced plans that exercise K3's half-width column groups.
+  * PA_FORCE_PLAN / PA_K3_HALF -- forced plans that exercise K3's half-width column groups;
+  * PA_K1P=0 / PA_K2_FRESH=0 -- the plain K1 and the per-key-spectra fresh-seed path, each
+                 bit-identical to the product path it replaces.
 """
 import json
 import os
@@ -185,3 +187,31 @@ def test_k1p_matches_plain_k1(count, tmp_path):
     rows = np.unique(np.random.default_rng(7).integers(0, m, 128))
     got = oracle.unpack(outs[count - 1].view(np.uint32), m)
     assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kk, rows))
+
+
+def body_fresh(n, m, count, out):
+    """pa_hash_fresh_batch of `count` keys against their own seeds; save outputs + residual."""
+    import numpy as np
+
+    import pa_synth as syn
+    L = n + m - 1
+    seeds = syn.random_bits_torch([syn.seed_stream(190 + k) for k in range(count)], L, "cuda")
+    keys = syn.random_bits_torch([syn.key_stream(190, k) for k in range(count)], n, "cuda")
+    import paper_1805_02372_b200 as pa
+    with pa.Hasher(n, m, seeds[0], route="transform") as h:
+        outs = h.hash_fresh_batch(seeds, keys).cpu().numpy()
+        np.save(out, np.concatenate([outs.reshape(-1).view(np.uint32),
+                                     np.array([h.residual()]).view(np.uint32)]))
+
+
+@pytest.mark.parametrize("n,m,count", [(1_000_003, 250_000, 5), (50_000_017, 5_000_001, 2)])
+def test_fresh_fused_matches_spectra_path(n, m, count, tmp_path):
+    """The fused fresh-seed K2 (seed forward half in the hash's K2, spectrum row in TMEM; product
+    path) and the per-key spectra path (PA_K2_FRESH=0: seed K2 writes spectra to HBM, the hash's
+    K2 reads them) perform the same FP64 operations in the same order: identical outputs and the
+    identical residual, bit for bit."""
+    import numpy as np
+    f1, f0 = str(tmp_path / "fused.npy"), str(tmp_path / "spectra.npy")
+    body_fresh(n, m, count, f1)
+    run_child("body_fresh", {"n": n, "m": m, "count": count, "out": f0}, {"PA_K2_FRESH": "0"})
+    assert np.array_equal(np.load(f1), np.load(f0))
