@@ -175,11 +175,13 @@ pa_status pa_set_seed(pa_handle h, const uint32_t *seed_bits, void *stream);
  * new uniform seed): for k < count, rebind the handle to seed k (seeds +
  * k*seed_stride_words, n+m-1 bits at the handle's seed_bit_offset) and hash key k into
  * output k -- the result of pa_set_seed + pa_hash per key, i.e. three transforms per key on
- * route (a).  An unsplit route-(a) handle without a workspace transforms the seeds of a chunk of
- * keys as one batch into per-key spectra (extra device memory: chunk x the spectrum, grown on
- * demand) and hashes the chunk's keys as one batch; otherwise (or if that memory is not
- * available) one key at a time.  Strides in uint32 words, multiples of 4.  Afterwards the
- * handle holds the last seed. */
+ * route (a).  An unsplit route-(a) handle without a workspace, given two keys or more, runs the
+ * seeds of a chunk of keys through K0/K1 as one batch into a second work array (extra device
+ * memory: chunk x 16 M bytes, grown on demand) and hashes the chunk's keys as one batch whose K2
+ * runs each seed's forward half itself, the spectrum row held in tensor memory (where that K2
+ * does not apply, the chunk's seeds are transformed into per-key spectra first); otherwise (or
+ * if the memory is not available) one key at a time.  Strides in uint32 words, multiples of 4.
+ * Afterwards the handle holds the last seed. */
 pa_status pa_hash_fresh_batch(pa_handle h, const uint32_t *seeds, uint64_t seed_stride_words,
                               const uint32_t *keys, uint64_t key_stride_words, uint32_t *outs,
                               uint64_t out_stride_words, uint32_t count, void *stream);
