@@ -812,7 +812,7 @@ k2_rows(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, Rou
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
-    if (g.pfs && mode == 0) l2_prefetch_row(sp, N1);
+    if (g.pfs && mode == 0 && (blockIdx.x == 0 || spec_stride)) l2_prefetch_row(sp, N1);  // see k2_rows_t
     grid_dep_wait();  // K1's work array
     const FftPlan &P0 = g.f1;
     if (P0.S <= 1) {  // tiny rows: stage through shared memory
@@ -942,7 +942,11 @@ k2_rows_t(double2 *buf, double2 *out2, double2 *__restrict__ spec, Geometry g, R
         const double2 *rt0 = T.rho + (size_t)row * (64 + g.f1.nhi);
         load_tables_async(rlo, rhi, rt0, rt0 + 64, g.f1.nhi);
     }
-    if (KM == kHash && g.pfs) l2_prefetch_row(sp, N1);  // this row's spectrum, pulled in under the forward stages
+    // this row's spectrum, pulled into L2 under the forward stages -- by the first key's CTA only
+    // (unless each key has its own spectrum): a batch's CTAs of one row run back to back and share
+    // it (C5d x 16: 881.8 -> 867.8 us per key with no prefetch at all, whereas a single C4 key
+    // needs it: 2179 -> 2219 us without)
+    if (KM == kHash && g.pfs && (blockIdx.x == 0 || spec_stride)) l2_prefetch_row(sp, N1);
     // kFresh: TMEM for the spectrum row (256 columns when two CTAs share the SM, else 512)
     uint32_t *tmb = reinterpret_cast<uint32_t *>(rhi + g.f1.nhi);
     const uint32_t tcols = k2f_tcols(g, blockDim.x);
