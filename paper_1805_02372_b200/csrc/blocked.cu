@@ -55,19 +55,33 @@ unsigned grid_for(uint64_t words)
     return (unsigned)(b == 0 ? 1 : (b < 4096 ? b : 4096));
 }
 
-// Block shape for a transform-length limit: (nb, mb) multiples of 32 with nb + mb - 1 <= lim.
-// One row block when m fits half the limit, else square-ish blocks (the work (m/mb)(n/nb)(nb+mb)
-// is smallest at nb = mb).
+// Block shape for a transform-length limit: (nb, mb) multiples of 32 with nb + mb - 1 <= lim,
+// the one with the least transform work: k row blocks of mb = m / k rows and the longest key
+// blocks that fit, work = k * ceil(n / nb) * (nb + mb), over k = 1 .. 64 (one row block whenever
+// m fits with room for key blocks -- e.g. m = 10^8, lim = 1.6 * 10^8: 17 blocks of 1.6 * 10^8
+// against 26 for square 8 * 10^7 blocks).
 bool block_shape(uint64_t n, uint64_t m, uint64_t lim, uint64_t *nb, uint64_t *mb)
 {
-    const uint64_t mr = (m + 31) / 32 * 32;
-    if (mr + 31 <= lim / 2 || (lim > mr && mr + 64 <= lim - mr)) *mb = mr;
-    else *mb = (lim / 2) / 32 * 32;
-    if (*mb < 32 || *mb + 31 > lim) return false;
-    uint64_t x = (lim + 1 - *mb) / 32 * 32;
     const uint64_t nr = (n + 31) / 32 * 32;
-    *nb = std::min(x, nr);
-    return *nb >= 32;
+    double best = 0.0;
+    bool found = false;
+    for (uint64_t k = 0; k <= 64; ++k) {
+        // k >= 1: m split into k row blocks; k = 0: square blocks of half the limit (the only
+        // shape once the limit is far below m)
+        const uint64_t mbk = k ? ((m + k - 1) / k + 31) / 32 * 32 : std::min((lim / 2) / 32 * 32, (m + 31) / 32 * 32);
+        if (mbk < 32 || mbk + 31 > lim) continue;
+        const uint64_t nbk = std::min((lim + 1 - mbk) / 32 * 32, nr);
+        if (nbk < 32) continue;
+        const double work = (double)((m + mbk - 1) / mbk) * (double)((nr + nbk - 1) / nbk) * (double)(nbk + mbk);
+        if (!found || work < best) {
+            best = work;
+            *nb = nbk;
+            *mb = mbk;
+            found = true;
+        }
+        if (k && mbk == 32) break;
+    }
+    return found;
 }
 
 struct Staging {
@@ -301,10 +315,8 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
     return res;
 }
 
-// default block limit: the whole product if one handle can plan it, else the longest
-// transform the planner accepts (binary search over n' + m' - 1)
-// default block limit: the longest blocks whose (nb, mb) shape route (a) plans as ONE transform
-// (a block that itself needed the in-handle Eq. (4) split would transform its seed windows twice)
+// A block shape route (a) plans as ONE transform (a block that itself needed the in-handle
+// Eq. (4) split would transform its seed windows twice).
 static bool one_plan(uint64_t n, uint64_t m, uint64_t lim)
 {
     uint64_t nb, mb;
@@ -313,6 +325,11 @@ static bool one_plan(uint64_t n, uint64_t m, uint64_t lim)
     char err[256];
     return ra_plan(nb, mb, &g, err, sizeof err, 0) == PA_OK;
 }
+// default block limit: the longest blocks whose (nb, mb) shape route (a) plans as one transform.
+// Pricing shorter limits by the cost model instead (blocks x (hash + seed transform)) picked
+// 2-3 * 10^8-bit blocks it rated 25-30% cheaper that measured 25-45% slower (n = 10^9, m = 10^8:
+// 98 ms at the longest, 125-146 ms at the model's picks): the model is calibrated on shapes up
+// to ~1.3 * 10^8 points and misjudges the one-column, general-kernel plans of the longest blocks.
 static uint64_t default_limit(uint64_t n, uint64_t m)
 {
     if (one_plan(n, m, n + m - 1)) return n + m - 1;
