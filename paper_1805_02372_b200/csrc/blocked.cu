@@ -23,6 +23,8 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <cmath>
+#include <map>
 #include <mutex>
 
 #include "bits.cuh"
@@ -220,13 +222,20 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
             x = cudaMemsetAsync(st.seed[i], 0, 4 * st.sw, cs);
         if (x == cudaSuccess && wb > wa)
             x = cudaMemcpyAsync(st.seed[i] + (wa - w0), seed_bits + wa, 4 * (wb - wa), kin, cs);
-        if (x == cudaSuccess && wb > wa && (uint64_t)wb == SW)  // bits past n+m-1 of the last seed word
-            k_mask_from<<<1, 32, 0, cs>>>(st.seed[i] + (wa - w0), (uint64_t)(wb - wa),
-                                          (n + m - 1) - 32 * (uint64_t)wa);
+        if (x == cudaSuccess && wb > wa && (uint64_t)wb == SW) {  // bits past n+m-1 of the last seed word
+            // only the words from the one holding bit n+m-1 on (masking the whole window with one
+            // warp cost ~7 ms per 3 * 10^8-bit block)
+            const uint64_t rel = (n + m - 1) - 32 * (uint64_t)wa, q = rel / 32;
+            if (q < (uint64_t)(wb - wa))
+                k_mask_from<<<1, 32, 0, cs>>>(st.seed[i] + (wa - w0) + q, (uint64_t)(wb - wa) - q, rel - 32 * q);
+        }
         const uint64_t ka = c0 / 32, kb = std::min<uint64_t>(KW, ka + nb / 32);
         if (x == cudaSuccess && kb - ka < nb / 32) x = cudaMemsetAsync(st.key[i], 0, 4 * st.kw, cs);
         if (x == cudaSuccess) x = cudaMemcpyAsync(st.key[i], key_bits + ka, 4 * (kb - ka), kin, cs);
-        if (x == cudaSuccess && kb == KW) k_mask_from<<<grid_for(kb - ka), 256, 0, cs>>>(st.key[i], kb - ka, n - c0);
+        if (x == cudaSuccess && kb == KW) {  // key bits past n: the words from the one holding bit n on
+            const uint64_t q = (n - c0) / 32;
+            if (q < kb - ka) k_mask_from<<<1, 32, 0, cs>>>(st.key[i] + q, kb - ka - q, n - c0 - 32 * q);
+        }
         if (x == cudaSuccess) x = cudaGetLastError();
         if (x == cudaSuccess) x = cudaEventRecord(ev_in[i], cs);
         return x == cudaSuccess ? PA_OK : cuda_fail(x, who);
@@ -325,12 +334,27 @@ static bool one_plan(uint64_t n, uint64_t m, uint64_t lim)
     char err[256];
     return ra_plan(nb, mb, &g, err, sizeof err, 0) == PA_OK;
 }
-// default block limit: the longest blocks whose (nb, mb) shape route (a) plans as one transform.
-// Pricing shorter limits by the cost model instead (blocks x (hash + seed transform)) picked
-// 2-3 * 10^8-bit blocks it rated 25-30% cheaper that measured 25-45% slower (n = 10^9, m = 10^8:
-// 98 ms at the longest, 125-146 ms at the model's picks): the model is calibrated on shapes up
-// to ~1.3 * 10^8 points and misjudges the one-column, general-kernel plans of the longest blocks.
+// default block limit: among limits from the longest block route (a) plans as one transform down
+// to a third of it, the one whose blocks the cost model prices cheapest in total -- blocks x
+// (hash + seed transform ~ 0.57 hash, measured at C4) + a per-block fixed cost (launches, copy
+// latency).  The longest block is not always the fastest: its plans tend to general kernels.
+static uint64_t default_limit_search(uint64_t n, uint64_t m);
+// the search plans ~80 shapes (~20 ms of host time): remembered per (n, m) for the process
 static uint64_t default_limit(uint64_t n, uint64_t m)
+{
+    static std::mutex mu;
+    static std::map<std::pair<uint64_t, uint64_t>, uint64_t> memo;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = memo.find({n, m});
+        if (it != memo.end()) return it->second;
+    }
+    const uint64_t lim = default_limit_search(n, m);
+    std::lock_guard<std::mutex> lock(mu);
+    memo[{n, m}] = lim;
+    return lim;
+}
+static uint64_t default_limit_search(uint64_t n, uint64_t m)
 {
     if (one_plan(n, m, n + m - 1)) return n + m - 1;
     uint64_t lo = 64, hi = n + m - 1;
@@ -339,7 +363,37 @@ static uint64_t default_limit(uint64_t n, uint64_t m)
         if (one_plan(n, m, mid)) lo = mid;
         else hi = mid;
     }
-    return lo;
+    uint64_t pick = lo;
+    double best = 1e300;
+    auto price = [&](uint64_t L, Geometry *g) -> bool {
+        uint64_t nb, mb;
+        if (L < 64 || L > lo || !block_shape(n, m, L, &nb, &mb)) return false;
+        char err[256];
+        if (ra_plan(nb, mb, g, err, sizeof err, 0) != PA_OK) return false;
+        const double blocks = (double)((m + mb - 1) / mb) * (double)((n + nb - 1) / nb);
+        const double t = blocks * (1.57 * ra_last_plan_cost() * (ra_plan_specialised(*g) ? 1.0 : 1.2) + 30e-6);
+        if (const char *e = dev_env("PA_BLOCKED_DEBUG"); e && atoi(e))
+            fprintf(stderr, "blocked: model %8.2f ms lim %llu -> nb %llu mb %llu plan %ux%u C=%u spec %d blocks %.0f\n",
+                    t * 1e3, (unsigned long long)L, (unsigned long long)nb, (unsigned long long)mb, g->N1, g->N2, g->C,
+                    (int)ra_plan_specialised(*g), blocks);
+        if (t < best) {
+            best = t;
+            pick = L;
+        }
+        return true;
+    };
+    for (int i = 0; i < 48; ++i) {
+        const uint64_t L = (uint64_t)((double)lo * std::pow(0.977, i));
+        Geometry g;
+        if (L < 64) break;
+        if (!price(L, &g)) continue;
+        // and the longest block the same plan holds (2 N1 N2 points): fewer blocks at no cost
+        Geometry g2;
+        price(2ull * g.N1 * g.N2, &g2);
+    }
+    if (const char *e = dev_env("PA_BLOCKED_DEBUG"); e && atoi(e))
+        fprintf(stderr, "blocked: pick lim %llu (longest %llu)\n", (unsigned long long)pick, (unsigned long long)lo);
+    return pick;
 }
 
 extern "C" pa_status pa_hash_blocked(uint64_t n, uint64_t m, const uint32_t *seed_bits,

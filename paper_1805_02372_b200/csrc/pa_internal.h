@@ -180,6 +180,8 @@ namespace pa {
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len = 0,
                   const PlanChoice *force = nullptr);
 // the cost model's distinct candidate plans, cheapest first (PA_PLAN_MEASURE)
+double ra_last_plan_cost();
+bool ra_plan_specialised(const Geometry &g);
 int ra_plan_candidates(uint64_t n, uint64_t m, uint64_t max_len, PlanChoice *out, int max);
 pa_status ra_create(pa_ctx *h, const uint32_t *seed, cudaStream_t s);
 pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s);

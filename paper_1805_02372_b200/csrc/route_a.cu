@@ -1587,6 +1587,13 @@ static void keep_cand(const PlanCand &c)
     if (c.cost < g_cand[worst].cost) g_cand[worst] = c;
 }
 
+// the cost model's time (seconds per hash) of the plan the last ra_plan call on this thread chose
+static thread_local double g_plan_cost = 0.0;
+double ra_last_plan_cost() { return g_plan_cost; }
+// whether a planned (N1, N2) runs the shape-specialised K2 and K1 / K3 (the kernels the cost
+// model is calibrated on; the general ones measured 16-23% slower per point on 10^8-point plans)
+bool ra_plan_specialised(const Geometry &g);
+
 pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen, uint64_t max_len,
                   const PlanChoice *force)
 {
@@ -1652,7 +1659,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             // K1 runs as the persistent TMEM write-behind K1P on one-CTA-per-SM multi-wave plans
             // (C4: K1 735 -> 670 us; the calibration sweep, tools/dev/plan_calib.py, found the
             // model preferring two-CTA C = 2 plans over faster K1P C = 4 ones without this)
-            const bool k1p = spec13 && occ13 == 1 && C < 16 && N1 / C >= 2 * 148u && p2.S >= 3 &&
+            const bool k1p = spec13 && occ13 == 1 && C >= 2 && C < 16 && N1 / C >= 2 * 148u && p2.S >= 3 &&
                              p2.st[p2.S - 1].R == 16;
             // (a grid refit of the throughput scales on 70 random single-key lengths x 12 plans,
             // tools/dev/plan_refit.py, cut the mean regret 2.9% -> 1.6% there but lost on held-out
@@ -1670,6 +1677,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
             }
             if (cost < best) {
                 best = cost;
+                g_plan_cost = cost;
                 found = true;
                 g->M = (uint64_t)N1 * N2;
                 g->N1 = N1;
@@ -1824,7 +1832,9 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         g->pfs = e ? (uint32_t)atoi(e) : g->t2 == PA_TMAX ? 1u : 0u;
     }
     // K1P (persistent K1, finished tiles written behind through TMEM, k1p_fwd_columns): one CTA of
-    // 512 threads per SM, a multi-wave grid, a shape-specialised plan ending in radix 16 whose
+    // 512 threads per SM, a multi-wave grid, column groups of C >= 2 (at C = 1 its 16-byte drain
+    // stores are partial-sector writes nothing merges: a 12288 x 12288 plan's K1 took 6.37 ms
+    // against 2.48 ms for the plain K1), a shape-specialised plan ending in radix 16 whose
     // last-stage outputs fit the 512 TMEM columns (<= 2 butterflies per thread), and K0's bit
     // streams (not the C = 16 direct gather).  Developer override PA_K1P=0.
     g->k1p_kmax = 0;
@@ -1847,7 +1857,7 @@ pa_status ra_plan(uint64_t n, uint64_t m, Geometry *g, char *err, size_t errlen,
         const uint32_t nbl = g->f2.S ? (g->f2.st[g->f2.S - 1].nb << g->logC) : 0;
         const uint32_t kmax = (nbl + g->k1p_t - 1) / g->k1p_t;
         if ((!e || atoi(e) != 0) && g->k13 && g->f2.S >= 3 && g->f2.st[g->f2.S - 1].R == 16 &&
-            (g->t1 == PA_TMAX || two) && g->C < 16 && kmax >= 1 &&
+            (g->t1 == PA_TMAX || two) && g->C >= 2 && g->C < 16 && kmax >= 1 &&
             (g->k1p_t / 128) * kmax * 64 <= g->k1p_tcols && g->smem1p + 64 <= kSmemLimit &&
             g->N1 / g->C >= 2 * 148u * (two ? 2u : 1u))
             g->k1p_kmax = kmax;
@@ -2262,6 +2272,13 @@ void ra_destroy(pa_ctx *h)
 
 namespace pa {
 // The cost model's distinct candidate plans for (n, m), cheapest first (measured planning).
+bool ra_plan_specialised(const Geometry &g)
+{
+    FftPlan p1, p2, p2a;
+    if (!make_plan(g.N1, &p1) || !make_plan(g.N2, &p2)) return false;
+    return k2_shape(p1) && (k13_shape(p2) || (make_plan(g.N2, &p2a, 16, true) && k13_shape(p2a)));
+}
+
 int ra_plan_candidates(uint64_t n, uint64_t m, uint64_t max_len, PlanChoice *out, int max)
 {
     Geometry g;
