@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <cmath>
 #include <new>
 #include <tuple>
 #include <string>
@@ -363,6 +364,47 @@ static bool plan_fits(uint64_t n, uint64_t m, uint64_t maxlen)  // route (a) can
     return ra_plan(n, m, &g, err, sizeof err, maxlen) == PA_OK;
 }
 
+// The automatic split's block length: the longest blocks one plan holds are not the fastest
+// (their plans are one-column, general-kernel ones).  Among caps from kMaxPlanLen down to a
+// third of it -- each also stretched to the longest block its plan holds, 2 N1 N2 -- take the
+// one the cost model prices cheapest as key blocks x model time per hash (x 1.2 for plans
+// without the shape-specialised kernels; measured n = 3e8, m = 3e7: see DESIGN.md Sec. 6d).
+// Memoised per (n, m): ~80 plans per search.
+static uint64_t auto_cap(uint64_t n, uint64_t m)
+{
+    static std::mutex mu;
+    static std::map<std::pair<uint64_t, uint64_t>, uint64_t> memo;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = memo.find({n, m});
+        if (it != memo.end()) return it->second;
+    }
+    uint64_t pick = kMaxPlanLen;
+    double best = 1e300;
+    auto price = [&](uint64_t L, Geometry *g) -> bool {
+        if (L > kMaxPlanLen || L + 1 < m + 128) return false;
+        uint64_t nb = (L + 1 - m) / 128 * 128;
+        if (nb >= n) nb = (n + 127) / 128 * 128;
+        char err[256];
+        if (ra_plan(nb, m, g, err, sizeof err, kMaxPlanLen) != PA_OK) return false;
+        const double t = (double)((n + nb - 1) / nb) * ra_last_plan_cost() * (ra_plan_specialised(*g) ? 1.0 : 1.2);
+        if (t < best) {
+            best = t;
+            pick = L;
+        }
+        return true;
+    };
+    for (int i = 0; i < 48; ++i) {
+        const uint64_t L = (uint64_t)((double)kMaxPlanLen * std::pow(0.977, i));
+        Geometry g, g2;
+        if (!price(L, &g)) continue;
+        price(std::min<uint64_t>(2ull * g.N1 * g.N2, kMaxPlanLen), &g2);
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    memo[{n, m}] = pick;
+    return pick;
+}
+
 // Eq. (4) column blocks for a transform-length cap: equal blocks of nb key
 // bits (a multiple of 128, so every block's key pointer stays 16-byte aligned) and a
 // shorter last one.  c0 receives the block starts; one entry = no split.
@@ -371,10 +413,10 @@ static pa_status split_plan(uint64_t n, uint64_t m, uint64_t maxlen, std::vector
     c0->assign(1, 0);
     if (!maxlen) {
         // no cap requested: split only when no single transform can be planned (n + m beyond
-        // ~3.5e8 bits -- the paper's length-compatible regime), with the blocks as
-        // long as one plan allows
+        // ~3.5e8 bits -- the paper's length-compatible regime), with the block length
+        // the cost model prices cheapest (auto_cap)
         if (plan_fits(n, m, 0)) return PA_OK;
-        maxlen = kMaxPlanLen;
+        maxlen = auto_cap(n, m);
     }
     if (plan_fits(n, m, maxlen)) return PA_OK;
     if (maxlen + 1 < m + 128) {
