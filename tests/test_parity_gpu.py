@@ -761,6 +761,28 @@ def test_auto_split_gigabit_key():
     assert bad.size == 0, f"{bad.size} wrong bits, first {bad[:8]}"
 
 
+@pytest.mark.parametrize("n,m", [(400_000_007, 4_000_001), (300_000_011, 30_000_007)])
+def test_auto_split_priced_block_length(n, m):
+    """Keys just beyond one plan: the automatic Eq. (4) split takes the block length the cost
+    model prices cheapest (shorter blocks with the shape-specialised kernels, not the longest
+    one-column plans).  Every output bit of the all-ones key against the prefix-XOR closed form,
+    sampled rows of a random key against the oracle."""
+    sw = syn.random_bits(syn.seed_stream(98), n + m - 1)
+    kw = syn.random_bits(syn.key_stream(98, 0), n)
+    with pa.Hasher(n, m, to_dev(sw)) as h:
+        assert h.info["column_blocks"] > 1 and h.route == "transform", h.info
+        got = from_dev(h.hash(to_dev(kw)), m)
+        got_ones = from_dev(h.hash(to_dev(syn.ones_bits(n))), m)
+        torch.cuda.synchronize()
+        assert h.residual() < 1e-3
+    rows = sample_rows(m, 98, k=384)
+    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+    s01 = oracle.unpack(sw, n + m - 1)
+    P = np.zeros(n + m, dtype=np.uint8)
+    np.bitwise_xor.accumulate(s01, out=P[1:])
+    assert np.array_equal(got_ones, P[n:n + m] ^ P[:m])
+
+
 def test_key_and_output_must_not_overlap():
     n, m = 1_000_003, 250_000
     with pa.Hasher(n, m, to_dev(syn.random_bits(syn.seed_stream(99), n + m - 1))) as h:
