@@ -263,14 +263,31 @@ class ColSplit:
             dist.all_gather_object(handles, mine, group=self.group)
         else:
             handles = [mine]
-        ptrs = []
-        for g, hd in enumerate(handles):
-            if g == self.rank:
-                ptrs.append(self.part_ptr)
-            else:
-                p = pa_peer_open(hd)
-                self._opened.append(p)
-                ptrs.append(p)
+        ptrs, err = [], None
+        try:
+            for g, hd in enumerate(handles):
+                if g == self.rank:
+                    ptrs.append(self.part_ptr)
+                else:
+                    p = pa_peer_open(hd)
+                    self._opened.append(p)
+                    ptrs.append(p)
+        except Exception as e:  # noqa: BLE001 - any mapping failure: every rank falls back together
+            err = e
+        if self.world > 1:
+            # all ranks agree on the merge: one rank that cannot map a peer's partial must not leave
+            # the others waiting in a collective the fused path would enter
+            ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+            agreed = bool(ok.item())
+        else:
+            agreed = err is None
+        if not agreed:
+            import warnings
+            warnings.warn(f"fused column split unavailable ({err or 'a peer could not map'}): NCCL merge")
+            self._release_peers()
+            self.fused = False
+            return
         self.ptrs_dev = torch.tensor(ptrs, dtype=torch.int64, device=dev)
         self.myslice = torch.zeros(self.slice_w, dtype=torch.int32, device=dev)
         self.tick = torch.zeros(1, dtype=torch.float32, device=dev)
@@ -334,16 +351,21 @@ class ColSplit:
         dist.all_gather_into_tensor(self.gathered, myslice, group=self.group)
         return self.gathered[: self.words]
 
+    def _release_peers(self):
+        """Unmap the peers' partials and free this rank's (local only: no collective)."""
+        from . import pa_peer_close, pa_peer_free
+        for p in self._opened:
+            pa_peer_close(p)
+        if self.part_ptr:
+            pa_peer_free(self.part_ptr)
+        self._opened, self.part_ptr = [], None
+
     def close(self):
         if self._opened or self.part_ptr:
-            from . import pa_peer_close, pa_peer_free
             torch.cuda.synchronize(self.device)
             if self.world > 1:
                 dist.barrier(group=self.group)  # no peer still reads this rank's partial
-            for p in self._opened:
-                pa_peer_close(p)
-            pa_peer_free(self.part_ptr)
-            self._opened, self.part_ptr = [], None
+            self._release_peers()
         if self.h is not None:
             self.h.close()
 
