@@ -418,8 +418,11 @@ def run_ours(args):
     # N > 1: the other split and the cost model's choice, and C5 key dealing, same protocol
     side = {}
     if world > 1 or args.side_smoke:
-        side = multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush,
-                              split if world > 1 else "cols", name)
+        try:
+            side = multi_gpu_side(args, torch, dist, pa, pd, dev, rank, world, flush,
+                                  split if world > 1 else "cols", name)
+        except Exception as e:  # noqa: BLE001 - the headline above stands; report the side failure
+            side = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     t = torch.tensor([tot_ms, float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
