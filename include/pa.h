@@ -110,7 +110,8 @@ typedef struct pa_options {
                                  multiples of 128 key bits.  PA_ERR_UNSUPPORTED if even a
                                  128-bit block's transform (>= 128 + m - 1) exceeds it.  Ignored
                                  by route (b).  With 0, pa_create splits by itself when n + m is
-                                 beyond one transform (~3.3e8 bits; pa_plan reports the blocks) */
+                                 beyond one transform (~3.3e8 bits; pa_plan reports the blocks),
+                                 at the block length the cost model prices cheapest */
     int32_t arith;            /* pa_arith: AUTO or FP64 (route (a)); NTT32 / NTT64 -> PA_ERR_UNSUPPORTED */
     int32_t device;           /* CUDA device of the handle: -1 (pa_options_init's default) = the
                                  caller's current device at create; >= 0 = that device.  Every
@@ -270,8 +271,10 @@ pa_status pa_profile_read(pa_handle h, pa_kernel_time *out, uint32_t max, uint32
 
 /* Length-compatible hashing for keys whose single transform would be too long
  * (Sec. 3, Fig. 1, Eq. (4)-(7)): T is cut into row blocks of mb rows and
- * key (column) blocks of nb bits, nb + mb - 1 <= max_block_bits (0 = the largest block one
- * handle plans), nb and mb multiples of 32; block (r0, c0) is a Toeplitz hash on the seed window
+ * key (column) blocks of nb bits, nb + mb - 1 <= max_block_bits (0 = library choice: the block
+ * length, up to the largest one handle plans, whose blocks the planner's cost model prices
+ * cheapest in total), nb and mb multiples of 32 with the least total transform work for the
+ * limit; block (r0, c0) is a Toeplitz hash on the seed window
  * at bit r0 + n - c0 - nb (zero-padded before s[0]; the last key block's bits past n and the
  * last row block's rows past m are padding), and each row block's output is the XOR of its
  * column blocks (Eq. (7)).  One handle of the block shape serves every block (pa_set_seed per
