@@ -2033,17 +2033,16 @@ static void ra_seed_transform(pa_ctx *h, const uint32_t *seeds, uint64_t seed_st
     }
     if (k1_out) return;
     if (g.k2shape)
-        launch_pdl(kK2[g.k2shape].seed, dim3(count, g.N2), k2_threads(g, count), g.smem2, s, a.buf, a.buf, spec, g, a.T, spec_stride);
+        launch_pdl(kK2[g.k2shape].seed, dim3(count, g.N2), k2_threads(g, count), g.smem2, s, a.buf, a.buf, spec, g,
+                   a.T, spec_stride);
     else
         launch_pdl(k2_rows, dim3(count, g.N2), k2_threads(g, count), g.smem2, s, a.buf, a.buf, spec, g, a.T, 1,
-                   1.0 / (double)g.M,
-                   spec_stride);
+                   1.0 / (double)g.M, spec_stride);
 }
 
 pa_status ra_seed(pa_ctx *h, const uint32_t *seed, cudaStream_t s)
 {
     RouteA &a = h->a;
-    const Geometry &g = a.g;
     cudaError_t e;
     // the attribute is per device (a process may drive several): set once per device
     static std::atomic<uint64_t> attr_done{0};
