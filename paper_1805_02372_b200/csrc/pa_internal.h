@@ -52,7 +52,7 @@ struct Geometry {
     bool k2fresh;           // pa_hash_fresh_batch fuses the seeds' forward half into K2 (k2_rows_t kFresh)
     double2 *fout;          // kFresh launches: key fkey's spectrum row also goes to fout (the handle's)
     uint32_t fkey;
-    int k2shape;            // K2 as k2_rows_t<R0, R1> (1: 16,16  2: 5,8  3: 3,8  4: 7,4), 0: k2_rows
+    int k2shape;            // K2 as k2_rows_t<R0, R1, NS> (index into route_a.cu kK2), 0: general k2_rows
     int k13;                // K1/K3 instantiation (route_a.cu kK13), 0: general
 };
 

@@ -1120,6 +1120,9 @@ static const K2Shape kK2[] = {
     PA_K2(5, 4, 4),    // 5120
     PA_K2(8, 16, 3),   // 2048
     PA_K2(3, 4, 4),    // 3072
+    PA_K2(5, 5, 4),    // 6400 (round 2)
+    PA_K2(7, 7, 4),    // 12544 (round 2: next to the longest plans, where the blocked / split
+                       // block-length search meets it)
 };
 #undef PA_K2
 
