@@ -294,6 +294,14 @@ pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t *seed_host
                                uint32_t *out_host, uint64_t max_block_bits, uint64_t device_budget_bytes,
                                void *stream);
 
+/* The block shape pa_hash_blocked / pa_hash_blocked_host would use for (n, m, max_block_bits,
+ * device_budget_bytes) -- same arguments, same rules (Eq. (4)-(7)): nb key
+ * bits and mb rows per block (multiples of 32, nb + mb - 1 <= the limit) and the number of
+ * blocks ceil(m/mb) * ceil(n/nb).  Host-only planning (no device work); PA_ERR_NOMEM when the
+ * budget cannot hold the smallest block, PA_ERR_INVALID_ARG for m > n, m = 0 or NULL outputs. */
+pa_status pa_blocked_plan(uint64_t n, uint64_t m, uint64_t max_block_bits, uint64_t device_budget_bytes,
+                          uint64_t *nb, uint64_t *mb, uint64_t *blocks);
+
 /* pa_hash_blocked / pa_hash_blocked_host keep their block handle and staging buffers (one set per
  * process, reused by calls of the same block shape on the same device; calls are serialised)
  * because creating and freeing a multi-GB handle costs more than hashing a block.  This frees

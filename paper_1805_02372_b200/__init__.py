@@ -28,7 +28,7 @@ from ._lib import (PA_ARITH_AUTO, PA_ARITH_FP64, PA_ARITH_NTT32, PA_ARITH_NTT64,
                    pa_options_init, pa_plan, pa_profile_enable, pa_profile_read, pa_set_seed, pa_xor_fold, pa_residual, pa_status_string,
                    pa_version, pa_workspace_size, pa_create_ws, pa_hash_fresh_batch, pa_seed_from_paper_eq1,
                    pa_hash_host_batch, pa_xor_fold_peers, pa_peer_alloc, pa_peer_free, pa_peer_export,
-                   pa_peer_open, pa_peer_close, pa_hash_blocked_release)
+                   pa_peer_open, pa_peer_close, pa_hash_blocked_release, pa_blocked_plan)
 
 ROUTES = {"auto": PA_ROUTE_AUTO, "transform": PA_ROUTE_TRANSFORM, "bitpacked": PA_ROUTE_BITPACKED}
 

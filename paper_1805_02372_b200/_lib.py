@@ -37,7 +37,7 @@ EXPORTED = ["pa_options_init", "pa_create", "pa_create_ex", "pa_hash", "pa_hash_
             "pa_profile_read", "pa_plan", "pa_set_seed", "pa_xor_fold", "pa_hash_host_async", "pa_hash_blocked", "pa_hash_blocked_host",
             "pa_workspace_size", "pa_create_ws", "pa_hash_fresh_batch", "pa_seed_from_paper_eq1",
             "pa_hash_host_batch", "pa_xor_fold_peers", "pa_peer_alloc", "pa_peer_free", "pa_peer_export",
-            "pa_peer_open", "pa_peer_close", "pa_hash_blocked_release"]
+            "pa_peer_open", "pa_peer_close", "pa_hash_blocked_release", "pa_blocked_plan"]
 
 
 class PaError(RuntimeError):
@@ -113,6 +113,8 @@ _sig = {
     "pa_peer_open": (_st, [ctypes.POINTER(pa_peer_handle), ctypes.POINTER(_p)]),
     "pa_peer_close": (_st, [_p]),
     "pa_hash_blocked_release": (None, []),
+    "pa_blocked_plan": (_st, [_u64, _u64, _u64, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                              ctypes.POINTER(_u64)]),
     "pa_profile_read": (_st, [_H, ctypes.POINTER(pa_kernel_time), ctypes.c_uint32,
                               ctypes.POINTER(ctypes.c_uint32)]),
 }
@@ -302,6 +304,14 @@ def pa_peer_open(handle: bytes) -> int:
 
 def pa_peer_close(ptr: int) -> None:
     _check(_lib.pa_peer_close(ptr))
+
+
+def pa_blocked_plan(n: int, m: int, max_block_bits: int = 0, device_budget_bytes: int = 0) -> dict:
+    """The block shape pa_hash_blocked(_host) would use: {"nb", "mb", "blocks"} (host-only)."""
+    nb, mb, blocks = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_lib.pa_blocked_plan(n, m, max_block_bits, device_budget_bytes, ctypes.byref(nb), ctypes.byref(mb),
+                                ctypes.byref(blocks)))
+    return {"nb": nb.value, "mb": mb.value, "blocks": blocks.value}
 
 
 def pa_hash_blocked_release() -> None:

@@ -109,12 +109,11 @@ static struct BlockCache {
     int stage_device = -1;
 } g_bcache;
 
-// The block loop shared by the device- and host-resident entry points.
-static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits, const uint32_t *key_bits,
-                              uint32_t *out_bits, uint64_t lim, bool host, uint64_t budget, cudaStream_t s,
-                              const char *who)
+// The block shape for a limit and an optional device budget: the largest limit <= lim whose
+// block handle + staging fit the budget (when one is given), then block_shape.
+static pa_status blocked_shape_for(uint64_t n, uint64_t m, uint64_t lim, uint64_t budget, const char *who,
+                                   uint64_t *nb_out, uint64_t *mb_out)
 {
-    // largest limit within the device budget (handle + staging), when one is given
     auto device_bytes = [&](uint64_t L, uint64_t *nb, uint64_t *mb) -> uint64_t {
         if (!block_shape(n, m, L, nb, mb)) return ~0ull;
         pa_options o;
@@ -146,6 +145,18 @@ static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits,
         set_error("%s: max_block_bits = %llu is too small for 32-bit aligned blocks", who, (unsigned long long)lim);
         return PA_ERR_INVALID_ARG;
     }
+    *nb_out = nb;
+    *mb_out = mb;
+    return PA_OK;
+}
+
+// The block loop shared by the device- and host-resident entry points.
+static pa_status blocked_impl(uint64_t n, uint64_t m, const uint32_t *seed_bits, const uint32_t *key_bits,
+                              uint32_t *out_bits, uint64_t lim, bool host, uint64_t budget, cudaStream_t s,
+                              const char *who)
+{
+    uint64_t nb = 0, mb = 0;
+    if (pa_status st0 = blocked_shape_for(n, m, lim, budget, who, &nb, &mb); st0 != PA_OK) return st0;
     const uint64_t KW = (n + 31) / 32, SW = (n + m - 1 + 31) / 32, OW = (m + 31) / 32;
     const uint64_t off = n % 32;
     Staging st;
@@ -430,6 +441,25 @@ extern "C" pa_status pa_hash_blocked_host(uint64_t n, uint64_t m, const uint32_t
     }
     return blocked_impl(n, m, seed_host, key_host, out_host, lim, true, device_budget_bytes, (cudaStream_t)stream,
                         "pa_hash_blocked_host");
+}
+
+extern "C" pa_status pa_blocked_plan(uint64_t n, uint64_t m, uint64_t max_block_bits, uint64_t device_budget_bytes,
+                                     uint64_t *nb, uint64_t *mb, uint64_t *blocks)
+{
+    if (n == 0 || m == 0 || m > n || !nb || !mb || !blocks) {
+        set_error("pa_blocked_plan: need 1 <= m <= n and non-NULL outputs (n = %llu, m = %llu)",
+                  (unsigned long long)n, (unsigned long long)m);
+        return PA_ERR_INVALID_ARG;
+    }
+    const uint64_t lim = max_block_bits ? max_block_bits : default_limit(n, m);
+    if (lim < 64) {
+        set_error("pa_blocked_plan: max_block_bits = %llu is too small (>= 64)", (unsigned long long)lim);
+        return PA_ERR_INVALID_ARG;
+    }
+    pa_status st = blocked_shape_for(n, m, lim, device_budget_bytes, "pa_blocked_plan", nb, mb);
+    if (st != PA_OK) return st;
+    *blocks = ((m + *mb - 1) / *mb) * ((n + *nb - 1) / *nb);
+    return PA_OK;
 }
 
 extern "C" void pa_hash_blocked_release(void)
