@@ -796,6 +796,58 @@ def test_key_and_output_must_not_overlap():
 
 
 
+def _path_cases(count=24, seed=4242):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(count):
+        kind = ["fresh", "batch", "blocked", "blocked_host"][i % 4]
+        n = int(np.exp(rng.uniform(np.log(2e4), np.log(3e6))))
+        m = max(1, int(n * rng.uniform(0.02, 0.9)))
+        cases.append((kind, n, m, int(rng.integers(2, 6)), int(rng.integers(0, 3))))
+    return cases
+
+
+@pytest.mark.parametrize("kind,n,m,count,variant", _path_cases())
+def test_random_paths_fuzz(kind, n, m, count, variant):
+    """Seeded random shapes through the batched, fresh-seed (fused K2 + the handle's last seed
+    afterwards) and blocked (device / host-streamed, random block limits and budgets) paths;
+    sampled rows (both ends + random) against the oracle."""
+    L = n + m - 1
+    rows = sample_rows(m, n % 1000, k=96)
+    if kind in ("fresh", "batch"):
+        seeds = [syn.random_bits(syn.seed_stream(300 + k), L) for k in range(count)]
+        keys = [syn.random_bits(syn.key_stream(300, k), n) for k in range(count)]
+        kt = torch.stack([to_dev(k) for k in keys])
+        with pa.Hasher(n, m, to_dev(seeds[0]), route="transform") as h:
+            if kind == "fresh":
+                outs = h.hash_fresh_batch(torch.stack([to_dev(s) for s in seeds]), kt)
+                after = from_dev(h.hash(to_dev(keys[0])), m)
+            else:
+                outs = h.hash_batch(kt)
+            torch.cuda.synchronize()
+        for k in range(count):
+            sk = seeds[k] if kind == "fresh" else seeds[0]
+            assert np.array_equal(from_dev(outs[k], m)[rows], oracle.toeplitz_rows(n, m, sk, keys[k], rows)), k
+        if kind == "fresh":
+            assert np.array_equal(after[rows], oracle.toeplitz_rows(n, m, seeds[-1], keys[0], rows))
+        return
+    sw = syn.random_bits(syn.seed_stream(301), L)
+    kw = syn.random_bits(syn.key_stream(301, 0), n)
+    lim = [0, max(n // 3 + m, 4096), max(m + 64, (n + m) // 5)][variant]
+    if kind == "blocked":
+        sd, kd = to_dev(sw), to_dev(kw)
+        out = torch.zeros(pa.words32(m) + 4, dtype=torch.int32, device=DEV)
+        pa.pa_hash_blocked(n, m, sd.data_ptr(), kd.data_ptr(), out.data_ptr(), lim, 0)
+        got = from_dev(out, m)
+    else:
+        sh = torch.from_numpy(np.ascontiguousarray(sw).view(np.int32).copy()).pin_memory()
+        kh = torch.from_numpy(np.ascontiguousarray(kw).view(np.int32).copy()).pin_memory()
+        oh = torch.zeros(pa.words32(m), dtype=torch.int32).pin_memory()
+        pa.pa_hash_blocked_host(n, m, sh.data_ptr(), kh.data_ptr(), oh.data_ptr(), lim, [0, 256 << 20, 1 << 30][variant], 0)
+        got = oracle.unpack(oh.numpy().view(np.uint32), m)
+    assert np.array_equal(got[rows], oracle.toeplitz_rows(n, m, sw, kw, rows))
+
+
 def _fuzz_shapes(count=48, seed=1805):
     rng = np.random.default_rng(seed)
     shapes = []
