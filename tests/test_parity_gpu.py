@@ -570,14 +570,16 @@ def test_hash_fresh_batch_per_key_seeds(route, maxlen, count):
     assert np.array_equal(after, oracle.unpack(oracle.toeplitz_words(n, m, seeds[-1], probe), m))
 
 
-@pytest.mark.parametrize("n,m,count", [(250_007, 62_000, 3), (20_000_003, 4_000_000, 2), (50_000_017, 5_000_001, 2)])
+@pytest.mark.parametrize("n,m,count", [(250_007, 62_000, 3), (20_000_003, 4_000_000, 2), (50_000_017, 5_000_001, 2),
+                                     (1_048_576, 104_857, 70)])
 def test_hash_fresh_batch_fused_k2_shapes(n, m, count):
     """The fresh-seed K2 (each seed's forward half in the hash's K2, its spectrum row held in
     TMEM) on the row shapes 2048 = [8, 16, 16] (two CTAs per SM, 256 TMEM columns each),
     6144 = [3, 8, 16, 16] and 10240 = [5, 8, 16, 16] (one CTA per SM, 512 columns, two last-stage
     butterflies per thread): every key against its own seed, and the handle afterwards holds the
-    last seed (the spectrum row the last key's CTAs wrote).  Full outputs at the small shape,
-    sampled rows (both ends + random) at the large ones."""
+    last seed (the spectrum row the last key's CTAs wrote; 70 keys: two chunks, each chunk's
+    last key rewrites it).  Full outputs at the small shape, sampled rows (both ends + random) at
+    the large ones."""
     L = n + m - 1
     seeds = [syn.random_bits(syn.seed_stream(150 + k), L) for k in range(count)]
     keys = [syn.random_bits(syn.key_stream(150, k), n) for k in range(count)]
